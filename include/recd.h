@@ -1,0 +1,176 @@
+/*
+ * librecd -- C ABI of the B200-native IKJT training hot path.
+ *
+ * Every entry point replaces one function of the reference's Python API
+ * (`/root/reference/pkg/src/sessiondedup/`), batched over all feature keys of a
+ * step so that one call launches one kernel per phase for every key:
+ *
+ *   recd_dedup                 <- tensors.build_ikjt            (tensors.py:269-308)
+ *                                 (one IKJT per dedup group, reader.convert, reader.py:160-175)
+ *   recd_pool_fwd              <- trainer_sim.embedding_lookup + pool + b[inv]
+ *                                 (trainer_sim.py:308-344, 539-561), fused: the
+ *                                 [N_u, D] activations are never materialised
+ *   recd_embedding_lookup      <- trainer_sim.embedding_lookup  (trainer_sim.py:308-321)
+ *   recd_pool_dense            <- trainer_sim.pool              (trainer_sim.py:324-344)
+ *   recd_pool_bwd              <- (absent in the reference) segment-reduce
+ *                                 onto unique rows + deterministic sorted scatter-add
+ *                                 (+ fused SGD) into the tables
+ *   recd_jagged_index_select_* <- tensors.jagged_index_select   (tensors.py:363-390)
+ *                                 and ikjt_to_kjt (tensors.py:393-399)
+ *   recd_slice_renumber        <- trainer_sim.slice_ikjt_rows   (trainer_sim.py:394-413)
+ *
+ * Conventions
+ *   - Jagged features use the reference layout: int64 values[N] and one int64
+ *     offset per row (no trailing total; the last row runs to N).
+ *   - Pointer arguments documented "device" point to GPU memory owned by the
+ *     caller; "host [K]" arrays are read during the call only.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t); they never allocate
+ *     and never synchronise, so a whole step can be captured in a CUDA graph.
+ *   - Counts only known after a kernel ran (U unique rows, N_u unique values)
+ *     stay on the device: `counts` arrays are int64[2F] with counts[f] = rows of
+ *     feature f (U of its group) and counts[F+f] = values of feature f.
+ *   - Return value: RECD_OK or an RECD_ERR_* code (argument / launch errors).
+ *     Data-dependent errors the reference raises (out-of-range IDs/indices) are
+ *     reported through a device int64 slot holding the first offending
+ *     position, which the Python shim turns into the reference's exception.
+ */
+#ifndef RECD_H_
+#define RECD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* recd_stream_t; /* cudaStream_t */
+
+enum {
+  RECD_OK = 0,
+  RECD_ERR_ARG = 1,
+  RECD_ERR_CUDA = 2,
+  RECD_ERR_SCRATCH = 3,
+  RECD_ERR_UNSUPPORTED = 4
+};
+
+enum { RECD_POOL_SUM = 0, RECD_POOL_AVG = 1, RECD_POOL_MAX = 2 };
+
+/* Value of an error slot when no error occurred. */
+#define RECD_NO_ERROR ((int64_t)0x7f7f7f7f7f7f7f7fLL)
+
+int recd_version(void);
+/* Human-readable description of the last non-OK return on this thread. */
+const char* recd_last_error(void);
+/* Kernels enqueued by this library since load (host counter). */
+int64_t recd_launch_count(void);
+/* Test hook: AND-mask applied to the 64-bit row hash (forces collisions so
+ * the exact fallback path is exercised).  ~0 restores the default. */
+void recd_debug_set_hash_mask(uint64_t mask);
+
+/* ---------------------------------------------------------------- dedup --
+ * KJT -> IKJT for `num_groups` feature groups of one batch of B rows.
+ * Rows i, j of a group merge iff every feature list in the group is equal
+ * (lengths included); unique rows are numbered in first-occurrence order and
+ * the unique lists are copied in that order -- bit-identical to build_ikjt.
+ *   group_sizes  host [G]       features per group (sum = F, F <= 64 per call)
+ *   values       host [F]       device int64[num_values[f]]
+ *   offsets      host [F]       device int64[B]
+ *   num_values   host [F]
+ *   inverse_out  host [G]       device int64[B]
+ *   uoffsets_out host [F]       device int64[B]           (first U valid)
+ *   uvalues_out  host [F]       device int64[num_values[f]] (first N_u valid)
+ *   counts_out   device int64[2F]
+ */
+size_t recd_dedup_scratch_bytes(int32_t num_groups, int32_t num_features, int64_t batch_size);
+int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+               const int64_t* const* values, const int64_t* const* offsets,
+               const int64_t* num_values, int64_t* const* inverse_out,
+               int64_t* const* uoffsets_out, int64_t* const* uvalues_out, int64_t* counts_out,
+               void* scratch, size_t scratch_bytes, recd_stream_t stream);
+
+/* ------------------------------------------------------------- pool fwd --
+ * For every feature f: pooled[u] = pool_{v in row u} tables[f][v] over the
+ * unique rows (sum / avg / max, empty row -> 0; the sum follows numpy's
+ * reduceat order a[0] + pairwise(a[1:]) so it is bit-identical to `pool`),
+ * then out[i] = pooled[inverse[f][i]] for i < B (skipped where out[f] or
+ * inverse[f] is NULL; with inverse[f] NULL and out[f] set, out = pooled).
+ *   tables      host [F] device float[table_rows[f] x dim]
+ *   uvalues/uoffsets host [F] device (jagged rows of feature f)
+ *   counts      device int64[2F]
+ *   pooled_out  host [F] device float[U_cap x dim]  (may alias out[f] when inverse[f] is NULL)
+ *   err         device int64[1]: first bad ID as (f << 40) | position, or RECD_NO_ERROR
+ */
+int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                  const float* const* tables, const int64_t* table_rows,
+                  const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                  const int64_t* counts, const int64_t* const* inverse,
+                  float* const* pooled_out, float* const* out, int64_t* err,
+                  recd_stream_t stream);
+
+/* weights[values[j]] for j < n (materialised lookup, reference API). */
+int recd_embedding_lookup(const float* table, int64_t table_rows, int32_t dim,
+                          const int64_t* values, int64_t n, float* out, int64_t* err,
+                          recd_stream_t stream);
+
+/* pool(activations, offsets, op) over materialised activations [n_values x dim]. */
+int recd_pool_dense(const float* acts, int64_t n_values, int32_t dim, const int64_t* offsets,
+                    int64_t n_rows, int32_t mode, float* out, recd_stream_t stream);
+
+/* ------------------------------------------------------------- pool bwd --
+ * grad_u[u] = sum_{i: inverse[i]=u} grad_out[i]  (ascending i; /len for avg),
+ * then for every distinct ID v of the feature, in ascending v:
+ *   g[v] = sum over occurrences (u, p) with uvalues[u][p] == v, ascending
+ *          (u, p), of grad_u[u];
+ * apply_sgd = 1: tables[f][v] -= fp32(lr * g[v]) in place (no FMA);
+ * apply_sgd = 0: grad_ids_out[f][k], grad_rows_out[f][k] = k-th distinct ID
+ *                and its gradient, grad_counts_out[f] = number of IDs.
+ * Features sharing an inverse pointer share one inverse CSR.  Only sum/avg.
+ *   value_caps  host [F] capacity of uvalues[f] (worst-case N_u)
+ */
+size_t recd_pool_bwd_scratch_bytes(int32_t num_features, int64_t batch_size, int32_t dim,
+                                   const int64_t* value_caps);
+int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                  float* const* tables, const int64_t* table_rows,
+                  const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                  const int64_t* value_caps, const int64_t* counts,
+                  const int64_t* const* inverse, const float* const* grad_out, float lr,
+                  int32_t apply_sgd, int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                  int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                  recd_stream_t stream);
+
+/* --------------------------------------------------- jagged index select --
+ * Output row k of feature f = input row indices[k] (same indices for every
+ * feature, as ikjt_to_kjt does with inverse_lookup).
+ * plan: out_offsets[f] (int64[n_idx]) and totals_out[f] (device) = output
+ *       value counts; err (device int64[1]) = first position p with
+ *       indices[p] outside [0, num_rows), else RECD_NO_ERROR.
+ * copy: out_values[f] (int64[total_f]).
+ */
+size_t recd_jagged_scratch_bytes(int32_t num_features, int64_t num_indices);
+int recd_jagged_index_select_plan(int32_t num_features, const int64_t* const* offsets,
+                                  int64_t num_rows, const int64_t* num_values,
+                                  const int64_t* indices, int64_t num_indices,
+                                  int64_t* const* out_offsets, int64_t* totals_out, int64_t* err,
+                                  void* scratch, size_t scratch_bytes, recd_stream_t stream);
+int recd_jagged_index_select_copy(int32_t num_features, const int64_t* const* values,
+                                  const int64_t* const* offsets, int64_t num_rows,
+                                  const int64_t* num_values, const int64_t* indices,
+                                  int64_t num_indices, const int64_t* const* out_offsets,
+                                  int64_t* const* out_values, recd_stream_t stream);
+
+/* ------------------------------------------------------- slice renumber --
+ * DP slice of an IKJT without re-hashing: for rows [start, stop) of
+ * `inverse` (values in [0, num_unique)), new_inverse = first-occurrence
+ * renumbering and order_out[k] = old unique row of new unique row k;
+ * count_out (device int64[1]) = number of surviving unique rows.
+ */
+size_t recd_slice_scratch_bytes(int64_t num_unique, int64_t num_rows);
+int recd_slice_renumber(const int64_t* inverse, int64_t start, int64_t stop, int64_t num_unique,
+                        int64_t* new_inverse_out, int64_t* order_out, int64_t* count_out,
+                        void* scratch, size_t scratch_bytes, recd_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RECD_H_ */

@@ -1,0 +1,143 @@
+"""ctypes binding of librecd.so (the C ABI declared in include/recd.h).
+
+The library is the product; this module only marshals torch CUDA tensors into
+raw device pointers and the current CUDA stream.  There is no CPU fallback:
+if the shared library is missing or the tensors are not on a CUDA device,
+every op raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import torch
+
+_LIB_PATH = Path(__file__).resolve().parent / "librecd.so"
+_lib = None
+
+RECD_OK = 0
+RECD_NO_ERROR = 0x7F7F7F7F7F7F7F7F
+POOL_MODES = {"sum": 0, "avg": 1, "mean": 1, "max": 2}
+_ERRORS = {1: "invalid argument", 2: "CUDA error", 3: "scratch buffer too small",
+           4: "unsupported configuration"}
+
+_vp = C.c_void_p
+_i32 = C.c_int32
+_i64 = C.c_int64
+_sz = C.c_size_t
+_f32 = C.c_float
+_pp = C.POINTER(C.c_void_p)
+_p64 = C.POINTER(C.c_int64)
+_p32 = C.POINTER(C.c_int32)
+
+_SIGS = {
+    "recd_version": (_i32, []),
+    "recd_last_error": (C.c_char_p, []),
+    "recd_launch_count": (_i64, []),
+    "recd_debug_set_hash_mask": (None, [C.c_uint64]),
+    "recd_dedup_scratch_bytes": (_sz, [_i32, _i32, _i64]),
+    "recd_dedup": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _pp, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_pool_fwd": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _pp, _pp, _pp,
+                             _vp, _vp]),
+    "recd_embedding_lookup": (_i32, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _vp]),
+    "recd_pool_dense": (_i32, [_vp, _i64, _i32, _vp, _i64, _i32, _vp, _vp]),
+    "recd_pool_bwd_scratch_bytes": (_sz, [_i32, _i64, _i32, _p64]),
+    "recd_pool_bwd": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _pp,
+                             _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_jagged_scratch_bytes": (_sz, [_i32, _i64]),
+    "recd_jagged_index_select_plan": (_i32, [_i32, _pp, _i64, _p64, _vp, _i64, _pp, _vp, _vp,
+                                             _vp, _sz, _vp]),
+    "recd_jagged_index_select_copy": (_i32, [_i32, _pp, _pp, _i64, _p64, _vp, _i64, _pp, _pp,
+                                             _vp]),
+    "recd_slice_scratch_bytes": (_sz, [_i64, _i64]),
+    "recd_slice_renumber": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+}
+
+EXPORTS = tuple(_SIGS)
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load librecd.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else _LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: build the CUDA extension with "
+            "`python -m paper_2211_05239_b200.build` (there is no CPU fallback)")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != RECD_OK:
+        detail = load().recd_last_error().decode() or _ERRORS.get(rc, "")
+        raise RuntimeError(f"{what} failed: {_ERRORS.get(rc, rc)} {detail}".strip())
+
+
+def require_cuda(*tensors: torch.Tensor) -> None:
+    for t in tensors:
+        if t is not None and not t.is_cuda:
+            raise ValueError("the IKJT hot path runs on CUDA tensors only (no CPU fallback)")
+
+
+def ptrs(ts) -> C.Array:
+    arr = (C.c_void_p * max(1, len(ts)))()
+    for i, t in enumerate(ts):
+        arr[i] = None if t is None else (t if isinstance(t, int) else t.data_ptr())
+    return arr
+
+
+def i64s(xs) -> C.Array:
+    arr = (C.c_int64 * max(1, len(xs)))()
+    for i, x in enumerate(xs):
+        arr[i] = int(x)
+    return arr
+
+
+def i32s(xs) -> C.Array:
+    arr = (C.c_int32 * max(1, len(xs)))()
+    for i, x in enumerate(xs):
+        arr[i] = int(x)
+    return arr
+
+
+def stream_ptr(device: torch.device | None = None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class Workspace:
+    """Grow-only device scratch arena per device (the C ABI never allocates)."""
+
+    _bufs: dict = {}
+
+    @classmethod
+    def get(cls, nbytes: int, device: torch.device, tag: str = "default") -> torch.Tensor:
+        key = (str(device), tag)
+        buf = cls._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            cls._bufs[key] = buf
+        return buf
+
+
+def launch_count() -> int:
+    return int(load().recd_launch_count())
+
+
+def set_hash_mask(mask: int) -> None:
+    """Test hook: weaken the row hash to force collisions (0 or ~0 restores)."""
+    load().recd_debug_set_hash_mask(C.c_uint64(mask & 0xFFFFFFFFFFFFFFFF))

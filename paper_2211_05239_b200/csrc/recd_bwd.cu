@@ -1,0 +1,536 @@
+// Backward of the deduplicated pooled lookup + fused SGD (sm_100a).
+//
+// The reference has no backward (SPEC.md:13 puts training out of scope);
+// the definition implemented here is the one in oracle/embedding.py:
+//   grad_u[u]  = sum_{i: inv[i] = u} grad_out[i], fp32 from +0.0 in ascending i
+//                (avg: divided by fp32(len_u));
+//   g[v]       = sum over occurrences of ID v in ascending (feature, u, pos)
+//                order of grad_u[u] -- a deterministic sorted scatter-add;
+//   SGD        : W[v] -= fp32(lr * g[v]) (no FMA contraction).
+// Steps (one launch per phase for every feature of the step):
+//   1 inverse CSR  : stable radix sort of (inv[i], i) per group  -> rows of u
+//   2 k_grad_u     : worker per unique row, ordered segment reduce
+//   3 k_occ        : (ID, feature*B + u) pairs of every unique value, laid out
+//                    per table (features sharing a table are concatenated)
+//   4 radix sort   : stable by ID within each table segment
+//   5 k_scatter    : worker per 256-position chunk of the sorted pairs; each run
+//                    of equal IDs is reduced in order, then RMW'd into the table
+//                    (or emitted as a sparse gradient row).
+#include <algorithm>
+#include <map>
+#include <vector>
+
+#include "recd_prims.cuh"
+#include "recd_slice.cuh"
+
+namespace recd {
+
+constexpr int RC = 256;  // sorted positions per scatter work item
+
+struct BwdParams {
+  int F;
+  int D;
+  int mode;
+  int64_t B;
+  int apply_sgd;
+  float lr;
+  int nis;  // inverse segments
+  int nts;  // table segments
+  // per feature
+  const int64_t* uvalues[RECD_MAX_FEAT];
+  const int64_t* uoffsets[RECD_MAX_FEAT];
+  const float* grad_out[RECD_MAX_FEAT];
+  int feat_is[RECD_MAX_FEAT];  // inverse segment or -1 (identity)
+  int feat_ts[RECD_MAX_FEAT];  // table segment
+  // per inverse segment
+  const int64_t* inverse[RECD_MAX_FEAT];
+  int is_feat[RECD_MAX_FEAT];  // a feature of the segment (for U)
+  // per table segment
+  float* table[RECD_MAX_FEAT];
+  int64_t ts_base[RECD_MAX_FEAT];    // element base in the occurrence arrays
+  int64_t ts_chunk0[RECD_MAX_FEAT];  // first scatter chunk
+  int64_t* grad_ids[RECD_MAX_FEAT];
+  float* grad_rows[RECD_MAX_FEAT];
+  int64_t* grad_count[RECD_MAX_FEAT];
+  int64_t total_rc_chunks;
+  const int64_t* counts;  // [2*Ftot] device, offset to this call's f0
+  int64_t Ftot;
+  // scratch
+  int64_t* feat_base;     // [F] device: offset of feature f inside its table segment
+  int64_t* seg_count;     // [nts] device
+  int64_t* is_count;      // [nis] device (= B)
+  uint32_t* inv_keys;     // [nis][B] sorted
+  uint32_t* inv_rows;     // [nis][B]
+  int32_t* csr_start;     // [nis][B + 1]
+  float* grad_u;          // [F][B][D]
+  uint32_t* occ_keys;     // sorted occurrence IDs
+  uint32_t* occ_vals;     // f * B + u
+  int64_t* run_part;      // [total_rc_chunks] exclusive run counts (grad-output mode)
+};
+
+__global__ void k_bwd_setup(const __grid_constant__ BwdParams p) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int s = 0; s < p.nts; ++s) p.seg_count[s] = 0;
+  for (int f = 0; f < p.F; ++f) {
+    const int s = p.feat_ts[f];
+    p.feat_base[f] = p.seg_count[s];
+    p.seg_count[s] += p.counts[p.Ftot + f];
+  }
+  for (int s = 0; s < p.nis; ++s) p.is_count[s] = p.B;
+}
+
+// keys = inverse value, vals = row: sorted by key -> CSR of each unique row
+__global__ void k_inv_pairs(const __grid_constant__ BwdParams p, uint32_t* keys, uint32_t* vals) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)p.nis * p.B) return;
+  const int s = (int)(idx / p.B);
+  const int64_t i = idx - (int64_t)s * p.B;
+  keys[idx] = (uint32_t)p.inverse[s][i];
+  vals[idx] = (uint32_t)i;
+}
+
+__global__ void k_csr_bounds(const __grid_constant__ BwdParams p) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)p.nis * p.B) return;
+  const int s = (int)(idx / p.B);
+  const int64_t j = idx - (int64_t)s * p.B;
+  const uint32_t* k = p.inv_keys + (int64_t)s * p.B;
+  int32_t* start = p.csr_start + (int64_t)s * (p.B + 1);
+  const uint32_t u = k[j];
+  if (j == 0 || k[j - 1] != u) start[u] = (int32_t)j;
+  if (j == p.B - 1) start[u + 1] = (int32_t)p.B;
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) k_grad_u(const __grid_constant__ BwdParams p) {
+  __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int f = 0; f < p.F; ++f) {
+      s_pref[f] = acc;
+      acc += p.counts[f];
+    }
+    s_pref[p.F] = acc;
+  }
+  __syncthreads();
+  const int64_t total = s_pref[p.F];
+  const int sl = threadIdx.x % S::LPR;
+  const int64_t nworkers = (int64_t)gridDim.x * blockDim.x / S::LPR;
+  constexpr int N = S::N;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::LPR; w < total;
+       w += nworkers) {
+    const int f = find_seg(s_pref, p.F, w);
+    const int64_t u = w - s_pref[f];
+    const float* G = p.grad_out[f];
+    const int is = p.feat_is[f];
+    float acc[N];
+    if (is < 0) {
+      S::load(G + u * p.D, sl, p.D, acc);
+    } else {
+      const int32_t* start = p.csr_start + (int64_t)is * (p.B + 1);
+      const uint32_t* rows = p.inv_rows + (int64_t)is * p.B;
+      const int64_t a = start[u], e = start[u + 1];
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc[k] = 0.0f;
+      float x[8][N];
+      for (int64_t j = a; j < e; j += 8) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (j + t < e) S::load(G + (int64_t)rows[j + t] * p.D, sl, p.D, x[t]);
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (j + t < e) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) acc[k] = __fadd_rn(acc[k], x[t][k]);
+          }
+      }
+    }
+    if (p.mode == RECD_POOL_AVG) {
+      const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
+      const int64_t* uo = p.uoffsets[f];
+      const int64_t len = ((u + 1 < U) ? uo[u + 1] : NV) - uo[u];
+      if (len > 0) {
+        const float fl = (float)len;
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc[k] = __fdiv_rn(acc[k], fl);
+      }
+    }
+    S::store(p.grad_u + ((int64_t)f * p.B + u) * p.D, sl, p.D, acc);
+  }
+}
+
+// occurrence pairs: warp per unique row writes (ID, f*B+u) for its values
+__global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p, uint32_t* keys,
+                                             uint32_t* vals) {
+  __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int f = 0; f < p.F; ++f) {
+      s_pref[f] = acc;
+      acc += p.counts[f];
+    }
+    s_pref[p.F] = acc;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t total = s_pref[p.F];
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
+       w += nwarps) {
+    const int f = find_seg(s_pref, p.F, w);
+    const int64_t u = w - s_pref[f];
+    const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
+    const int64_t* uo = p.uoffsets[f];
+    const int64_t a = uo[u], e = (u + 1 < U) ? uo[u + 1] : NV;
+    const int64_t dst = p.ts_base[p.feat_ts[f]] + p.feat_base[f];
+    const uint32_t tag = (uint32_t)((int64_t)f * p.B + u);
+    const int64_t* vals_f = p.uvalues[f];
+    for (int64_t j = a + lane; j < e; j += 32) {
+      keys[dst + j] = (uint32_t)vals_f[j];
+      vals[dst + j] = tag;
+    }
+  }
+}
+
+__device__ __forceinline__ int rc_seg(const BwdParams& p, int64_t chunk) {
+  int lo = 0, hi = p.nts - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (p.ts_chunk0[mid] <= chunk) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// number of run starts per RC chunk (grad-output mode)
+__global__ void __launch_bounds__(RC) k_run_count(const __grid_constant__ BwdParams p) {
+  const int64_t chunk = blockIdx.x;
+  const int s = rc_seg(p, chunk);
+  const int64_t n = p.seg_count[s];
+  const int64_t j = (chunk - p.ts_chunk0[s]) * RC + threadIdx.x;
+  const uint32_t* K = p.occ_keys + p.ts_base[s];
+  const int start = (j < n) && (j == 0 || K[j] != K[j - 1]);
+  const int cnt = __syncthreads_count(start);
+  if (threadIdx.x == 0) p.run_part[chunk] = cnt;
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) k_scatter(const __grid_constant__ BwdParams p) {
+  constexpr int N = S::N;
+  const int sl = threadIdx.x % S::LPR;
+  const int64_t nworkers = (int64_t)gridDim.x * blockDim.x / S::LPR;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::LPR;
+       w < p.total_rc_chunks; w += nworkers) {
+    const int s = rc_seg(p, w);
+    const int64_t n = p.seg_count[s];
+    const int64_t lo = (w - p.ts_chunk0[s]) * RC;
+    if (lo >= n) continue;
+    const int64_t hi = min(n, lo + (int64_t)RC);
+    const uint32_t* K = p.occ_keys + p.ts_base[s];
+    const uint32_t* V = p.occ_vals + p.ts_base[s];
+    int64_t j = lo;
+    if (j > 0)
+      while (j < hi && K[j] == K[j - 1]) ++j;
+    int64_t run_idx = p.apply_sgd ? 0 : p.run_part[w];
+    while (j < hi) {
+      const uint32_t id = K[j];
+      float acc[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc[k] = 0.0f;
+      int64_t k0 = j;
+      while (true) {
+        uint32_t ks[8], vs[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const bool ok = k0 + t < n;
+          ks[t] = ok ? K[k0 + t] : ~id;
+          vs[t] = ok ? V[k0 + t] : 0u;
+        }
+        int m = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (m == t && ks[t] == id) m = t + 1;
+        float x[8][N];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (t < m) S::load(p.grad_u + (int64_t)vs[t] * p.D, sl, p.D, x[t]);
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (t < m) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) acc[k] = __fadd_rn(acc[k], x[t][k]);
+          }
+        k0 += m;
+        if (m < 8) break;
+      }
+      if (p.apply_sgd) {
+        float* row = p.table[s] + (int64_t)id * p.D;
+        float wv[N];
+        S::load_rw(row, sl, p.D, wv);
+#pragma unroll
+        for (int k = 0; k < N; ++k) wv[k] = __fsub_rn(wv[k], __fmul_rn(p.lr, acc[k]));
+        S::store(row, sl, p.D, wv);
+      } else {
+        if (sl == 0) p.grad_ids[s][run_idx] = (int64_t)id;
+        S::store(p.grad_rows[s] + run_idx * p.D, sl, p.D, acc);
+        ++run_idx;
+      }
+      j = k0;
+    }
+  }
+}
+
+static int64_t bits_for(int64_t n) {
+  int b = 0;
+  while ((1ll << b) < n) ++b;
+  return b;
+}
+
+}  // namespace recd
+
+using namespace recd;
+
+namespace {
+
+struct Plan {
+  int F, nis, nts;
+  std::vector<int> feat_is, feat_ts, is_feat;
+  std::vector<const int64_t*> inverse;
+  std::vector<float*> table;
+  std::vector<int64_t> table_rows;  // max rows per table seg
+  std::vector<int64_t> ts_base, ts_cap, ts_chunk0;
+  int64_t occ_total, rc_chunks;
+};
+
+Plan make_plan(int F, const int64_t* const* inverse, float* const* tables, const int64_t* rows,
+               const int64_t* caps) {
+  Plan pl;
+  pl.F = F;
+  pl.feat_is.assign(F, -1);
+  pl.feat_ts.assign(F, -1);
+  std::map<const void*, int> is_map, ts_map;
+  for (int f = 0; f < F; ++f) {
+    const int64_t* inv = inverse ? inverse[f] : nullptr;
+    if (inv) {
+      auto it = is_map.find(inv);
+      if (it == is_map.end()) {
+        it = is_map.emplace(inv, (int)pl.inverse.size()).first;
+        pl.inverse.push_back(inv);
+        pl.is_feat.push_back(f);
+      }
+      pl.feat_is[f] = it->second;
+    }
+    auto jt = ts_map.find(tables[f]);
+    if (jt == ts_map.end()) {
+      jt = ts_map.emplace(tables[f], (int)pl.table.size()).first;
+      pl.table.push_back(tables[f]);
+      pl.table_rows.push_back(rows[f]);
+      pl.ts_cap.push_back(0);
+    }
+    pl.feat_ts[f] = jt->second;
+    pl.ts_cap[jt->second] += caps[f];
+    pl.table_rows[jt->second] = std::max(pl.table_rows[jt->second], rows[f]);
+  }
+  pl.nis = (int)pl.inverse.size();
+  pl.nts = (int)pl.table.size();
+  int64_t base = 0, chunk = 0;
+  for (int s = 0; s < pl.nts; ++s) {
+    pl.ts_base.push_back(base);
+    pl.ts_chunk0.push_back(chunk);
+    base += pl.ts_cap[s];
+    chunk += std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RC));
+  }
+  pl.occ_total = base;
+  pl.rc_chunks = chunk;
+  return pl;
+}
+
+struct BwdScratch {
+  int64_t *feat_base, *seg_count, *is_count, *run_part, *scan_part;
+  uint32_t *inv_k0, *inv_v0, *inv_k1, *inv_v1, *hist;
+  int32_t* csr_start;
+  float* grad_u;
+  uint32_t *occ_k0, *occ_v0, *occ_k1, *occ_v1;
+};
+
+size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdScratch* s) {
+  Arena a(base, cap);
+  s->feat_base = a.take<int64_t>(RECD_MAX_FEAT);
+  s->seg_count = a.take<int64_t>(RECD_MAX_FEAT);
+  s->is_count = a.take<int64_t>(RECD_MAX_FEAT);
+  s->run_part = a.take<int64_t>(pl.rc_chunks);
+  const size_t nib = (size_t)std::max(pl.nis, 1) * B;
+  s->inv_k0 = a.take<uint32_t>(nib);
+  s->inv_v0 = a.take<uint32_t>(nib);
+  s->inv_k1 = a.take<uint32_t>(nib);
+  s->inv_v1 = a.take<uint32_t>(nib);
+  s->csr_start = a.take<int32_t>((size_t)std::max(pl.nis, 1) * (B + 1));
+  s->grad_u = a.take<float>((size_t)pl.F * B * D);
+  s->occ_k0 = a.take<uint32_t>(pl.occ_total);
+  s->occ_v0 = a.take<uint32_t>(pl.occ_total);
+  s->occ_k1 = a.take<uint32_t>(pl.occ_total);
+  s->occ_v1 = a.take<uint32_t>(pl.occ_total);
+  // sort histograms: max of the inverse sort and the table sort
+  std::vector<SegDesc> segs;
+  for (int i = 0; i < pl.nis; ++i) segs.push_back({(int64_t)i * B, B, nullptr});
+  int64_t hw = segs.empty() ? 0 : sort_hist_words(segs.data(), (int)segs.size());
+  segs.clear();
+  for (int t = 0; t < pl.nts; ++t) segs.push_back({pl.ts_base[t], pl.ts_cap[t], nullptr});
+  hw = std::max(hw, sort_hist_words(segs.data(), (int)segs.size()));
+  s->hist = a.take<uint32_t>(std::max<int64_t>(hw, 256));
+  // run-count scan partials (one scan segment per table)
+  std::vector<ScanDesc> sd;
+  for (int t = 0; t < pl.nts; ++t) {
+    const int64_t nch = std::max<int64_t>(1, ceil_div(pl.ts_cap[t], RC));
+    sd.push_back({nullptr, nullptr, nch, nullptr, nullptr});
+  }
+  s->scan_part = a.take<int64_t>(std::max<int64_t>(scan_part_words(sd.data(), (int)sd.size()), 1));
+  return a.used;
+}
+
+}  // namespace
+
+extern "C" size_t recd_pool_bwd_scratch_bytes(int32_t num_features, int64_t batch_size,
+                                              int32_t dim, const int64_t* value_caps) {
+  if (num_features <= 0 || num_features > RECD_MAX_FEAT) return 0;
+  // worst case: every feature has its own inverse and its own table
+  std::vector<const int64_t*> inv(num_features);
+  std::vector<float*> tab(num_features);
+  std::vector<int64_t> rows(num_features, 1);
+  for (int f = 0; f < num_features; ++f) {
+    inv[f] = reinterpret_cast<const int64_t*>((uintptr_t)(f + 1) * 64);
+    tab[f] = reinterpret_cast<float*>((uintptr_t)(f + 1) * 64);
+  }
+  Plan pl = make_plan(num_features, inv.data(), tab.data(), rows.data(), value_caps);
+  BwdScratch s;
+  return carve_bwd(nullptr, 0, pl, batch_size, dim, &s);
+}
+
+extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                             float* const* tables, const int64_t* table_rows,
+                             const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                             const int64_t* value_caps, const int64_t* counts,
+                             const int64_t* const* inverse, const float* const* grad_out,
+                             float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
+                             float* const* grad_rows_out, int64_t* grad_counts_out,
+                             void* scratch, size_t scratch_bytes, recd_stream_t stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int F = num_features;
+  const int64_t B = batch_size;
+  if (F <= 0 || F > RECD_MAX_FEAT || B <= 0 || dim <= 0 || !counts) return RECD_ERR_ARG;
+  if (mode != RECD_POOL_SUM && mode != RECD_POOL_AVG) return RECD_ERR_UNSUPPORTED;
+  if ((int64_t)F * B >= (1ll << 32)) return RECD_ERR_UNSUPPORTED;
+  for (int f = 0; f < F; ++f) {
+    if (!tables[f] || !uoffsets[f] || !grad_out[f]) return RECD_ERR_ARG;
+    if (table_rows[f] <= 0 || table_rows[f] > (1ll << 32)) return RECD_ERR_UNSUPPORTED;
+  }
+  Plan pl = make_plan(F, inverse, const_cast<float**>(tables), table_rows, value_caps);
+  if (pl.occ_total >= (1ll << 32)) return RECD_ERR_UNSUPPORTED;
+  if (!apply_sgd && (!grad_ids_out || !grad_rows_out || !grad_counts_out)) return RECD_ERR_ARG;
+  BwdScratch sc;
+  if (carve_bwd(scratch, scratch_bytes, pl, B, dim, &sc) > scratch_bytes) return RECD_ERR_SCRATCH;
+
+  BwdParams p;
+  memset(&p, 0, sizeof(p));
+  p.F = F;
+  p.D = dim;
+  p.mode = mode;
+  p.B = B;
+  p.apply_sgd = apply_sgd;
+  p.lr = lr;
+  p.nis = pl.nis;
+  p.nts = pl.nts;
+  p.counts = counts;
+  p.Ftot = F;
+  for (int f = 0; f < F; ++f) {
+    p.uvalues[f] = uvalues[f];
+    p.uoffsets[f] = uoffsets[f];
+    p.grad_out[f] = grad_out[f];
+    p.feat_is[f] = pl.feat_is[f];
+    p.feat_ts[f] = pl.feat_ts[f];
+  }
+  for (int s = 0; s < pl.nis; ++s) {
+    p.inverse[s] = pl.inverse[s];
+    p.is_feat[s] = pl.is_feat[s];
+  }
+  int first_feat_of_ts[RECD_MAX_FEAT];
+  for (int s = 0; s < pl.nts; ++s) first_feat_of_ts[s] = -1;
+  for (int f = 0; f < F; ++f)
+    if (first_feat_of_ts[pl.feat_ts[f]] < 0) first_feat_of_ts[pl.feat_ts[f]] = f;
+  for (int s = 0; s < pl.nts; ++s) {
+    p.table[s] = pl.table[s];
+    p.ts_base[s] = pl.ts_base[s];
+    p.ts_chunk0[s] = pl.ts_chunk0[s];
+    if (!apply_sgd) {
+      const int f = first_feat_of_ts[s];
+      p.grad_ids[s] = grad_ids_out[f];
+      p.grad_rows[s] = grad_rows_out[f];
+      p.grad_count[s] = grad_counts_out + f;
+    }
+  }
+  p.total_rc_chunks = pl.rc_chunks;
+  p.feat_base = sc.feat_base;
+  p.seg_count = sc.seg_count;
+  p.is_count = sc.is_count;
+  p.csr_start = sc.csr_start;
+  p.grad_u = sc.grad_u;
+  p.run_part = sc.run_part;
+
+  k_bwd_setup<<<1, 32, 0, stream>>>(p);
+  note_launch();
+  if (!apply_sgd) RECD_CUDA_CHECK(cudaMemsetAsync(grad_counts_out, 0, sizeof(int64_t) * F, stream));
+
+  // 1. inverse CSR
+  if (pl.nis > 0) {
+    const int64_t n = (int64_t)pl.nis * B;
+    k_inv_pairs<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p, sc.inv_k0, sc.inv_v0);
+    note_launch();
+    std::vector<SegDesc> segs;
+    for (int s = 0; s < pl.nis; ++s) segs.push_back({(int64_t)s * B, B, sc.is_count + s});
+    bool alt = false;
+    int rc = seg_sort_pairs(segs.data(), pl.nis, (int)bits_for(B), sc.inv_k0, sc.inv_v0, sc.inv_k1,
+                            sc.inv_v1, sc.hist, &alt, stream);
+    if (rc != RECD_OK) return rc;
+    p.inv_keys = alt ? sc.inv_k1 : sc.inv_k0;
+    p.inv_rows = alt ? sc.inv_v1 : sc.inv_v0;
+    k_csr_bounds<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p);
+    note_launch();
+  }
+  // 2-5
+  int rc = RECD_DISPATCH_SLICE(dim, {
+    const int64_t per_block = 256 / S::LPR;
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(B * F, per_block), (int64_t)num_sms() * 8);
+    k_grad_u<S><<<grid, 256, 0, stream>>>(p);
+    k_occ<<<num_sms() * 4, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
+    note_launch(2);
+    std::vector<SegDesc> segs;
+    int64_t maxrows = 1;
+    for (int s = 0; s < pl.nts; ++s) {
+      segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
+      maxrows = std::max(maxrows, pl.table_rows[s]);
+    }
+    bool alt = false;
+    int r2 = seg_sort_pairs(segs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
+                            sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream);
+    if (r2 != RECD_OK) return r2;
+    p.occ_keys = alt ? sc.occ_k1 : sc.occ_k0;
+    p.occ_vals = alt ? sc.occ_v1 : sc.occ_v0;
+    if (!apply_sgd) {
+      k_run_count<<<(unsigned)pl.rc_chunks, RC, 0, stream>>>(p);
+      note_launch();
+      std::vector<ScanDesc> sd;
+      for (int s = 0; s < pl.nts; ++s) {
+        const int64_t nch = std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RC));
+        sd.push_back({sc.run_part + pl.ts_chunk0[s], sc.run_part + pl.ts_chunk0[s], nch, nullptr,
+                      p.grad_count[s]});
+      }
+      int r3 = seg_exclusive_scan(sd.data(), (int)sd.size(), sc.scan_part, stream);
+      if (r3 != RECD_OK) return r3;
+    }
+    const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks, per_block), (int64_t)num_sms() * 16);
+    k_scatter<S><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+    note_launch();
+  });
+  if (rc != RECD_OK) return rc;
+  RECD_LAUNCH_CHECK();
+  return RECD_OK;
+}

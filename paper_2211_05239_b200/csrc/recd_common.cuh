@@ -1,0 +1,144 @@
+// Shared device helpers for librecd (sm_100a).
+//
+// Layout conventions (mirror the reference's JaggedTensor, tensors.py:60-111):
+//   a jagged feature is values int64[N] + offsets int64[R], one offset per
+//   row, the last row running to N.  All counts that are only known after a
+//   kernel ran (U unique rows, N_u unique values) stay in device memory; the
+//   kernels that consume them read them there, so a whole training step can
+//   be enqueued (and graph-captured) without a host round trip.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/recd.h"
+
+#define RECD_MAX_FEAT 64
+#define RECD_WARP 32
+
+#define RECD_CUDA_CHECK(expr)                                   \
+  do {                                                          \
+    cudaError_t _e = (expr);                                    \
+    if (_e != cudaSuccess) return RECD_ERR_CUDA;                \
+  } while (0)
+
+#define RECD_LAUNCH_CHECK()                                     \
+  do {                                                          \
+    cudaError_t _e = cudaGetLastError();                        \
+    if (_e != cudaSuccess) return RECD_ERR_CUDA;                \
+  } while (0)
+
+namespace recd {
+
+// Number of kernels this library enqueued (host-side counter; reported by
+// bench.py as "gpu_launches").
+void note_launch(int n = 1);
+
+int num_sms();
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+__host__ __device__ inline uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// splitmix64 finalizer.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Position-dependent element hash; a row hash is the (mod 2^64) sum of its
+// element hashes plus one length term per feature, so any partition of the
+// row's values over threads yields the same row hash.
+__device__ __forceinline__ uint64_t elem_hash(int64_t v, int64_t pos, int f) {
+  return mix64((uint64_t)v ^ ((uint64_t)pos * 0x9E3779B97F4A7C15ull) ^
+               ((uint64_t)(f + 1) * 0xD1B54A32D192ED03ull));
+}
+__device__ __forceinline__ uint64_t len_hash(int64_t len, int f) {
+  return mix64(((uint64_t)len << 7) ^ ((uint64_t)(f + 7) * 0xA0761D6478BD642Full) ^ 0x5bd1e995ull);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Block-wide exclusive scan of one int64 per thread; returns the exclusive
+// prefix, writes the block total to *total.  `smem` needs 32 int64 slots.
+template <int NT>
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* smem, int64_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) smem[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = (lane < NT / 32) ? smem[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    smem[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  int64_t base = warp ? smem[warp - 1] : 0;
+  *total = smem[NT / 32 - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+// Block-wide inclusive max-scan of one int64 per thread.
+template <int NT>
+__device__ __forceinline__ int64_t block_inclusive_max(int64_t v, int64_t* smem, int64_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x = max(x, y);
+  }
+  if (lane == 31) smem[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = (lane < NT / 32) ? smem[lane] : INT64_MIN;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w = max(w, y);
+    }
+    smem[lane] = w;
+  }
+  __syncthreads();
+  int64_t r = warp ? max(x, smem[warp - 1]) : x;
+  *total = smem[NT / 32 - 1];
+  __syncthreads();
+  return r;
+}
+
+// Scratch arena carving helper (256-byte aligned sub-buffers).
+struct Arena {
+  char* base;
+  size_t cap;
+  size_t used;
+  __host__ Arena(void* p, size_t c) : base((char*)p), cap(c), used(0) {}
+  template <class T>
+  __host__ T* take(size_t n) {
+    size_t bytes = (n * sizeof(T) + 255) & ~size_t(255);
+    T* p = (T*)(base ? base + used : nullptr);
+    used += bytes;
+    return p;
+  }
+  __host__ bool ok() const { return used <= cap; }
+};
+
+}  // namespace recd
