@@ -10,6 +10,7 @@
  *   recd_pool_fwd              <- trainer_sim.embedding_lookup + pool + b[inv]
  *                                 (trainer_sim.py:308-344, 539-561), fused: the
  *                                 [N_u, D] activations are never materialised
+ *   recd_expand                <- the expansion b[inv] alone     (trainer_sim.py:558-561)
  *   recd_embedding_lookup      <- trainer_sim.embedding_lookup  (trainer_sim.py:308-321)
  *   recd_pool_dense            <- trainer_sim.pool              (trainer_sim.py:324-344)
  *   recd_pool_bwd              <- (absent in the reference) segment-reduce
@@ -107,6 +108,13 @@ int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t
                   const int64_t* counts, const int64_t* const* inverse,
                   float* const* pooled_out, float* const* out, int64_t* err,
                   recd_stream_t stream);
+
+/* Expansion only: out[f][i] = pooled[f][inverse[f][i]] (inverse[f] NULL =
+ * identity).  recd_pool_fwd with out = NULL followed by recd_expand equals one
+ * recd_pool_fwd with out set (the split lets callers time the two kernels). */
+int recd_expand(int32_t num_features, int64_t batch_size, int32_t dim,
+                const int64_t* const* inverse, const float* const* pooled, float* const* out,
+                recd_stream_t stream);
 
 /* weights[values[j]] for j < n (materialised lookup, reference API). */
 int recd_embedding_lookup(const float* table, int64_t table_rows, int32_t dim,

@@ -41,6 +41,7 @@ _SIGS = {
     "recd_dedup": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _pp, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_pool_fwd": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _pp, _pp, _pp,
                              _vp, _vp]),
+    "recd_expand": (_i32, [_i32, _i64, _i32, _pp, _pp, _pp, _vp]),
     "recd_embedding_lookup": (_i32, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _vp]),
     "recd_pool_dense": (_i32, [_vp, _i64, _i32, _vp, _i64, _i32, _vp, _vp]),
     "recd_pool_bwd_scratch_bytes": (_sz, [_i32, _i64, _i32, _p64]),

@@ -164,11 +164,16 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
                            (p.out[f] && (uintptr_t)p.out[f] % 16)))
         return RECD_ERR_ARG;
     }
+    bool any_expand = false;
+    for (int f = 0; f < p.F; ++f) any_expand |= (p.out[f] != nullptr && p.out[f] != p.pooled[f]);
     int rc = RECD_DISPATCH_SLICE(dim, {
       const unsigned grid = grid_for(batch_size * p.F, S::LPR);
       k_pool_fwd<S><<<grid, 256, 0, stream>>>(p);
-      k_expand<S><<<grid, 256, 0, stream>>>(p);
-      note_launch(2);
+      note_launch();
+      if (any_expand) {
+        k_expand<S><<<grid, 256, 0, stream>>>(p);
+        note_launch();
+      }
     });
     if (rc != RECD_OK) return rc;
     RECD_LAUNCH_CHECK();
@@ -206,5 +211,32 @@ extern "C" int recd_pool_dense(const float* acts, int64_t n_values, int32_t dim,
   });
   if (rc != RECD_OK) return rc;
   RECD_LAUNCH_CHECK();
+  return RECD_OK;
+}
+
+extern "C" int recd_expand(int32_t num_features, int64_t batch_size, int32_t dim,
+                           const int64_t* const* inverse, const float* const* pooled,
+                           float* const* out, recd_stream_t stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (num_features <= 0 || batch_size < 0 || dim <= 0 || !pooled || !out) return RECD_ERR_ARG;
+  for (int f0 = 0; f0 < num_features; f0 += RECD_MAX_FEAT) {
+    PoolParams p;
+    memset(&p, 0, sizeof(p));
+    p.F = std::min(RECD_MAX_FEAT, num_features - f0);
+    p.D = dim;
+    p.B = batch_size;
+    for (int f = 0; f < p.F; ++f) {
+      p.inverse[f] = inverse ? inverse[f0 + f] : nullptr;
+      p.pooled[f] = const_cast<float*>(pooled[f0 + f]);
+      p.out[f] = out[f0 + f];
+      if (!p.pooled[f] || !p.out[f]) return RECD_ERR_ARG;
+    }
+    int rc = RECD_DISPATCH_SLICE(dim, {
+      k_expand<S><<<grid_for(batch_size * p.F, S::LPR), 256, 0, stream>>>(p);
+      note_launch();
+    });
+    if (rc != RECD_OK) return rc;
+    RECD_LAUNCH_CHECK();
+  }
   return RECD_OK;
 }
