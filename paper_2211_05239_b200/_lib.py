@@ -14,7 +14,7 @@ from pathlib import Path
 
 import torch
 
-_LIB_PATH = Path(__file__).resolve().parent / "librecd.so"
+_LIB_PATH = Path(os.environ.get("RECD_LIB", Path(__file__).resolve().parent / "librecd.so"))
 _lib = None
 
 RECD_OK = 0

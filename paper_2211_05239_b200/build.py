@@ -42,15 +42,20 @@ def _stale(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OBJ.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None,
+          tag: str = "") -> Path:
+    """Compile csrc/*.cu and link librecd.so (or `out` for a tuning variant
+    built with extra -D `defines`, objects kept under build/obj<tag>)."""
+    obj_dir = OBJ.parent / f"obj{tag}" if tag else OBJ
+    lib = Path(out) if out else LIB
+    obj_dir.mkdir(parents=True, exist_ok=True)
     objs = []
     jobs = []
     for src in sources():
-        obj = OBJ / (src.stem + ".o")
+        obj = obj_dir / (src.stem + ".o")
         objs.append(obj)
         if force or _stale(obj, _deps(src)):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)
@@ -65,10 +70,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         for err in ex.map(run, jobs):
             if verbose and err:
                 print(err, file=sys.stderr)
-    if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
+    if force or jobs or _stale(lib, objs):
+        lib.parent.mkdir(parents=True, exist_ok=True)
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs)]
         run(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

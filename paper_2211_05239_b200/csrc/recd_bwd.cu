@@ -13,15 +13,23 @@
 //   3 k_occ        : (ID, feature*B + u) pairs of every unique value, laid out
 //                    per table (features sharing a table are concatenated)
 //   4 radix sort   : stable by ID within each table segment
-//   5 k_scatter    : worker per 256-position chunk of the sorted pairs; each run
-//                    of equal IDs is reduced in order, then RMW'd into the table
-//                    (or emitted as a sparse gradient row).
+//   5 k_scatter    : warp per (256-position chunk of the sorted pairs, column
+//                    block); it lists the runs of equal IDs starting in its chunk,
+//                    prefetches the table rows of 4 runs at a time, reduces each
+//                    run in order and RMWs the row (or emits a sparse gradient row).
 #include <algorithm>
 #include <map>
 #include <vector>
 
 #include "recd_prims.cuh"
 #include "recd_slice.cuh"
+
+#ifndef RECD_BWD_VW
+#define RECD_BWD_VW 4
+#endif
+#ifndef RECD_SCATTER_MINB
+#define RECD_SCATTER_MINB 3
+#endif
 
 namespace recd {
 
@@ -101,47 +109,48 @@ __global__ void k_csr_bounds(const __grid_constant__ BwdParams p) {
   if (j == p.B - 1) start[u + 1] = (int32_t)p.B;
 }
 
-template <class S>
-__global__ void __launch_bounds__(256) k_grad_u(const __grid_constant__ BwdParams p) {
+template <class C>
+__global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdParams p) {
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
+  const int ncb = col_blocks<C>(p.D);
   if (threadIdx.x == 0) {
     int64_t acc = 0;
     for (int f = 0; f < p.F; ++f) {
       s_pref[f] = acc;
-      acc += p.counts[f];
+      acc += p.counts[f] * ncb;
     }
     s_pref[p.F] = acc;
   }
   __syncthreads();
   const int64_t total = s_pref[p.F];
-  const int sl = threadIdx.x % S::LPR;
-  const int64_t nworkers = (int64_t)gridDim.x * blockDim.x / S::LPR;
-  constexpr int N = S::N;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::LPR; w < total;
-       w += nworkers) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  constexpr int V = C::VW;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
+       w += nwarps) {
     const int f = find_seg(s_pref, p.F, w);
-    const int64_t u = w - s_pref[f];
-    const float* G = p.grad_out[f];
+    const ColWork cw = col_work<C>(w - s_pref[f], p.D, lane);
+    const int64_t u = cw.row;
+    const float* G = p.grad_out[f] + cw.lo;
     const int is = p.feat_is[f];
-    float acc[N];
+    float acc[V];
     if (is < 0) {
-      S::load(G + u * p.D, sl, p.D, acc);
+      C::ld(G + u * p.D, cw.ok, acc);
     } else {
       const int32_t* start = p.csr_start + (int64_t)is * (p.B + 1);
       const uint32_t* rows = p.inv_rows + (int64_t)is * p.B;
       const int64_t a = start[u], e = start[u + 1];
-#pragma unroll
-      for (int k = 0; k < N; ++k) acc[k] = 0.0f;
-      float x[8][N];
+      C::zero(acc);
+      float x[8][V];
       for (int64_t j = a; j < e; j += 8) {
 #pragma unroll
         for (int t = 0; t < 8; ++t)
-          if (j + t < e) S::load(G + (int64_t)rows[j + t] * p.D, sl, p.D, x[t]);
+          if (j + t < e) C::ld(G + (uint64_t)__ldg(rows + j + t) * (uint32_t)p.D, cw.ok, x[t]);
 #pragma unroll
         for (int t = 0; t < 8; ++t)
           if (j + t < e) {
 #pragma unroll
-            for (int k = 0; k < N; ++k) acc[k] = __fadd_rn(acc[k], x[t][k]);
+            for (int k = 0; k < V; ++k) acc[k] = __fadd_rn(acc[k], x[t][k]);
           }
       }
     }
@@ -152,10 +161,10 @@ __global__ void __launch_bounds__(256) k_grad_u(const __grid_constant__ BwdParam
       if (len > 0) {
         const float fl = (float)len;
 #pragma unroll
-        for (int k = 0; k < N; ++k) acc[k] = __fdiv_rn(acc[k], fl);
+        for (int k = 0; k < V; ++k) acc[k] = __fdiv_rn(acc[k], fl);
       }
     }
-    S::store(p.grad_u + ((int64_t)f * p.B + u) * p.D, sl, p.D, acc);
+    C::st(p.grad_u + ((int64_t)f * p.B + u) * p.D + cw.lo, cw.ok, acc);
   }
 }
 
@@ -213,69 +222,110 @@ __global__ void __launch_bounds__(RC) k_run_count(const __grid_constant__ BwdPar
   if (threadIdx.x == 0) p.run_part[chunk] = cnt;
 }
 
-template <class S>
-__global__ void __launch_bounds__(256) k_scatter(const __grid_constant__ BwdParams p) {
-  constexpr int N = S::N;
-  const int sl = threadIdx.x % S::LPR;
-  const int64_t nworkers = (int64_t)gridDim.x * blockDim.x / S::LPR;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::LPR;
-       w < p.total_rc_chunks; w += nworkers) {
-    const int s = rc_seg(p, w);
+// first position >= j whose key differs from `id` (lane-parallel search)
+__device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t n, uint32_t id,
+                                           int lane) {
+  for (int64_t j0 = j; j0 < n; j0 += 32) {
+    const int64_t q = j0 + lane;
+    const bool diff = q >= n || __ldg(K + q) != id;
+    const unsigned b = __ballot_sync(0xffffffffu, diff);
+    if (b) return j0 + __ffs(b) - 1;
+  }
+  return n;
+}
+
+constexpr int SC_G = 4;  // runs (distinct IDs) in flight per warp
+
+template <class C>
+__global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid_constant__ BwdParams p) {
+  constexpr int V = C::VW;
+  __shared__ int32_t s_starts[8][RC + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const int ncb = col_blocks<C>(p.D);
+  const int64_t total = p.total_rc_chunks * ncb;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int32_t* starts = s_starts[warp];
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
+    const int64_t chunk = (ncb == 1) ? w : w / ncb;
+    const int lo_f = (int)(w - chunk * ncb) * C::CB + lane * V;  // this lane's first float
+    const bool ok = lo_f < p.D;
+    const uint32_t D32 = (uint32_t)p.D;
+    const int s = rc_seg(p, chunk);
     const int64_t n = p.seg_count[s];
-    const int64_t lo = (w - p.ts_chunk0[s]) * RC;
+    const int64_t lo = (chunk - p.ts_chunk0[s]) * RC;
     if (lo >= n) continue;
     const int64_t hi = min(n, lo + (int64_t)RC);
     const uint32_t* K = p.occ_keys + p.ts_base[s];
-    const uint32_t* V = p.occ_vals + p.ts_base[s];
-    int64_t j = lo;
-    if (j > 0)
-      while (j < hi && K[j] == K[j - 1]) ++j;
-    int64_t run_idx = p.apply_sgd ? 0 : p.run_part[w];
-    while (j < hi) {
-      const uint32_t id = K[j];
-      float acc[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) acc[k] = 0.0f;
-      int64_t k0 = j;
-      while (true) {
-        uint32_t ks[8], vs[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const bool ok = k0 + t < n;
-          ks[t] = ok ? K[k0 + t] : ~id;
-          vs[t] = ok ? V[k0 + t] : 0u;
-        }
-        int m = 0;
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (m == t && ks[t] == id) m = t + 1;
-        float x[8][N];
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (t < m) S::load(p.grad_u + (int64_t)vs[t] * p.D, sl, p.D, x[t]);
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (t < m) {
-#pragma unroll
-            for (int k = 0; k < N; ++k) acc[k] = __fadd_rn(acc[k], x[t][k]);
-          }
-        k0 += m;
-        if (m < 8) break;
+    const uint32_t* Vv = p.occ_vals + p.ts_base[s];
+    // 1. run starts inside [lo, hi)
+    int nruns = 0;
+    for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+      const int64_t j = j0 + lane;
+      bool st = false;
+      if (j < hi) {
+        const uint32_t k = __ldg(K + j);
+        st = (j == 0) || __ldg(K + j - 1) != k;
       }
-      if (p.apply_sgd) {
-        float* row = p.table[s] + (int64_t)id * p.D;
-        float wv[N];
-        S::load_rw(row, sl, p.D, wv);
-#pragma unroll
-        for (int k = 0; k < N; ++k) wv[k] = __fsub_rn(wv[k], __fmul_rn(p.lr, acc[k]));
-        S::store(row, sl, p.D, wv);
-      } else {
-        if (sl == 0) p.grad_ids[s][run_idx] = (int64_t)id;
-        S::store(p.grad_rows[s] + run_idx * p.D, sl, p.D, acc);
-        ++run_idx;
-      }
-      j = k0;
+      const unsigned b = __ballot_sync(0xffffffffu, st);
+      if (st) starts[nruns + __popc(b & lt)] = (int32_t)(j - lo);
+      nruns += __popc(b);
     }
+    __syncwarp();
+    // end of the last run (may continue past hi)
+    int64_t last_end = hi;
+    if (nruns > 0) last_end = run_end(K, hi, n, __ldg(K + lo + starts[nruns - 1]), lane);
+    int64_t run_idx = p.apply_sgd ? 0 : p.run_part[w / ncb];
+    float* table = p.table[s] + lo_f;
+    const float* gu = p.grad_u + lo_f;
+    U32Win vwin{Vv, n, lane, 0, 0};
+    vwin.window(lo);
+    // 2. groups of SC_G runs: table rows prefetched together, then ordered sums
+    for (int r0 = 0; r0 < nruns; r0 += SC_G) {
+      uint32_t ids[SC_G];
+      float wv[SC_G][V];
+#pragma unroll
+      for (int g = 0; g < SC_G; ++g) {
+        ids[g] = 0;
+        if (r0 + g < nruns) {
+          ids[g] = __ldg(K + lo + starts[r0 + g]);
+          if (p.apply_sgd) C::ld_rw(table + (uint64_t)ids[g] * D32, ok, wv[g]);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < SC_G; ++g) {
+        if (r0 + g >= nruns) break;
+        const int64_t a = lo + starts[r0 + g];
+        const int64_t e = (r0 + g + 1 < nruns) ? lo + starts[r0 + g + 1] : last_end;
+        float acc[V];
+        C::zero(acc);
+        float x[8][V];
+        for (int64_t k0 = a; k0 < e; k0 += 8) {
+          vwin.need(k0, 8);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const uint32_t vv = vwin.get(k0 + t);
+            if (k0 + t < e) C::ld(gu + (uint64_t)vv * D32, ok, x[t]);
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (k0 + t < e) {
+#pragma unroll
+              for (int k = 0; k < V; ++k) acc[k] = __fadd_rn(acc[k], x[t][k]);
+            }
+        }
+        if (p.apply_sgd) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) wv[g][k] = __fsub_rn(wv[g][k], __fmul_rn(p.lr, acc[k]));
+          C::st(table + (uint64_t)ids[g] * D32, ok, wv[g]);
+        } else {
+          if (lo_f == 0) p.grad_ids[s][run_idx] = (int64_t)ids[g];
+          C::st(p.grad_rows[s] + run_idx * p.D + lo_f, ok, acc);
+          ++run_idx;
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -496,10 +546,10 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
     note_launch();
   }
   // 2-5
-  int rc = RECD_DISPATCH_SLICE(dim, {
-    const int64_t per_block = 256 / S::LPR;
-    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(B * F, per_block), (int64_t)num_sms() * 8);
-    k_grad_u<S><<<grid, 256, 0, stream>>>(p);
+  int rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, {
+    const int ncb = col_blocks<C>(dim);
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(B * F * ncb, 8), (int64_t)num_sms() * 16);
+    k_grad_u<C><<<grid, 256, 0, stream>>>(p);
     k_occ<<<num_sms() * 4, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
     note_launch(2);
     std::vector<SegDesc> segs;
@@ -526,8 +576,8 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
       int r3 = seg_exclusive_scan(sd.data(), (int)sd.size(), sc.scan_part, stream);
       if (r3 != RECD_OK) return r3;
     }
-    const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks, per_block), (int64_t)num_sms() * 16);
-    k_scatter<S><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+    const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks * ncb, 8), (int64_t)num_sms() * 16);
+    k_scatter<C><<<std::max(g2, 1u), 256, 0, stream>>>(p);
     note_launch();
   });
   if (rc != RECD_OK) return rc;

@@ -1,121 +1,105 @@
-// Row slices and the exact-order pooling reductions shared by the forward
-// and backward kernels.
+// Column-block row workers and the exact-order pooling reductions shared by
+// the forward and backward kernels.
 //
-// A "worker" is LPR consecutive lanes owning one embedding row of D floats:
-// lane sl of the worker holds NV float4 vectors (dims 4*(sl + LPR*v) ..) when
-// D % 4 == 0, else NV scalars (dims sl + LPR*v).  D = 128 -> 32 lanes x 1
-// float4 (one 512-byte row per warp, fully coalesced 128-bit loads);
-// D = 64 -> 16 lanes (two rows per warp).
+// A worker is one warp owning a 32*VW-float column block of an embedding row:
+// lane l holds dims [off + l*VW, off + l*VW + VW).  With VW = 2 a warp moves a
+// contiguous 256-byte slice per load instruction (LDG.64, fully coalesced);
+// a D = 128 row is two workers, D = 64 one.  Reductions are per dimension,
+// so splitting a row's dims over warps never changes the arithmetic, and the
+// small per-lane state (8 accumulators x 2 floats) keeps kernels at <= 64
+// registers, i.e. >= 32 resident warps per SM to hide gather latency.
 #pragma once
 
 #include "recd_common.cuh"
 
 namespace recd {
 
-template <int LPR_, int NV_, bool F4_>
-struct Slice {
-  static constexpr int LPR = LPR_;
-  static constexpr int NV = NV_;
-  static constexpr bool F4 = F4_;
-  static constexpr int N = F4 ? 4 * NV : NV;
+template <int VW_>
+struct Col {
+  static constexpr int VW = VW_;
+  static constexpr int CB = 32 * VW;  // floats per column block
 
-  __device__ __forceinline__ static void zero(float (&x)[N]) {
+  __device__ __forceinline__ static void zero(float (&x)[VW]) {
 #pragma unroll
-    for (int e = 0; e < N; ++e) x[e] = 0.0f;
+    for (int e = 0; e < VW; ++e) x[e] = 0.0f;
   }
-  __device__ __forceinline__ static void load(const float* __restrict__ row, int sl, int D,
-                                              float (&x)[N]) {
-    if (row == nullptr) {
+  // p points at this lane's first float; ok = lane's slice lies inside the row.
+  // Read-only path: tables are never written by the kernels that use it.
+  __device__ __forceinline__ static void ld(const float* __restrict__ p, bool ok, float (&x)[VW]) {
+    if (!ok) {
       zero(x);
       return;
     }
-    if constexpr (F4) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int d0 = 4 * (sl + LPR * v);
-        if (d0 < D) {
-          const float4 t = __ldg(reinterpret_cast<const float4*>(row + d0));
-          x[4 * v] = t.x; x[4 * v + 1] = t.y; x[4 * v + 2] = t.z; x[4 * v + 3] = t.w;
-        } else {
-          x[4 * v] = x[4 * v + 1] = x[4 * v + 2] = x[4 * v + 3] = 0.0f;
-        }
-      }
+    if constexpr (VW == 4) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+      x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+    } else if constexpr (VW == 2) {
+      const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+      x[0] = t.x; x[1] = t.y;
     } else {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int d = sl + LPR * v;
-        x[v] = d < D ? __ldg(row + d) : 0.0f;
-      }
+      x[0] = __ldg(p);
     }
   }
-  // plain (coherent) load, for rows that are read-modify-written
-  __device__ __forceinline__ static void load_rw(const float* row, int sl, int D, float (&x)[N]) {
-    if constexpr (F4) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int d0 = 4 * (sl + LPR * v);
-        if (d0 < D) {
-          const float4 t = *reinterpret_cast<const float4*>(row + d0);
-          x[4 * v] = t.x; x[4 * v + 1] = t.y; x[4 * v + 2] = t.z; x[4 * v + 3] = t.w;
-        }
-      }
+  // coherent load, for rows that are read-modify-written
+  __device__ __forceinline__ static void ld_rw(const float* p, bool ok, float (&x)[VW]) {
+    if (!ok) {
+      zero(x);
+      return;
+    }
+    if constexpr (VW == 4) {
+      const float4 t = *reinterpret_cast<const float4*>(p);
+      x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
+    } else if constexpr (VW == 2) {
+      const float2 t = *reinterpret_cast<const float2*>(p);
+      x[0] = t.x; x[1] = t.y;
     } else {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int d = sl + LPR * v;
-        if (d < D) x[v] = row[d];
-      }
+      x[0] = *p;
     }
   }
-  __device__ __forceinline__ static void store(float* row, int sl, int D, const float (&x)[N]) {
-    if constexpr (F4) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int d0 = 4 * (sl + LPR * v);
-        if (d0 < D)
-          *reinterpret_cast<float4*>(row + d0) =
-              make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
-      }
+  __device__ __forceinline__ static void st(float* p, bool ok, const float (&x)[VW]) {
+    if (!ok) return;
+    if constexpr (VW == 4) {
+      *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
+    } else if constexpr (VW == 2) {
+      *reinterpret_cast<float2*>(p) = make_float2(x[0], x[1]);
     } else {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int d = sl + LPR * v;
-        if (d < D) row[d] = x[v];
-      }
+      *p = x[0];
     }
   }
 };
 
-// Dispatch D -> Slice type.  Supported: D % 4 == 0 up to 1024, else D <= 256.
-#define RECD_DISPATCH_SLICE(D, ...)                                                   \
-  [&]() -> int {                                                                      \
-    const int _d = (D);                                                               \
-    if (_d <= 0) return RECD_ERR_ARG;                                                 \
-    if (_d % 4 == 0) {                                                                \
-      const int _v = _d / 4;                                                          \
-      if (_v <= 1) { using S = ::recd::Slice<1, 1, true>; __VA_ARGS__ }               \
-      else if (_v <= 2) { using S = ::recd::Slice<2, 1, true>; __VA_ARGS__ }          \
-      else if (_v <= 4) { using S = ::recd::Slice<4, 1, true>; __VA_ARGS__ }          \
-      else if (_v <= 8) { using S = ::recd::Slice<8, 1, true>; __VA_ARGS__ }          \
-      else if (_v <= 16) { using S = ::recd::Slice<16, 1, true>; __VA_ARGS__ }        \
-      else if (_v <= 32) { using S = ::recd::Slice<32, 1, true>; __VA_ARGS__ }        \
-      else if (_v <= 64) { using S = ::recd::Slice<32, 2, true>; __VA_ARGS__ }        \
-      else if (_v <= 128) { using S = ::recd::Slice<32, 4, true>; __VA_ARGS__ }       \
-      else if (_v <= 256) { using S = ::recd::Slice<32, 8, true>; __VA_ARGS__ }       \
-      else return RECD_ERR_UNSUPPORTED;                                               \
-    } else {                                                                          \
-      if (_d <= 1) { using S = ::recd::Slice<1, 1, false>; __VA_ARGS__ }              \
-      else if (_d <= 2) { using S = ::recd::Slice<2, 1, false>; __VA_ARGS__ }         \
-      else if (_d <= 4) { using S = ::recd::Slice<4, 1, false>; __VA_ARGS__ }         \
-      else if (_d <= 8) { using S = ::recd::Slice<8, 1, false>; __VA_ARGS__ }         \
-      else if (_d <= 16) { using S = ::recd::Slice<16, 1, false>; __VA_ARGS__ }       \
-      else if (_d <= 32) { using S = ::recd::Slice<32, 1, false>; __VA_ARGS__ }       \
-      else if (_d <= 64) { using S = ::recd::Slice<32, 2, false>; __VA_ARGS__ }       \
-      else if (_d <= 128) { using S = ::recd::Slice<32, 4, false>; __VA_ARGS__ }      \
-      else if (_d <= 256) { using S = ::recd::Slice<32, 8, false>; __VA_ARGS__ }      \
-      else return RECD_ERR_UNSUPPORTED;                                               \
-    }                                                                                 \
-    return RECD_OK;                                                                   \
+// (row, column block) of work item w for a D-wide row
+struct ColWork {
+  int64_t row;
+  int lo;   // this lane's first float inside a row: block offset + lane * VW
+  bool ok;  // the lane's slice lies inside the row
+};
+template <class C>
+__device__ __forceinline__ ColWork col_work(int64_t w, int D, int lane) {
+  const int ncb = (D + C::CB - 1) / C::CB;
+  ColWork c;
+  c.row = (ncb == 1) ? w : (ncb == 2 ? (w >> 1) : w / ncb);
+  const int cb = (int)(w - c.row * ncb);
+  c.lo = cb * C::CB + lane * C::VW;
+  c.ok = c.lo < D;
+  return c;
+}
+template <class C>
+__host__ __device__ __forceinline__ int col_blocks(int D) {
+  return (D + C::CB - 1) / C::CB;
+}
+
+// Dispatch D -> Col type: float4 lanes (one 512-byte row slice per warp load)
+// when D % 4 == 0 and D >= 64, float2 lanes when D is even, else scalars.
+#define RECD_DISPATCH_COL(D, ...) RECD_DISPATCH_COL_VW(D, 4, __VA_ARGS__)
+#define RECD_DISPATCH_COL_VW(D, MAXVW, ...)                     \
+  [&]() -> int {                                                \
+    const int _d = (D);                                         \
+    if (_d <= 0) return RECD_ERR_ARG;                           \
+    if ((MAXVW) >= 4 && _d % 4 == 0 && _d >= 64) { using C = ::recd::Col<4>; __VA_ARGS__ } \
+    else if (_d % 2 == 0) { using C = ::recd::Col<2>; __VA_ARGS__ } \
+    else { using C = ::recd::Col<1>; __VA_ARGS__ }              \
+    return RECD_OK;                                             \
   }()
 
 // ---------------------------------------------------------------------------
@@ -127,63 +111,80 @@ struct Slice {
 //     m > 128      : P(x[:h]) + P(x[h:]), h = m/2 rounded down to a multiple of 8
 // Verified bit-exact against the reference's `pool` (trainer_sim.py:336-343)
 // by tests/golden/pool.npz.  Every add is a separately rounded fp32 add.
+// `row(j)` returns the base pointer of value j's embedding row (nullptr = zeros).
 // ---------------------------------------------------------------------------
-template <class S, class Row>
-__device__ __forceinline__ void leaf_sum(const Row& row, int64_t a, int64_t m, int sl, int D,
-                                         float (&s)[S::N]) {
-  constexpr int N = S::N;
-  float x[8][N];
+template <class C, class Row>
+__device__ __forceinline__ void ld_row(Row& row, int64_t j, bool ok, float (&x)[C::VW]) {
+  C::ld(row(j), ok, x);
+}
+
+template <class C, class Row>
+__device__ __forceinline__ void leaf_sum(Row& row, int64_t a, int64_t m, bool ok,
+                                         float (&s)[C::VW]) {
+  constexpr int V = C::VW;
+#define ld(j, x) ld_row<C>(row, (j), ok, x)
+  float x[8][V];
   if (m < 8) {
+    row.need(a, (int)m);
 #pragma unroll
     for (int t = 0; t < 7; ++t)
-      if (t < m) S::load(row(a + t), sl, D, x[t]);
+      if (t < m) ld(a + t, x[t]);
 #pragma unroll
-    for (int e = 0; e < N; ++e) s[e] = -0.0f;
+    for (int e = 0; e < V; ++e) s[e] = -0.0f;
 #pragma unroll
     for (int t = 0; t < 7; ++t)
       if (t < m) {
 #pragma unroll
-        for (int e = 0; e < N; ++e) s[e] = __fadd_rn(s[e], x[t][e]);
+        for (int e = 0; e < V; ++e) s[e] = __fadd_rn(s[e], x[t][e]);
       }
     return;
   }
-  float r[8][N];
+  float r[8][V];
+  row.need(a, 8);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) S::load(row(a + k), sl, D, r[k]);
+  for (int k = 0; k < 8; ++k) ld(a + k, r[k]);
   const int64_t mb = m - (m % 8);
   for (int64_t i = 8; i < mb; i += 8) {
+    row.need(a + i, 8);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) S::load(row(a + i + k), sl, D, x[k]);
+    for (int k = 0; k < 8; ++k) ld(a + i + k, x[k]);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
 #pragma unroll
-      for (int e = 0; e < N; ++e) r[k][e] = __fadd_rn(r[k][e], x[k][e]);
+      for (int e = 0; e < V; ++e) r[k][e] = __fadd_rn(r[k][e], x[k][e]);
   }
 #pragma unroll
-  for (int e = 0; e < N; ++e)
+  for (int e = 0; e < V; ++e)
     s[e] = __fadd_rn(__fadd_rn(__fadd_rn(r[0][e], r[1][e]), __fadd_rn(r[2][e], r[3][e])),
                      __fadd_rn(__fadd_rn(r[4][e], r[5][e]), __fadd_rn(r[6][e], r[7][e])));
   const int tail = (int)(m - mb);
+  if (tail) row.need(a + mb, tail);
 #pragma unroll
   for (int t = 0; t < 7; ++t)
-    if (t < tail) S::load(row(a + mb + t), sl, D, x[t]);
+    if (t < tail) ld(a + mb + t, x[t]);
 #pragma unroll
   for (int t = 0; t < 7; ++t)
     if (t < tail) {
 #pragma unroll
-      for (int e = 0; e < N; ++e) s[e] = __fadd_rn(s[e], x[t][e]);
+      for (int e = 0; e < V; ++e) s[e] = __fadd_rn(s[e], x[t][e]);
     }
+#undef ld
 }
 
-// m > 128: the pairwise recursion P(x[:h]) + P(x[h:]) run as an explicit
-// post-order DFS (frames + value stack in local memory; only long rows take it).
-template <class S, class Row>
-__device__ __noinline__ void pairwise_big(const Row row, int64_t a, int64_t m, int sl, int D,
-                                          float* out) {
+// P over any m: the recursion P(x[:h]) + P(x[h:]) (m > 128) runs as an
+// explicit post-order DFS (frames + value stack in local memory); m <= 128 is a
+// single leaf.  One inlined leaf copy keeps register pressure low.
+template <int V>
+struct Vals {
+  float v[V];
+};
+
+template <class C, class Row>
+__device__ __forceinline__ Vals<C::VW> pairwise_big(Row& row, int64_t a, int64_t m, bool ok) {
   constexpr int DEPTH = 40;
   int64_t fa[DEPTH], fm[DEPTH];
   int fs[DEPTH];
-  float vals[DEPTH][S::N];
+  float vals[DEPTH][C::VW];
   int top = 1, vtop = 0;
   fa[0] = a;
   fm[0] = m;
@@ -191,7 +192,7 @@ __device__ __noinline__ void pairwise_big(const Row row, int64_t a, int64_t m, i
   while (top > 0) {
     const int t = top - 1;
     if (fm[t] <= 128) {
-      leaf_sum<S>(row, fa[t], fm[t], sl, D, vals[vtop]);
+      leaf_sum<C>(row, fa[t], fm[t], ok, vals[vtop]);
       ++vtop;
       --top;
       continue;
@@ -209,12 +210,14 @@ __device__ __noinline__ void pairwise_big(const Row row, int64_t a, int64_t m, i
     } else {
       --vtop;
 #pragma unroll
-      for (int e = 0; e < S::N; ++e) vals[vtop - 1][e] = __fadd_rn(vals[vtop - 1][e], vals[vtop][e]);
+      for (int e = 0; e < C::VW; ++e) vals[vtop - 1][e] = __fadd_rn(vals[vtop - 1][e], vals[vtop][e]);
       --top;
     }
   }
+  Vals<C::VW> out;
 #pragma unroll
-  for (int e = 0; e < S::N; ++e) out[e] = vals[0][e];
+  for (int e = 0; e < C::VW; ++e) out.v[e] = vals[0][e];
+  return out;
 }
 
 __device__ __forceinline__ float np_max(float acc, float x) {
@@ -222,72 +225,115 @@ __device__ __forceinline__ float np_max(float acc, float x) {
 }
 
 // pool one jagged row a[0..n) (trainer_sim.py:324-344): empty -> 0.
-template <class S, class Row>
-__device__ __forceinline__ void pool_row(const Row& row, int64_t a, int64_t n, int mode, int sl,
-                                         int D, float (&out)[S::N]) {
-  constexpr int N = S::N;
+template <class C, class Row>
+__device__ __forceinline__ void pool_row(Row& row, int64_t a, int64_t n, int mode, bool ok,
+                                         float (&out)[C::VW]) {
+  constexpr int V = C::VW;
   if (n <= 0) {
-    S::zero(out);
+    C::zero(out);
     return;
   }
-  S::load(row(a), sl, D, out);
+  row.need(a, 1);
+  C::ld(row(a), ok, out);
   if (mode == RECD_POOL_MAX) {
-    float x[8][N];
+    float x[8][V];
     for (int64_t i = 1; i < n; i += 8) {
+      row.need(a + i, (int)min((int64_t)8, n - i));
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (i + k < n) S::load(row(a + i + k), sl, D, x[k]);
+        if (i + k < n) C::ld(row(a + i + k), ok, x[k]);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
         if (i + k < n) {
 #pragma unroll
-          for (int e = 0; e < N; ++e) out[e] = np_max(out[e], x[k][e]);
+          for (int e = 0; e < V; ++e) out[e] = np_max(out[e], x[k][e]);
         }
     }
     return;
   }
   if (n > 1) {
-    float s[N];
-    if (n - 1 <= 128) {
-      leaf_sum<S>(row, a + 1, n - 1, sl, D, s);
-    } else {
-      pairwise_big<S, Row>(row, a + 1, n - 1, sl, D, s);
-    }
+    // one code path for every length: a single leaf when n - 1 <= 128
+    const Vals<V> s = pairwise_big<C, Row>(row, a + 1, n - 1, ok);
 #pragma unroll
-    for (int e = 0; e < N; ++e) out[e] = __fadd_rn(out[e], s[e]);
+    for (int e = 0; e < V; ++e) out[e] = __fadd_rn(out[e], s.v[e]);
   }
   if (mode == RECD_POOL_AVG) {
     const float fl = (float)n;
 #pragma unroll
-    for (int e = 0; e < N; ++e) out[e] = __fdiv_rn(out[e], fl);
+    for (int e = 0; e < V; ++e) out[e] = __fdiv_rn(out[e], fl);
   }
 }
 
 // Row accessors -----------------------------------------------------------
+// Table rows addressed through a warp-wide window of 32 IDs: lane l holds the
+// ID at position base + l (loaded once, coalesced, range-checked lane-parallel)
+// and every row gather gets its ID with one shuffle, so the gathers of a batch
+// issue back to back instead of each waiting on its own ID load.  An
+// out-of-range ID is recorded in `err` (the host raises the reference's
+// ValueError) and reads row 0 so the gather stays branch-free.
 struct TableRows {
-  const float* W;
+  const float* Wl;  // table + this lane's first float
   const int64_t* ids;
+  int64_t end;      // one past the last valid position
   int64_t rows;
-  int D;
+  uint32_t D;
   int64_t* err;
   int64_t errbase;
-  __device__ __forceinline__ const float* operator()(int64_t j) const {
-    const int64_t id = ids[j];
-    if ((uint64_t)id >= (uint64_t)rows) {
-      atomicMin(reinterpret_cast<unsigned long long*>(err), (unsigned long long)(errbase + j));
-      return nullptr;
+  int lane;
+  int64_t base;
+  uint32_t mine;
+
+  __device__ __forceinline__ void window(int64_t j) {
+    base = j;
+    const int64_t q = j + lane;
+    mine = 0;
+    if (q < end) {
+      const int64_t id = __ldg(ids + q);
+      if ((uint64_t)id < (uint64_t)rows) {
+        mine = (uint32_t)id;
+      } else {
+        atomicMin(reinterpret_cast<unsigned long long*>(err), (unsigned long long)(errbase + q));
+      }
     }
-    return W + id * (int64_t)D;
+  }
+  // make positions [j, j + n) (n <= 32) available
+  __device__ __forceinline__ void need(int64_t j, int n) {
+    if (j < base || j + n > base + 32) window(j);
+  }
+  __device__ __forceinline__ const float* operator()(int64_t j) const {
+    const uint32_t id = __shfl_sync(0xffffffffu, mine, (int)(j - base));
+    return Wl + (uint64_t)id * D;
+  }
+};
+
+// Warp-wide window of 32 consecutive uint32 values (lane l holds base + l).
+struct U32Win {
+  const uint32_t* p;
+  int64_t end;
+  int lane;
+  int64_t base;
+  uint32_t mine;
+  __device__ __forceinline__ void window(int64_t j) {
+    base = j;
+    const int64_t q = j + lane;
+    mine = q < end ? __ldg(p + q) : 0u;
+  }
+  __device__ __forceinline__ void need(int64_t j, int n) {
+    if (j < base || j + n > base + 32) window(j);
+  }
+  __device__ __forceinline__ uint32_t get(int64_t j) const {
+    return __shfl_sync(0xffffffffu, mine, (int)(j - base));
   }
 };
 
 struct DenseRows {
-  const float* A;
+  const float* Al;  // activations + this lane's first float
   int D;
-  __device__ __forceinline__ const float* operator()(int64_t j) const { return A + j * (int64_t)D; }
+  __device__ __forceinline__ void need(int64_t, int) {}
+  __device__ __forceinline__ const float* operator()(int64_t j) const { return Al + j * (int64_t)D; }
 };
 
-// find feature f with pref[f] <= w < pref[f+1] (pref in shared memory)
+// find segment f with pref[f] <= w < pref[f+1] (pref in shared memory)
 __device__ __forceinline__ int find_seg(const int64_t* pref, int F, int64_t w) {
   int lo = 0, hi = F - 1;
   while (lo < hi) {
