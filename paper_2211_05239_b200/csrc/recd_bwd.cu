@@ -234,18 +234,30 @@ __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t
   return n;
 }
 
-constexpr int SC_G = 4;  // runs (distinct IDs) in flight per warp
+constexpr int SC_RS = 8;  // table rows prefetched ahead per warp (shared-memory ring)
 
+// One warp per (chunk of RC sorted positions, column block).  Runs of equal
+// IDs that start in the chunk are reduced in position order (== ascending
+// (feature, unique row, position) order, so bit-identical to the oracle).
+// The table rows of the next SC_RS runs are prefetched with cp.async into a
+// per-warp shared ring while grad_u rows (L2-resident) are gathered 8 positions
+// at a time across run boundaries; at each run end the row is updated and
+// stored, and its slot refilled with the row of run r + SC_RS.
 template <class C>
 __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid_constant__ BwdParams p) {
   constexpr int V = C::VW;
-  __shared__ int32_t s_starts[8][RC + 1];
+  __shared__ uint16_t s_starts[8][RC + 2];
+  __shared__ uint32_t s_ids[8][RC];
+  __shared__ __align__(16) float s_ring[8][SC_RS][C::CB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   const int ncb = col_blocks<C>(p.D);
   const int64_t total = p.total_rc_chunks * ncb;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  int32_t* starts = s_starts[warp];
+  uint16_t* starts = s_starts[warp];
+  uint32_t* rids = s_ids[warp];
+  float* ring = &s_ring[warp][0][lane * V];
+  const bool apply = p.apply_sgd != 0;
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
     const int64_t chunk = (ncb == 1) ? w : w / ncb;
     const int lo_f = (int)(w - chunk * ncb) * C::CB + lane * V;  // this lane's first float
@@ -258,73 +270,82 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
     const int64_t hi = min(n, lo + (int64_t)RC);
     const uint32_t* K = p.occ_keys + p.ts_base[s];
     const uint32_t* Vv = p.occ_vals + p.ts_base[s];
-    // 1. run starts inside [lo, hi)
+    // 1. runs starting inside [lo, hi): start offsets and IDs
     int nruns = 0;
     for (int64_t j0 = lo; j0 < hi; j0 += 32) {
       const int64_t j = j0 + lane;
+      uint32_t k = 0;
       bool st = false;
       if (j < hi) {
-        const uint32_t k = __ldg(K + j);
+        k = __ldg(K + j);
         st = (j == 0) || __ldg(K + j - 1) != k;
       }
       const unsigned b = __ballot_sync(0xffffffffu, st);
-      if (st) starts[nruns + __popc(b & lt)] = (int32_t)(j - lo);
+      if (st) {
+        starts[nruns + __popc(b & lt)] = (uint16_t)(j - lo);
+        rids[nruns + __popc(b & lt)] = k;
+      }
       nruns += __popc(b);
     }
     __syncwarp();
-    // end of the last run (may continue past hi)
-    int64_t last_end = hi;
-    if (nruns > 0) last_end = run_end(K, hi, n, __ldg(K + lo + starts[nruns - 1]), lane);
-    int64_t run_idx = p.apply_sgd ? 0 : p.run_part[w / ncb];
+    if (nruns == 0) continue;
+    const int64_t pend = run_end(K, hi, n, rids[nruns - 1], lane);  // end of the last run
     float* table = p.table[s] + lo_f;
     const float* gu = p.grad_u + lo_f;
-    U32Win vwin{Vv, n, lane, 0, 0};
-    vwin.window(lo);
-    // 2. groups of SC_G runs: table rows prefetched together, then ordered sums
-    for (int r0 = 0; r0 < nruns; r0 += SC_G) {
-      uint32_t ids[SC_G];
-      float wv[SC_G][V];
+    // 2. prefetch the table rows of the first SC_RS runs
+    if (apply) {
 #pragma unroll
-      for (int g = 0; g < SC_G; ++g) {
-        ids[g] = 0;
-        if (r0 + g < nruns) {
-          ids[g] = __ldg(K + lo + starts[r0 + g]);
-          if (p.apply_sgd) C::ld_rw(table + (uint64_t)ids[g] * D32, ok, wv[g]);
-        }
+      for (int r = 0; r < SC_RS; ++r) {
+        if (r < nruns && ok) cp_async<V * 4>(ring + r * C::CB, table + (uint64_t)rids[r] * D32);
+        cp_async_commit();
+      }
+    }
+    const int64_t run_base = apply ? 0 : p.run_part[chunk];
+    // 3. flat pass over the positions of the chunk's runs
+    U32Win vwin{Vv, pend, lane, 0, 0};
+    vwin.window(lo + starts[0]);
+    int r = 0;
+    int64_t bnd = (nruns > 1) ? lo + starts[1] : pend;  // end of run r
+    float acc[V];
+    C::zero(acc);
+    float x[8][V];
+    for (int64_t k0 = lo + starts[0]; k0 < pend; k0 += 8) {
+      vwin.need(k0, 8);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t vv = vwin.get(k0 + t);
+        if (k0 + t < pend) C::ld(gu + (uint64_t)vv * D32, ok, x[t]);
       }
 #pragma unroll
-      for (int g = 0; g < SC_G; ++g) {
-        if (r0 + g >= nruns) break;
-        const int64_t a = lo + starts[r0 + g];
-        const int64_t e = (r0 + g + 1 < nruns) ? lo + starts[r0 + g + 1] : last_end;
-        float acc[V];
-        C::zero(acc);
-        float x[8][V];
-        for (int64_t k0 = a; k0 < e; k0 += 8) {
-          vwin.need(k0, 8);
+      for (int t = 0; t < 8; ++t) {
+        if (k0 + t < pend) {
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const uint32_t vv = vwin.get(k0 + t);
-            if (k0 + t < e) C::ld(gu + (uint64_t)vv * D32, ok, x[t]);
-          }
+          for (int e = 0; e < V; ++e) acc[e] = __fadd_rn(acc[e], x[t][e]);
+          if (k0 + t + 1 == bnd) {  // run r complete (warp-uniform)
+            const uint32_t id = rids[r];
+            if (apply) {
+              cp_async_wait<SC_RS - 1>();
+              float* slot = ring + (r % SC_RS) * C::CB;
+              float wv[V];
 #pragma unroll
-          for (int t = 0; t < 8; ++t)
-            if (k0 + t < e) {
-#pragma unroll
-              for (int k = 0; k < V; ++k) acc[k] = __fadd_rn(acc[k], x[t][k]);
+              for (int e = 0; e < V; ++e) wv[e] = __fsub_rn(slot[e], __fmul_rn(p.lr, acc[e]));
+              C::st(table + (uint64_t)id * D32, ok, wv);
+              if (r + SC_RS < nruns && ok)
+                cp_async<V * 4>(slot, table + (uint64_t)rids[r + SC_RS] * D32);
+              cp_async_commit();
+            } else {
+              const int64_t ri = run_base + r;
+              if (lo_f == 0) p.grad_ids[s][ri] = (int64_t)id;
+              C::st(p.grad_rows[s] + ri * p.D + lo_f, ok, acc);
             }
-        }
-        if (p.apply_sgd) {
-#pragma unroll
-          for (int k = 0; k < V; ++k) wv[g][k] = __fsub_rn(wv[g][k], __fmul_rn(p.lr, acc[k]));
-          C::st(table + (uint64_t)ids[g] * D32, ok, wv[g]);
-        } else {
-          if (lo_f == 0) p.grad_ids[s][run_idx] = (int64_t)ids[g];
-          C::st(p.grad_rows[s] + run_idx * p.D + lo_f, ok, acc);
-          ++run_idx;
+            ++r;
+            C::zero(acc);
+            bnd = (r + 1 < nruns) ? lo + starts[r + 1] : pend;
+          }
         }
       }
     }
+    if (apply) cp_async_wait<0>();
     __syncwarp();
   }
 }

@@ -68,6 +68,24 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// cp.async (LDGSTS): asynchronous global -> shared copy of 4/8/16 bytes per
+// thread; in-flight copies hold no registers, so a warp can keep many table
+// rows in flight.  Completion is per thread via commit/wait groups.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  if constexpr (BYTES == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 // Block-wide exclusive scan of one int64 per thread; returns the exclusive
 // prefix, writes the block total to *total.  `smem` needs 32 int64 slots.
 template <int NT>

@@ -7,7 +7,8 @@
 // never merges unequal rows (full compare on hash match, tensors.py:270-276).
 //
 // Pipeline (one launch per phase for all groups of the step):
-//   k_rowscan  (group, 256-row chunk) blocks stream the KJT values once:
+//   k_rowscan  (group, 256-row chunk) blocks stream the KJT values once
+//              (8 consecutive values per thread, 128-bit loads):
 //              head[i] = row i differs from row i-1 (session-clustered batches
 //              make ~80% of rows non-heads), row hash for every row; the block
 //              also clears its slice of the group's hash table.
@@ -81,10 +82,11 @@ __device__ __forceinline__ uint64_t finalize_hash(uint64_t h, uint64_t mask) {
 // ---------------------------------------------------------------- rowscan
 constexpr int RS_NT = 256;
 constexpr int RS_RPB = 256;
+constexpr int RS_IT = 8;  // consecutive values per thread
 
 __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ DedupParams p) {
   const int g = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * RS_RPB;
   if (r0 >= p.B) return;
   const int64_t r1 = min(p.B, r0 + (int64_t)RS_RPB);
@@ -130,32 +132,51 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
       s_hash[j] += len_hash(len, fi);
     }
     __syncthreads();
+    // Each thread scans RS_IT consecutive values (one binary search, then a
+    // forward walk over the rows), compares them with the same positions of
+    // the previous row and accumulates the row hash locally; only row changes
+    // touch shared memory.
     const int64_t vbeg = s_start[0], vend = s_start[n];
-    for (int64_t qb = vbeg; qb < vend; qb += RS_NT) {
-      const int64_t q = qb + tid;
-      const bool valid = q < vend;
-      int j = 0x7fffffff;
-      uint64_t h = 0;
-      if (valid) {
-        int lo = 0, hi = n - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (s_start[mid] <= q) lo = mid; else hi = mid - 1;
-        }
-        j = lo;
-        const int64_t v = val[q];
-        if (s_mism[j] == 0u && val[q - s_len[j]] != v) s_mism[j] = 1u;
-        h = elem_hash(v, q - s_start[j], fi);
-      }
-      // segmented (by row j) warp reduction; rows are contiguous across lanes
+    const int64_t tb0 = vbeg & ~(int64_t)(RS_IT - 1);  // 64-byte aligned tiles
+    for (int64_t tb = tb0; tb < vend; tb += (int64_t)RS_NT * RS_IT) {
+      const int64_t q0 = tb + (int64_t)tid * RS_IT;
+      if (q0 >= vend || q0 + RS_IT <= vbeg) continue;
+      int64_t v[RS_IT];
+      if (q0 + RS_IT <= nv && (reinterpret_cast<uintptr_t>(val) & 15) == 0) {
+        const longlong2* src = reinterpret_cast<const longlong2*>(val + q0);
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t y = __shfl_down_sync(0xffffffffu, h, d);
-        const int jy = __shfl_down_sync(0xffffffffu, j, d);
-        if (lane + d < 32 && jy == j) h += y;
+        for (int k = 0; k < RS_IT / 2; ++k) {
+          const longlong2 t = __ldg(src + k);
+          v[2 * k] = t.x;
+          v[2 * k + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < RS_IT; ++k) v[k] = (q0 + k < nv) ? __ldg(val + q0 + k) : 0;
       }
-      const int jp = __shfl_up_sync(0xffffffffu, j, 1);
-      if (valid && (lane == 0 || jp != j)) atomicAdd(&s_hash[j], (unsigned long long)h);
+      const int64_t qs = max(q0, vbeg);
+      int lo = 0, hi = n - 1;  // row containing qs: last j with s_start[j] <= qs
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_start[mid] <= qs) lo = mid; else hi = mid - 1;
+      }
+      int j = lo;
+      int64_t jend = s_start[j + 1];
+      uint64_t h = 0;
+#pragma unroll
+      for (int k = 0; k < RS_IT; ++k) {
+        const int64_t q = q0 + k;
+        if (q < vbeg || q >= vend) continue;
+        if (q >= jend) {
+          if (h) atomicAdd(&s_hash[j], (unsigned long long)h);
+          h = 0;
+          do { ++j; jend = s_start[j + 1]; } while (q >= jend);
+        }
+        const int64_t st = s_start[j];
+        if (s_mism[j] == 0u && __ldg(val + q - s_len[j]) != v[k]) s_mism[j] = 1u;
+        h += elem_hash(v[k], q - st, fi);
+      }
+      if (h) atomicAdd(&s_hash[j], (unsigned long long)h);
     }
     __syncthreads();
   }
