@@ -567,7 +567,7 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
     note_launch();
   }
   // 2-5
-  int rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, {
+  int rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, 0, {
     const int ncb = col_blocks<C>(dim);
     const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(B * F * ncb, 8), (int64_t)num_sms() * 16);
     k_grad_u<C><<<grid, 256, 0, stream>>>(p);

@@ -71,19 +71,32 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // cp.async (LDGSTS): asynchronous global -> shared copy of 4/8/16 bytes per
 // thread; in-flight copies hold no registers, so a warp can keep many table
 // rows in flight.  Completion is per thread via commit/wait groups.
+#ifndef RECD_CPASYNC_CLOBBER
+#define RECD_CPASYNC_CLOBBER 0
+#endif
+#if RECD_CPASYNC_CLOBBER
+#define RECD_CLOB : "memory"
+#else
+#define RECD_CLOB
+#endif
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   if constexpr (BYTES == 16) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) RECD_CLOB);
   } else {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES)
+                 RECD_CLOB);
   }
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" :: RECD_CLOB);
+}
+// Waits for this thread's older copy groups.  The shared-memory reads that
+// follow are ordinary loads issued after the asm volatile in program order.
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // Block-wide exclusive scan of one int64 per thread; returns the exclusive

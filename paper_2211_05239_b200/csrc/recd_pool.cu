@@ -17,6 +17,7 @@
 #define RECD_POOL_MINB 2
 #endif
 
+
 namespace recd {
 
 struct PoolParams {
@@ -185,7 +186,7 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
     }
     bool any_expand = false;
     for (int f = 0; f < p.F; ++f) any_expand |= (p.out[f] != nullptr && p.out[f] != p.pooled[f]);
-    int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, {
+    int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, 1, {
       const unsigned grid = grid_for(batch_size * p.F * col_blocks<C>(dim));
       k_pool_fwd<C><<<grid, 256, 0, stream>>>(p);
       note_launch();

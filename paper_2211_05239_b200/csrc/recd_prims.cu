@@ -67,12 +67,22 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_up(const __grid_constant__ Sor
   __syncthreads();
   const uint32_t mask = (1u << p.nbits) - 1u;
   const uint32_t* k = p.kin + sg.base;
-  for (int64_t j0 = lo; j0 < hi; j0 += SORT_NT) {
-    const int64_t j = j0 + threadIdx.x;
-    const bool valid = j < hi;
-    const uint32_t d = valid ? ((k[j] >> p.shift) & mask) : 0x100u;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    if (valid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[d], (uint32_t)__popc(peers));
+  constexpr int U = 8;  // loads in flight per thread
+  for (int64_t j0 = lo; j0 < hi; j0 += SORT_NT * U) {
+    uint32_t kk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * SORT_NT + threadIdx.x;
+      kk[u] = j < hi ? __ldg(k + j) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * SORT_NT + threadIdx.x;
+      const bool valid = j < hi;
+      const uint32_t d = valid ? ((kk[u] >> p.shift) & mask) : 0x100u;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      if (valid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[d], (uint32_t)__popc(peers));
+    }
   }
   __syncthreads();
   p.hist[sg.hbase + (int64_t)threadIdx.x * sg.nchunks + c] = sh[threadIdx.x];
@@ -150,11 +160,15 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_down(const __grid_constant__ S
     __syncwarp();
     uint32_t key[SORT_ITEMS], val[SORT_ITEMS], rank[SORT_ITEMS];
 #pragma unroll
+    for (int r = 0; r < SORT_ITEMS; ++r) {  // all loads first: 16 in flight per thread
+      const int e = warp * (SORT_TILE / (SORT_NT / 32)) + r * 32 + lane;
+      key[r] = e < tn ? __ldg(kin + tlo + e) : 0u;
+      val[r] = e < tn ? __ldg(vin + tlo + e) : 0u;
+    }
+#pragma unroll
     for (int r = 0; r < SORT_ITEMS; ++r) {
       const int e = warp * (SORT_TILE / (SORT_NT / 32)) + r * 32 + lane;
       const bool valid = e < tn;
-      key[r] = valid ? kin[tlo + e] : 0u;
-      val[r] = valid ? vin[tlo + e] : 0u;
       const uint32_t d = valid ? ((key[r] >> p.shift) & mask) : 0x100u;
       const unsigned peers = __match_any_sync(0xffffffffu, d);
       uint32_t before = 0;

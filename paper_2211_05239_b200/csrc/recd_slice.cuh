@@ -14,10 +14,11 @@
 
 namespace recd {
 
-template <int VW_>
+template <int VW_, bool FULL_ = false>
 struct Col {
   static constexpr int VW = VW_;
-  static constexpr int CB = 32 * VW;  // floats per column block
+  static constexpr bool FULL = FULL_;  // D is a multiple of CB: every lane is in range
+  static constexpr int CB = 32 * VW;   // floats per column block
 
   __device__ __forceinline__ static void zero(float (&x)[VW]) {
 #pragma unroll
@@ -26,7 +27,7 @@ struct Col {
   // p points at this lane's first float; ok = lane's slice lies inside the row.
   // Read-only path: tables are never written by the kernels that use it.
   __device__ __forceinline__ static void ld(const float* __restrict__ p, bool ok, float (&x)[VW]) {
-    if (!ok) {
+    if (!FULL && !ok) {
       zero(x);
       return;
     }
@@ -42,7 +43,7 @@ struct Col {
   }
   // coherent load, for rows that are read-modify-written
   __device__ __forceinline__ static void ld_rw(const float* p, bool ok, float (&x)[VW]) {
-    if (!ok) {
+    if (!FULL && !ok) {
       zero(x);
       return;
     }
@@ -57,7 +58,7 @@ struct Col {
     }
   }
   __device__ __forceinline__ static void st(float* p, bool ok, const float (&x)[VW]) {
-    if (!ok) return;
+    if (!FULL && !ok) return;
     if constexpr (VW == 4) {
       *reinterpret_cast<float4*>(p) = make_float4(x[0], x[1], x[2], x[3]);
     } else if constexpr (VW == 2) {
@@ -91,12 +92,14 @@ __host__ __device__ __forceinline__ int col_blocks(int D) {
 
 // Dispatch D -> Col type: float4 lanes (one 512-byte row slice per warp load)
 // when D % 4 == 0 and D >= 64, float2 lanes when D is even, else scalars.
-#define RECD_DISPATCH_COL(D, ...) RECD_DISPATCH_COL_VW(D, 4, __VA_ARGS__)
-#define RECD_DISPATCH_COL_VW(D, MAXVW, ...)                     \
+#define RECD_DISPATCH_COL(D, ...) RECD_DISPATCH_COL_VW(D, 4, 1, __VA_ARGS__)
+#define RECD_DISPATCH_COL_VW(D, MAXVW, FULLOK, ...)             \
   [&]() -> int {                                                \
     const int _d = (D);                                         \
     if (_d <= 0) return RECD_ERR_ARG;                           \
-    if ((MAXVW) >= 4 && _d % 4 == 0 && _d >= 64) { using C = ::recd::Col<4>; __VA_ARGS__ } \
+    if ((FULLOK) && (MAXVW) >= 4 && _d % 128 == 0) { using C = ::recd::Col<4, true>; __VA_ARGS__ } \
+    else if ((MAXVW) >= 4 && _d % 4 == 0 && _d >= 64) { using C = ::recd::Col<4>; __VA_ARGS__ } \
+    else if ((FULLOK) && _d % 64 == 0) { using C = ::recd::Col<2, true>; __VA_ARGS__ } \
     else if (_d % 2 == 0) { using C = ::recd::Col<2>; __VA_ARGS__ } \
     else { using C = ::recd::Col<1>; __VA_ARGS__ }              \
     return RECD_OK;                                             \
@@ -115,7 +118,15 @@ __host__ __device__ __forceinline__ int col_blocks(int D) {
 // ---------------------------------------------------------------------------
 template <class C, class Row>
 __device__ __forceinline__ void ld_row(Row& row, int64_t j, bool ok, float (&x)[C::VW]) {
-  C::ld(row(j), ok, x);
+  row.template fetch<C>(j, ok, x);
+}
+// predicated variant: the row address (ID shuffle) is computed by the whole
+// warp unconditionally, only the load is predicated -- no divergent region
+template <class C, class Row>
+__device__ __forceinline__ void ld_row_if(Row& row, int64_t j, bool pred, bool ok,
+                                          float (&x)[C::VW]) {
+  const float* pt = row(j);
+  if (pred) C::ld(pt, ok, x);
 }
 
 template <class C, class Row>
@@ -127,8 +138,7 @@ __device__ __forceinline__ void leaf_sum(Row& row, int64_t a, int64_t m, bool ok
   if (m < 8) {
     row.need(a, (int)m);
 #pragma unroll
-    for (int t = 0; t < 7; ++t)
-      if (t < m) ld(a + t, x[t]);
+    for (int t = 0; t < 7; ++t) ld_row_if<C>(row, a + t, t < m, ok, x[t]);
 #pragma unroll
     for (int e = 0; e < V; ++e) s[e] = -0.0f;
 #pragma unroll
@@ -160,8 +170,7 @@ __device__ __forceinline__ void leaf_sum(Row& row, int64_t a, int64_t m, bool ok
   const int tail = (int)(m - mb);
   if (tail) row.need(a + mb, tail);
 #pragma unroll
-  for (int t = 0; t < 7; ++t)
-    if (t < tail) ld(a + mb + t, x[t]);
+  for (int t = 0; t < 7; ++t) ld_row_if<C>(row, a + mb + t, t < tail, ok, x[t]);
 #pragma unroll
   for (int t = 0; t < 7; ++t)
     if (t < tail) {
@@ -234,14 +243,13 @@ __device__ __forceinline__ void pool_row(Row& row, int64_t a, int64_t n, int mod
     return;
   }
   row.need(a, 1);
-  C::ld(row(a), ok, out);
+  row.template fetch<C>(a, ok, out);
   if (mode == RECD_POOL_MAX) {
     float x[8][V];
     for (int64_t i = 1; i < n; i += 8) {
       row.need(a + i, (int)min((int64_t)8, n - i));
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (i + k < n) C::ld(row(a + i + k), ok, x[k]);
+      for (int k = 0; k < 8; ++k) ld_row_if<C>(row, a + i + k, i + k < n, ok, x[k]);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
         if (i + k < n) {
@@ -304,6 +312,10 @@ struct TableRows {
     const uint32_t id = __shfl_sync(0xffffffffu, mine, (int)(j - base));
     return Wl + (uint64_t)id * D;
   }
+  template <class C>
+  __device__ __forceinline__ void fetch(int64_t j, bool ok, float (&x)[C::VW]) {
+    C::ld((*this)(j), ok, x);
+  }
 };
 
 // Warp-wide window of 32 consecutive uint32 values (lane l holds base + l).
@@ -331,6 +343,10 @@ struct DenseRows {
   int D;
   __device__ __forceinline__ void need(int64_t, int) {}
   __device__ __forceinline__ const float* operator()(int64_t j) const { return Al + j * (int64_t)D; }
+  template <class C>
+  __device__ __forceinline__ void fetch(int64_t j, bool ok, float (&x)[C::VW]) {
+    C::ld((*this)(j), ok, x);
+  }
 };
 
 // find segment f with pref[f] <= w < pref[f+1] (pref in shared memory)
