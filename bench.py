@@ -235,6 +235,9 @@ def main():
     import paper_2211_05239_b200 as R
     from paper_2211_05239_b200.step import TrainStep
 
+    if world > 1:
+        return run_sharded(args, world, rank, local, dev)
+
     t_setup = time.perf_counter()
     batch = make_batch(args, rank, world)
     keys = list(batch.keys)
@@ -397,6 +400,118 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_sharded(args, world, rank, local, dev):
+    """N > 1: row-sharded tables (owner = id mod N) + data-parallel batch;
+    each rank deduplicates its own 65,536-row chunk of the global batch and
+    the NCCL exchange carries only deduplicated IDs, partially pooled rows and
+    unique-row gradients (paper_2211_05239_b200/sharded.py)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_05239_b200 as R
+    from paper_2211_05239_b200.sharded import ShardedTrainStep, shard_rows
+
+    t_setup = time.perf_counter()
+    batch = make_batch(args, rank, world)
+    keys = list(batch.keys)
+    lrows = shard_rows(args.rows, world, rank)
+    tables = {k: R.EmbeddingTable.create_on_device(f"{k}/shard{rank}", lrows, args.dim, seed=i,
+                                                   device=dev) for i, k in enumerate(keys)}
+    caps = {k: batch.values[k].size for k in keys}
+    step = ShardedTrainStep(keys, args.batch, caps, tables, "sum", args.lr, device=dev)
+    step.load_batch(batch.values, batch.offsets)
+    step.fill_grad_out(1 + rank)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream(dev)
+    B, K, D = args.batch, len(keys), args.dim
+    for _ in range(max(1, args.warmup)):
+        step.run()
+    torch.cuda.synchronize()
+    U, N_u = step.host_counts()
+
+    sampler = ClockSampler(local) if not args.profile else None
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = R.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step.run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    clocks = sampler.stop() if sampler else None
+    launches_per_step = (R.launch_count() - launches0) // max(args.steps, 1)
+    t = torch.tensor([ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * B / (ms / 1e3)
+
+    # sub-phase breakdown (one traced step per rank, max over ranks)
+    step.trace = True
+    step.run()
+    ph = step.phase_ms()
+    step.trace = False
+    names = list(ph)
+    tph = torch.tensor([ph[n] for n in names], device=dev)
+    dist.all_reduce(tph, op=dist.ReduceOp.MAX)
+    ph = dict(zip(names, tph.tolist()))
+    # per-rank communication volume of the step (bytes sent)
+    pl = step.plan
+    sent = 8 * int(pl.send_ids.sum()) + 8 * world * int(pl.send_rows.sum())  # ids + row counts
+    sent += 4 * D * int(pl.recv_rows.sum())  # partial pooled rows returned
+    sent += 4 * D * world * int(pl.send_rows.sum())  # unique-row gradients
+    N_kjt = int(sum(caps.values()))
+
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        pin_v = {k: torch.from_numpy(batch.values[k]).pin_memory() for k in keys}
+        pin_o = {k: torch.from_numpy(batch.offsets[k]).pin_memory() for k in keys}
+        res = torch.empty(2 * K, dtype=torch.int64).pin_memory()
+        h2d = sum(pin_v[k].numel() * 8 + pin_o[k].numel() * 8 for k in keys)
+        n_e2e = max(3, min(args.steps, 10))
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            for f, k in enumerate(keys):
+                step.in_values[f][: pin_v[k].numel()].copy_(pin_v[k], non_blocking=True)
+                step.in_offsets[f].copy_(pin_o[k], non_blocking=True)
+            step.run()
+            res.copy_(step.counts, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+        e2e = {"value": world * B / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": res.numel() * 8, "ms_per_step": e2e_s * 1e3,
+               "how": "ShardedTrainStep on every rank: pinned-host KJT -> H2D -> step -> D2H "
+                      "of the dedup counts; max over ranks"}
+    if rank == 0:
+        cfg = config_dict(args, "gpu")
+        cfg["parallelism"] = f"dp{world} x row-sharded tables (owner = id mod {world})"
+        cfg["table_rows_per_rank"] = lrows
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (ids int64)", "data": "synthetic (restated reference session generator)",
+            "config": cfg, "phases_ms": ph,
+            "comm_bytes_sent_per_rank": sent,
+            "stats_rank0": {"N_kjt": N_kjt, "N_u": int(sum(N_u)), "U_tot": int(sum(U))},
+            "roofline": None, "cpu_baseline": None, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches_per_step": launches_per_step, "clocks": clocks, "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
     return 0
 
 

@@ -16,6 +16,13 @@
  *   recd_pool_bwd              <- (absent in the reference) segment-reduce
  *                                 onto unique rows + deterministic sorted scatter-add
  *                                 (+ fused SGD) into the tables
+ *   recd_grad_unique /         the two halves of recd_pool_bwd, used by the row-sharded
+ *   recd_sparse_sgd            multi-GPU step (grad onto unique rows at the source,
+ *                              sorted scatter-add + SGD at the table owner)
+ *   recd_shard_bucketize /     row-sharded tables over R ranks: deduplicated IDs per
+ *   recd_shard_combine         owner, owner-order sum of partially pooled rows
+ *                              (the reference only simulates ranks,
+ *                              trainer_sim.py:281-305)
  *   recd_jagged_index_select_* <- tensors.jagged_index_select   (tensors.py:363-390)
  *                                 and ikjt_to_kjt (tensors.py:393-399)
  *   recd_slice_renumber        <- trainer_sim.slice_ikjt_rows   (trainer_sim.py:394-413)
@@ -146,6 +153,60 @@ int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t
                   int32_t apply_sgd, int64_t* const* grad_ids_out, float* const* grad_rows_out,
                   int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
                   recd_stream_t stream);
+
+/* Source half: grad_u_out[f] ([U x dim]) = grad_u of recd_pool_bwd (avg scaled). */
+size_t recd_grad_unique_scratch_bytes(int32_t num_features, int64_t batch_size);
+int recd_grad_unique(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                     const int64_t* const* uoffsets, const int64_t* counts,
+                     const int64_t* const* inverse, const float* const* grad_out,
+                     float* const* grad_u_out, void* scratch, size_t scratch_bytes,
+                     recd_stream_t stream);
+
+/* Owner half: grad_rows[f] holds one gradient row per unique row of feature f
+ * (max_rows >= its row count, < 2^24); occurrences are reduced per ID in
+ * ascending (feature, row, position) order and applied like recd_pool_bwd. */
+size_t recd_sparse_sgd_scratch_bytes(int32_t num_features, const int64_t* value_caps);
+int recd_sparse_sgd(int32_t num_features, int64_t max_rows, int32_t dim, float* const* tables,
+                    const int64_t* table_rows, const int64_t* const* uvalues,
+                    const int64_t* const* uoffsets, const int64_t* value_caps,
+                    const int64_t* counts, const float* const* grad_rows, float lr,
+                    int32_t apply_sgd, int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                    int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                    recd_stream_t stream);
+
+/* ------------------------------------------------------- row sharding --
+ * owner(id) = id mod R, local row = id div R.
+ * bucketize: for every feature f, ids_out[f] = the local IDs of its unique
+ *   values grouped by owner (owner-major, then unique row, then position);
+ *   rowcnt_out[f][o * batch_size + u] = values of row u owned by o;
+ *   totals_out[f * R + o] (device) = IDs of f owned by o.
+ * combine:   pooled_out[f][u] = sum over o = 0..R-1 (in that order) of
+ *   partial[f][(o * batch_size + u) * dim ...]; avg divides by the row length. */
+size_t recd_shard_scratch_bytes(int32_t num_features, int32_t num_ranks, int64_t batch_size);
+int recd_shard_bucketize(int32_t num_features, int32_t num_ranks, int64_t batch_size,
+                         const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                         const int64_t* counts, int64_t* const* ids_out, int64_t* const* rowcnt_out,
+                         int64_t* totals_out, void* scratch, size_t scratch_bytes,
+                         recd_stream_t stream);
+int recd_shard_combine(int32_t num_features, int32_t num_ranks, int64_t batch_size, int32_t dim,
+                       int32_t mode, const float* const* partial, const int64_t* const* uoffsets,
+                       const int64_t* counts, float* const* pooled_out, recd_stream_t stream);
+
+/* Batched copy of num_segments (src, dst, bytes) device segments in one
+ * launch (packing of exchange buffers).  host_staging / descs: a host and a
+ * device buffer of recd_batched_copy_desc_bytes(num_segments) bytes; the
+ * segment table goes host_staging -> descs with one async copy, so
+ * host_staging must stay untouched until the stream reaches this call. */
+size_t recd_batched_copy_desc_bytes(int32_t num_segments);
+int recd_batched_copy(int32_t num_segments, const void* const* src, void* const* dst,
+                      const int64_t* bytes, void* host_staging, void* descs, recd_stream_t stream);
+
+/* Segmented exclusive scan of int64 (segment s: caps[s] entries, or
+ * device_counts[s] when device_counts is not NULL); totals_out nullable. */
+size_t recd_exclusive_scan_scratch_bytes(int32_t num_segments, const int64_t* caps);
+int recd_exclusive_scan(int32_t num_segments, const int64_t* const* in, int64_t* const* out,
+                        const int64_t* caps, const int64_t* device_counts, int64_t* totals_out,
+                        void* scratch, size_t scratch_bytes, recd_stream_t stream);
 
 /* --------------------------------------------------- jagged index select --
  * Output row k of feature f = input row indices[k] (same indices for every

@@ -47,6 +47,19 @@ _SIGS = {
     "recd_pool_bwd_scratch_bytes": (_sz, [_i32, _i64, _i32, _p64]),
     "recd_pool_bwd": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _pp,
                              _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_grad_unique_scratch_bytes": (_sz, [_i32, _i64]),
+    "recd_grad_unique": (_i32, [_i32, _i64, _i32, _i32, _pp, _vp, _pp, _pp, _pp, _vp, _sz, _vp]),
+    "recd_sparse_sgd_scratch_bytes": (_sz, [_i32, _p64]),
+    "recd_sparse_sgd": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _f32, _i32,
+                               _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_shard_scratch_bytes": (_sz, [_i32, _i32, _i64]),
+    "recd_shard_bucketize": (_i32, [_i32, _i32, _i64, _pp, _pp, _vp, _pp, _pp, _vp, _vp, _sz,
+                                    _vp]),
+    "recd_shard_combine": (_i32, [_i32, _i32, _i64, _i32, _i32, _pp, _pp, _vp, _pp, _vp]),
+    "recd_batched_copy_desc_bytes": (_sz, [_i32]),
+    "recd_batched_copy": (_i32, [_i32, _pp, _pp, _p64, _vp, _vp, _vp]),
+    "recd_exclusive_scan_scratch_bytes": (_sz, [_i32, _p64]),
+    "recd_exclusive_scan": (_i32, [_i32, _pp, _pp, _p64, _vp, _vp, _vp, _sz, _vp]),
     "recd_jagged_scratch_bytes": (_sz, [_i32, _i64]),
     "recd_jagged_index_select_plan": (_i32, [_i32, _pp, _i64, _p64, _vp, _i64, _pp, _vp, _vp,
                                              _vp, _sz, _vp]),

@@ -10,7 +10,7 @@
 // Steps (one launch per phase for every feature of the step):
 //   1 inverse CSR  : stable radix sort of (inv[i], i) per group  -> rows of u
 //   2 k_grad_u     : worker per unique row, ordered segment reduce
-//   3 k_occ        : (ID, feature*B + u) pairs of every unique value, laid out
+//   3 k_occ        : (ID, (feature << 24) | u) pairs of every unique value, laid out
 //                    per table (features sharing a table are concatenated)
 //   4 radix sort   : stable by ID within each table segment
 //   5 k_scatter    : warp per (256-position chunk of the sorted pairs, column
@@ -70,9 +70,10 @@ struct BwdParams {
   uint32_t* inv_keys;     // [nis][B] sorted
   uint32_t* inv_rows;     // [nis][B]
   int32_t* csr_start;     // [nis][B + 1]
-  float* grad_u;          // [F][B][D]
+  float* gout[RECD_MAX_FEAT];         // grad_u destination per feature ([U x D])
+  const float* grow[RECD_MAX_FEAT];   // unique-row gradients read by the scatter
   uint32_t* occ_keys;     // sorted occurrence IDs
-  uint32_t* occ_vals;     // f * B + u
+  uint32_t* occ_vals;     // tag = (f << 24) | u
   int64_t* run_part;      // [total_rc_chunks] exclusive run counts (grad-output mode)
 };
 
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
         for (int k = 0; k < V; ++k) acc[k] = __fdiv_rn(acc[k], fl);
       }
     }
-    C::st(p.grad_u + ((int64_t)f * p.B + u) * p.D + cw.lo, cw.ok, acc);
+    C::st(p.gout[f] + u * p.D + cw.lo, cw.ok, acc);
   }
 }
 
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
     const int64_t* uo = p.uoffsets[f];
     const int64_t a = uo[u], e = (u + 1 < U) ? uo[u + 1] : NV;
     const int64_t dst = p.ts_base[p.feat_ts[f]] + p.feat_base[f];
-    const uint32_t tag = (uint32_t)((int64_t)f * p.B + u);
+    const uint32_t tag = ((uint32_t)f << 24) | (uint32_t)u;
     const int64_t* vals_f = p.uvalues[f];
     for (int64_t j = a + lane; j < e; j += 32) {
       keys[dst + j] = (uint32_t)vals_f[j];
@@ -291,7 +292,6 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
     if (nruns == 0) continue;
     const int64_t pend = run_end(K, hi, n, rids[nruns - 1], lane);  // end of the last run
     float* table = p.table[s] + lo_f;
-    const float* gu = p.grad_u + lo_f;
     // 2. prefetch the table rows of the first SC_RS runs
     if (apply) {
 #pragma unroll
@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const uint32_t vv = vwin.get(k0 + t);
-        if (k0 + t < pend) C::ld(gu + (uint64_t)vv * D32, ok, x[t]);
+        if (k0 + t < pend)
+          C::ld(p.grow[vv >> 24] + (uint64_t)(vv & 0xffffffu) * D32 + lo_f, ok, x[t]);
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
@@ -423,30 +424,39 @@ struct BwdScratch {
   uint32_t *occ_k0, *occ_v0, *occ_k1, *occ_v1;
 };
 
-size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdScratch* s) {
+enum { NEED_INV = 1, NEED_GRADU = 2, NEED_OCC = 4 };
+
+size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdScratch* s,
+                 int need = NEED_INV | NEED_GRADU | NEED_OCC) {
   Arena a(base, cap);
   s->feat_base = a.take<int64_t>(RECD_MAX_FEAT);
   s->seg_count = a.take<int64_t>(RECD_MAX_FEAT);
   s->is_count = a.take<int64_t>(RECD_MAX_FEAT);
-  s->run_part = a.take<int64_t>(pl.rc_chunks);
-  const size_t nib = (size_t)std::max(pl.nis, 1) * B;
+  s->run_part = a.take<int64_t>((need & NEED_OCC) ? pl.rc_chunks : 1);
+  const size_t nib = (need & NEED_INV) ? (size_t)std::max(pl.nis, 1) * B : 1;
   s->inv_k0 = a.take<uint32_t>(nib);
   s->inv_v0 = a.take<uint32_t>(nib);
   s->inv_k1 = a.take<uint32_t>(nib);
   s->inv_v1 = a.take<uint32_t>(nib);
-  s->csr_start = a.take<int32_t>((size_t)std::max(pl.nis, 1) * (B + 1));
-  s->grad_u = a.take<float>((size_t)pl.F * B * D);
-  s->occ_k0 = a.take<uint32_t>(pl.occ_total);
-  s->occ_v0 = a.take<uint32_t>(pl.occ_total);
-  s->occ_k1 = a.take<uint32_t>(pl.occ_total);
-  s->occ_v1 = a.take<uint32_t>(pl.occ_total);
+  s->csr_start = a.take<int32_t>((need & NEED_INV) ? (size_t)std::max(pl.nis, 1) * (B + 1) : 1);
+  s->grad_u = a.take<float>((need & NEED_GRADU) ? (size_t)pl.F * B * D : 1);
+  const size_t occ = (need & NEED_OCC) ? (size_t)pl.occ_total : 1;
+  s->occ_k0 = a.take<uint32_t>(occ);
+  s->occ_v0 = a.take<uint32_t>(occ);
+  s->occ_k1 = a.take<uint32_t>(occ);
+  s->occ_v1 = a.take<uint32_t>(occ);
   // sort histograms: max of the inverse sort and the table sort
   std::vector<SegDesc> segs;
-  for (int i = 0; i < pl.nis; ++i) segs.push_back({(int64_t)i * B, B, nullptr});
-  int64_t hw = segs.empty() ? 0 : sort_hist_words(segs.data(), (int)segs.size());
+  int64_t hw = 0;
+  if (need & NEED_INV) {
+    for (int i = 0; i < pl.nis; ++i) segs.push_back({(int64_t)i * B, B, nullptr});
+    if (!segs.empty()) hw = sort_hist_words(segs.data(), (int)segs.size());
+  }
   segs.clear();
-  for (int t = 0; t < pl.nts; ++t) segs.push_back({pl.ts_base[t], pl.ts_cap[t], nullptr});
-  hw = std::max(hw, sort_hist_words(segs.data(), (int)segs.size()));
+  if (need & NEED_OCC) {
+    for (int t = 0; t < pl.nts; ++t) segs.push_back({pl.ts_base[t], pl.ts_cap[t], nullptr});
+    hw = std::max(hw, sort_hist_words(segs.data(), (int)segs.size()));
+  }
   s->hist = a.take<uint32_t>(std::max<int64_t>(hw, 256));
   // run-count scan partials (one scan segment per table)
   std::vector<ScanDesc> sd;
@@ -458,47 +468,49 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   return a.used;
 }
 
-}  // namespace
+// Shared driver of the three backward entry points.
+//   full    : grad_u (scratch) -> occurrences -> sort -> scatter
+//   grad    : grad_u written to caller buffers only
+//   scatter : occurrences -> sort -> scatter, reading caller unique-row grads
+enum class BwdMode { Full, GradOnly, ScatterOnly };
 
-extern "C" size_t recd_pool_bwd_scratch_bytes(int32_t num_features, int64_t batch_size,
-                                              int32_t dim, const int64_t* value_caps) {
-  if (num_features <= 0 || num_features > RECD_MAX_FEAT) return 0;
-  // worst case: every feature has its own inverse and its own table
-  std::vector<const int64_t*> inv(num_features);
-  std::vector<float*> tab(num_features);
-  std::vector<int64_t> rows(num_features, 1);
-  for (int f = 0; f < num_features; ++f) {
-    inv[f] = reinterpret_cast<const int64_t*>((uintptr_t)(f + 1) * 64);
-    tab[f] = reinterpret_cast<float*>((uintptr_t)(f + 1) * 64);
-  }
-  Plan pl = make_plan(num_features, inv.data(), tab.data(), rows.data(), value_caps);
-  BwdScratch s;
-  return carve_bwd(nullptr, 0, pl, batch_size, dim, &s);
-}
-
-extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
-                             float* const* tables, const int64_t* table_rows,
-                             const int64_t* const* uvalues, const int64_t* const* uoffsets,
-                             const int64_t* value_caps, const int64_t* counts,
-                             const int64_t* const* inverse, const float* const* grad_out,
-                             float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
-                             float* const* grad_rows_out, int64_t* grad_counts_out,
-                             void* scratch, size_t scratch_bytes, recd_stream_t stream_) {
-  cudaStream_t stream = (cudaStream_t)stream_;
-  const int F = num_features;
-  const int64_t B = batch_size;
+int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* tables,
+            const int64_t* table_rows, const int64_t* const* uvalues,
+            const int64_t* const* uoffsets, const int64_t* value_caps, const int64_t* counts,
+            const int64_t* const* inverse, const float* const* grad_out, float* const* gout_ext,
+            const float* const* grow_ext, float lr, int apply_sgd, int64_t* const* grad_ids_out,
+            float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
+            size_t scratch_bytes, cudaStream_t stream) {
   if (F <= 0 || F > RECD_MAX_FEAT || B <= 0 || dim <= 0 || !counts) return RECD_ERR_ARG;
   if (mode != RECD_POOL_SUM && mode != RECD_POOL_AVG) return RECD_ERR_UNSUPPORTED;
-  if ((int64_t)F * B >= (1ll << 32)) return RECD_ERR_UNSUPPORTED;
+  if (B >= (1ll << 24)) return RECD_ERR_UNSUPPORTED;  // occurrence tags hold u in 24 bits
+  const bool do_grad = bm != BwdMode::ScatterOnly;
+  const bool do_scatter = bm != BwdMode::GradOnly;
+  std::vector<float*> dummy_tables(F, nullptr);
+  std::vector<int64_t> dummy_rows(F, 1), dummy_caps(F, 1);
   for (int f = 0; f < F; ++f) {
-    if (!tables[f] || !uoffsets[f] || !grad_out[f]) return RECD_ERR_ARG;
-    if (table_rows[f] <= 0 || table_rows[f] > (1ll << 32)) return RECD_ERR_UNSUPPORTED;
+    if (!uoffsets[f]) return RECD_ERR_ARG;
+    if (do_grad && !grad_out[f]) return RECD_ERR_ARG;
+    if (bm == BwdMode::GradOnly && !gout_ext[f]) return RECD_ERR_ARG;
+    if (bm == BwdMode::ScatterOnly && !grow_ext[f]) return RECD_ERR_ARG;
+    if (do_scatter) {
+      if (!tables[f]) return RECD_ERR_ARG;
+      if (table_rows[f] <= 0 || table_rows[f] > (1ll << 32)) return RECD_ERR_UNSUPPORTED;
+    } else {
+      // grad-only: every feature its own (unused) table segment
+      dummy_tables[f] = reinterpret_cast<float*>((uintptr_t)(f + 1) * 64);
+    }
   }
-  Plan pl = make_plan(F, inverse, const_cast<float**>(tables), table_rows, value_caps);
+  Plan pl = make_plan(F, do_grad ? inverse : nullptr, do_scatter ? tables : dummy_tables.data(),
+                      do_scatter ? table_rows : dummy_rows.data(),
+                      do_scatter ? value_caps : dummy_caps.data());
   if (pl.occ_total >= (1ll << 32)) return RECD_ERR_UNSUPPORTED;
-  if (!apply_sgd && (!grad_ids_out || !grad_rows_out || !grad_counts_out)) return RECD_ERR_ARG;
+  if (do_scatter && !apply_sgd && (!grad_ids_out || !grad_rows_out || !grad_counts_out))
+    return RECD_ERR_ARG;
+  const int need = (do_grad ? NEED_INV : 0) | (bm == BwdMode::Full ? NEED_GRADU : 0) |
+                   (do_scatter ? NEED_OCC : 0);
   BwdScratch sc;
-  if (carve_bwd(scratch, scratch_bytes, pl, B, dim, &sc) > scratch_bytes) return RECD_ERR_SCRATCH;
+  if (carve_bwd(scratch, scratch_bytes, pl, B, dim, &sc, need) > scratch_bytes) return RECD_ERR_SCRATCH;
 
   BwdParams p;
   memset(&p, 0, sizeof(p));
@@ -513,11 +525,19 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
   p.counts = counts;
   p.Ftot = F;
   for (int f = 0; f < F; ++f) {
-    p.uvalues[f] = uvalues[f];
+    p.uvalues[f] = uvalues ? uvalues[f] : nullptr;
     p.uoffsets[f] = uoffsets[f];
-    p.grad_out[f] = grad_out[f];
+    p.grad_out[f] = do_grad ? grad_out[f] : nullptr;
     p.feat_is[f] = pl.feat_is[f];
     p.feat_ts[f] = pl.feat_ts[f];
+    if (bm == BwdMode::Full) {
+      p.gout[f] = sc.grad_u + (int64_t)f * B * dim;
+      p.grow[f] = p.gout[f];
+    } else if (bm == BwdMode::GradOnly) {
+      p.gout[f] = gout_ext[f];
+    } else {
+      p.grow[f] = grow_ext[f];
+    }
   }
   for (int s = 0; s < pl.nis; ++s) {
     p.inverse[s] = pl.inverse[s];
@@ -531,7 +551,7 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
     p.table[s] = pl.table[s];
     p.ts_base[s] = pl.ts_base[s];
     p.ts_chunk0[s] = pl.ts_chunk0[s];
-    if (!apply_sgd) {
+    if (do_scatter && !apply_sgd) {
       const int f = first_feat_of_ts[s];
       p.grad_ids[s] = grad_ids_out[f];
       p.grad_rows[s] = grad_rows_out[f];
@@ -543,15 +563,15 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
   p.seg_count = sc.seg_count;
   p.is_count = sc.is_count;
   p.csr_start = sc.csr_start;
-  p.grad_u = sc.grad_u;
   p.run_part = sc.run_part;
 
   k_bwd_setup<<<1, 32, 0, stream>>>(p);
   note_launch();
-  if (!apply_sgd) RECD_CUDA_CHECK(cudaMemsetAsync(grad_counts_out, 0, sizeof(int64_t) * F, stream));
+  if (do_scatter && !apply_sgd)
+    RECD_CUDA_CHECK(cudaMemsetAsync(grad_counts_out, 0, sizeof(int64_t) * F, stream));
 
   // 1. inverse CSR
-  if (pl.nis > 0) {
+  if (do_grad && pl.nis > 0) {
     const int64_t n = (int64_t)pl.nis * B;
     k_inv_pairs<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p, sc.inv_k0, sc.inv_v0);
     note_launch();
@@ -569,39 +589,120 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
   // 2-5
   int rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, 0, {
     const int ncb = col_blocks<C>(dim);
-    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(B * F * ncb, 8), (int64_t)num_sms() * 16);
-    k_grad_u<C><<<grid, 256, 0, stream>>>(p);
-    k_occ<<<num_sms() * 4, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
-    note_launch(2);
-    std::vector<SegDesc> segs;
-    int64_t maxrows = 1;
-    for (int s = 0; s < pl.nts; ++s) {
-      segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
-      maxrows = std::max(maxrows, pl.table_rows[s]);
-    }
-    bool alt = false;
-    int r2 = seg_sort_pairs(segs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
-                            sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream);
-    if (r2 != RECD_OK) return r2;
-    p.occ_keys = alt ? sc.occ_k1 : sc.occ_k0;
-    p.occ_vals = alt ? sc.occ_v1 : sc.occ_v0;
-    if (!apply_sgd) {
-      k_run_count<<<(unsigned)pl.rc_chunks, RC, 0, stream>>>(p);
+    if (do_grad) {
+      const unsigned grid =
+          (unsigned)std::min<int64_t>(ceil_div(B * F * ncb, 8), (int64_t)num_sms() * 16);
+      k_grad_u<C><<<grid, 256, 0, stream>>>(p);
       note_launch();
-      std::vector<ScanDesc> sd;
-      for (int s = 0; s < pl.nts; ++s) {
-        const int64_t nch = std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RC));
-        sd.push_back({sc.run_part + pl.ts_chunk0[s], sc.run_part + pl.ts_chunk0[s], nch, nullptr,
-                      p.grad_count[s]});
-      }
-      int r3 = seg_exclusive_scan(sd.data(), (int)sd.size(), sc.scan_part, stream);
-      if (r3 != RECD_OK) return r3;
     }
-    const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks * ncb, 8), (int64_t)num_sms() * 16);
-    k_scatter<C><<<std::max(g2, 1u), 256, 0, stream>>>(p);
-    note_launch();
+    if (do_scatter) {
+      k_occ<<<num_sms() * 4, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
+      note_launch();
+      std::vector<SegDesc> segs;
+      int64_t maxrows = 1;
+      for (int s = 0; s < pl.nts; ++s) {
+        segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
+        maxrows = std::max(maxrows, pl.table_rows[s]);
+      }
+      bool alt = false;
+      int r2 = seg_sort_pairs(segs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
+                              sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream);
+      if (r2 != RECD_OK) return r2;
+      p.occ_keys = alt ? sc.occ_k1 : sc.occ_k0;
+      p.occ_vals = alt ? sc.occ_v1 : sc.occ_v0;
+      if (!apply_sgd) {
+        k_run_count<<<(unsigned)pl.rc_chunks, RC, 0, stream>>>(p);
+        note_launch();
+        std::vector<ScanDesc> sd;
+        for (int s = 0; s < pl.nts; ++s) {
+          const int64_t nch = std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RC));
+          sd.push_back({sc.run_part + pl.ts_chunk0[s], sc.run_part + pl.ts_chunk0[s], nch,
+                        nullptr, p.grad_count[s]});
+        }
+        int r3 = seg_exclusive_scan(sd.data(), (int)sd.size(), sc.scan_part, stream);
+        if (r3 != RECD_OK) return r3;
+      }
+      const unsigned g2 =
+          (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks * ncb, 8), (int64_t)num_sms() * 16);
+      k_scatter<C><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+      note_launch();
+    }
   });
   if (rc != RECD_OK) return rc;
   RECD_LAUNCH_CHECK();
   return RECD_OK;
+}
+
+Plan worst_plan(int F, const int64_t* caps) {
+  // worst case: every feature has its own inverse and its own table
+  std::vector<const int64_t*> inv(F);
+  std::vector<float*> tab(F);
+  std::vector<int64_t> rows(F, 1), ones(F, 1);
+  for (int f = 0; f < F; ++f) {
+    inv[f] = reinterpret_cast<const int64_t*>((uintptr_t)(f + 1) * 64);
+    tab[f] = reinterpret_cast<float*>((uintptr_t)(f + 1) * 64);
+  }
+  return make_plan(F, inv.data(), tab.data(), rows.data(), caps ? caps : ones.data());
+}
+
+}  // namespace
+
+extern "C" size_t recd_pool_bwd_scratch_bytes(int32_t num_features, int64_t batch_size,
+                                              int32_t dim, const int64_t* value_caps) {
+  if (num_features <= 0 || num_features > RECD_MAX_FEAT) return 0;
+  Plan pl = worst_plan(num_features, value_caps);
+  BwdScratch s;
+  return carve_bwd(nullptr, 0, pl, batch_size, dim, &s);
+}
+
+extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                             float* const* tables, const int64_t* table_rows,
+                             const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                             const int64_t* value_caps, const int64_t* counts,
+                             const int64_t* const* inverse, const float* const* grad_out,
+                             float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
+                             float* const* grad_rows_out, int64_t* grad_counts_out,
+                             void* scratch, size_t scratch_bytes, recd_stream_t stream) {
+  return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
+                 uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
+                 grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
+                 (cudaStream_t)stream);
+}
+
+extern "C" size_t recd_grad_unique_scratch_bytes(int32_t num_features, int64_t batch_size) {
+  if (num_features <= 0 || num_features > RECD_MAX_FEAT) return 0;
+  Plan pl = worst_plan(num_features, nullptr);
+  BwdScratch s;
+  return carve_bwd(nullptr, 0, pl, batch_size, 1, &s, NEED_INV);
+}
+
+extern "C" int recd_grad_unique(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                                const int64_t* const* uoffsets, const int64_t* counts,
+                                const int64_t* const* inverse, const float* const* grad_out,
+                                float* const* grad_u_out, void* scratch, size_t scratch_bytes,
+                                recd_stream_t stream) {
+  return run_bwd(BwdMode::GradOnly, num_features, batch_size, dim, mode, nullptr, nullptr, nullptr,
+                 uoffsets, nullptr, counts, inverse, grad_out, grad_u_out, nullptr, 0.f, 1,
+                 nullptr, nullptr, nullptr, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+extern "C" size_t recd_sparse_sgd_scratch_bytes(int32_t num_features, const int64_t* value_caps) {
+  if (num_features <= 0 || num_features > RECD_MAX_FEAT) return 0;
+  Plan pl = worst_plan(num_features, value_caps);
+  BwdScratch s;
+  return carve_bwd(nullptr, 0, pl, 1, 1, &s, NEED_OCC);
+}
+
+extern "C" int recd_sparse_sgd(int32_t num_features, int64_t max_rows, int32_t dim,
+                               float* const* tables, const int64_t* table_rows,
+                               const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                               const int64_t* value_caps, const int64_t* counts,
+                               const float* const* grad_rows, float lr, int32_t apply_sgd,
+                               int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                               int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                               recd_stream_t stream) {
+  return run_bwd(BwdMode::ScatterOnly, num_features, max_rows, dim, RECD_POOL_SUM, tables,
+                 table_rows, uvalues, uoffsets, value_caps, counts, nullptr, nullptr, nullptr,
+                 grad_rows, lr, apply_sgd, grad_ids_out, grad_rows_out, grad_counts_out, scratch,
+                 scratch_bytes, (cudaStream_t)stream);
 }

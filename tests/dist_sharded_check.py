@@ -1,0 +1,112 @@
+"""Multi-GPU parity check of the row-sharded step (run under torchrun).
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/dist_sharded_check.py
+
+Each rank deduplicates its contiguous chunk of one global session-clustered
+batch and owns rows id % R == rank of every table.  Checked against the CPU
+oracle (oracle/), on the same inputs:
+  * dedup outputs (inverse, unique values/offsets): bit-exact
+  * expanded pooled outputs: allclose(rtol=1e-5, atol=1e-5 * max|ref|)
+  * updated tables (gathered from all shards) vs the oracle SGD over the whole
+    global batch: same tolerance on the update.
+Prints one JSON line per rank; exits 1 on a mismatch.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_2211_05239_b200 as R  # noqa: E402
+from paper_2211_05239_b200.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
+                                           generate_clustered_batch)
+from paper_2211_05239_b200.sharded import ShardedTrainStep, shard_rows  # noqa: E402
+
+
+def close(a, b):
+    scale = max(float(np.abs(b).max()), 1e-30)
+    return bool(np.allclose(a, b, rtol=1e-5, atol=1e-5 * scale)), float(np.abs(a - b).max() / scale)
+
+
+def main():
+    op = os.environ.get("POOL_OP", "sum")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    world, rank = dist.get_world_size(), dist.get_rank()
+    B, D, rows, lr = 1500, 64, 3000, 0.05
+    specs = [FeatureSpec("k0", "user_sequence", 4.0, rows, 0.3),
+             FeatureSpec("k1", "user_sequence", 16.0, rows, 0.3),
+             FeatureSpec("k2", "user_sequence", 40.0, rows, 0.3)]
+    keys = [s.key for s in specs]
+    cfg = SessionConfig(int(world * B / 6) + 50, SampleCountDist("geometric", 8.0), 0)
+    chunks = [generate_clustered_batch(cfg, specs, B, row_start=r * B) for r in range(world)]
+    mine = chunks[rank]
+    full = {k: np.random.default_rng(100 + i).uniform(-0.1, 0.1, size=(rows, D)).astype(np.float32)
+            for i, k in enumerate(keys)}
+    local_tables = {k: R.EmbeddingTable(k, shard_rows(rows, world, rank), D,
+                                        torch.from_numpy(np.ascontiguousarray(full[k][rank::world]))
+                                        .to(dev)) for k in keys}
+    caps = {k: mine.values[k].size for k in keys}
+    step = ShardedTrainStep(keys, B, caps, local_tables, op, lr, device=dev)
+    step.load_batch(mine.values, mine.offsets)
+    grads = [np.random.default_rng(1000 * r + 7).standard_normal((B, D)).astype(np.float32)
+             for r in range(world)]
+    for g in step.grad_out:
+        g.copy_(torch.from_numpy(grads[rank]))
+    step.run()
+    torch.cuda.synchronize()
+
+    res = {"rank": rank, "world": world, "op": op, "ok": True}
+    U, N = step.host_counts()
+    # forward vs oracle on this rank's chunk
+    worst_fwd = 0.0
+    for f, k in enumerate(keys):
+        inv, [(uv, uo)] = oracle.build_ikjt_arrays([(mine.values[k], mine.offsets[k])])
+        same = (np.array_equal(step.inverse[f].cpu().numpy(), inv)
+                and np.array_equal(step.uvalues[f][:N[f]].cpu().numpy(), uv)
+                and np.array_equal(step.uoffsets[f][:U[f]].cpu().numpy(), uo))
+        res["ok"] &= bool(same)
+        ref = oracle.expand(oracle.pooled_lookup(uv, uo, full[k], op), inv)
+        ok, err = close(step.out[f].cpu().numpy(), ref)
+        res["ok"] &= ok
+        worst_fwd = max(worst_fwd, err)
+    res["fwd_max_rel_err"] = worst_fwd
+    # backward: gather the shards, compare with the oracle SGD over all ranks
+    worst_bwd = 0.0
+    for f, k in enumerate(keys):
+        w = local_tables[k].weights
+        pad = torch.zeros((shard_rows(rows, world, 0), D), device=dev)
+        pad[: w.shape[0]] = w
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        new = np.empty((rows, D), np.float32)
+        for r in range(world):
+            new[r::world] = parts[r][: shard_rows(rows, world, r)].cpu().numpy()
+        g64 = np.zeros((rows, D), np.float64)
+        for r in range(world):
+            inv, [(uv, uo)] = oracle.build_ikjt_arrays([(chunks[r].values[k], chunks[r].offsets[k])])
+            gu = oracle.pool_backward(grads[r], inv, uo.size)
+            ids, gw = oracle.sparse_table_grad(gu, uv, uo, op)
+            g64[ids] += gw
+        delta_ref = -(np.float32(lr) * g64.astype(np.float32))
+        ok, err = close(new - full[k], delta_ref)
+        res["ok"] &= ok
+        worst_bwd = max(worst_bwd, err)
+    res["bwd_max_rel_err"] = worst_bwd
+    res["launches"] = R.launch_count()
+    print(json.dumps(res), flush=True)
+    dist.destroy_process_group()
+    return 0 if res["ok"] else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
