@@ -35,6 +35,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "samples/sec for IKJT dedup + embedding fwd/bwd; achieved HBM GB/s vs peak"
+
+# DRAM bytes (read + write) per launch from one ncu capture of the cfg2 bench
+# (profiles/r1_ncu_dram_cfg2.txt); None until measured for the current build.
+TRAFFIC: dict = {"k_scatter": 10.800e9, "k_pool_fwd": 4.914e9}
 LENS = ([8, 16, 32, 64, 128, 256] * 5)[:26]
 
 
@@ -323,9 +327,47 @@ def main():
             phases[name].append(ev[i].elapsed_time(ev[i + 1]))
     ph = {k: float(np.mean(v)) for k, v in phases.items()}
     peaks = load_peaks()
-    # dominant kernel: k_pool_fwd (one launch per step = the "pool" phase)
-    pool_bytes = 8 * N_u + 8 * U_tot + 4 * D * N_u + 4 * D * U_tot
-    pool_gbs = pool_bytes / (ph["pool"] / 1e3) / 1e9
+    peak = peaks.get("hbm_gbs")
+
+    # the two largest kernels, timed live with CUDA events recorded by librecd
+    # right before / after their launch (recd_debug_kernel_events)
+    lib = R.load_library()
+
+    def kernel_ms(name, n):
+        ts = []
+        for _ in range(n):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            b.record(stream)
+            lib.recd_debug_kernel_events(name.encode(), a.cuda_event, b.cuda_event)
+            step.run()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        lib.recd_debug_kernel_events(None, None, None)
+        return float(np.mean(ts))
+
+    nk = max(3, min(args.steps, 10))
+    kernels = {}
+    # compulsory HBM bytes per launch (distinct table rows once; SURVEY §8(d)
+    # counts every gathered row: "requested")
+    kb = {"k_pool_fwd": (8 * N_u + 8 * U_tot + 4 * D * N_ids + 4 * D * U_tot,
+                         8 * N_u + 8 * U_tot + 4 * D * N_u + 4 * D * U_tot),
+          "k_scatter": (8 * N_u + 4 * D * U_tot + 8 * D * N_ids,
+                        8 * N_u + 4 * D * N_u + 8 * D * N_ids)}
+    if args.mode == "kjt":
+        kb = {"k_pool_fwd": (8 * N_kjt + 4 * D * N_ids + 4 * D * B * K,
+                             8 * N_kjt + 4 * D * N_kjt + 4 * D * B * K),
+              "k_scatter": (8 * N_kjt + 4 * D * B * K + 8 * D * N_ids,
+                            8 * N_kjt + 4 * D * N_kjt + 8 * D * N_ids)}
+    for name, (comp, req) in kb.items():
+        t = kernel_ms(name, nk)
+        kernels[name] = {"ms": t, "compulsory_bytes": comp, "requested_bytes": req,
+                         "achieved_gbs": comp / (t / 1e3) / 1e9,
+                         "achieved_requested_gbs": req / (t / 1e3) / 1e9}
+    dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    pool_bytes = kernels[dom]["compulsory_bytes"]
+    pool_gbs = kernels[dom]["achieved_gbs"]
     A = algorithmic_bytes(B, K, D, N_kjt, N_u, U_tot, N_ids)
     if args.mode == "kjt":
         A = algorithmic_bytes(B, K, D, N_kjt, N_kjt, B * K, N_ids) - 8 * (N_kjt + 2 * B * K)
@@ -372,19 +414,23 @@ def main():
                          f"{procs} processes, {t:.1f} s"}
 
     if rank == 0:
-        peak = peaks.get("hbm_gbs")
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 (ids int64)", "data": "synthetic (restated reference session generator)",
             "config": config_dict(args, "gpu"),
-            "roofline": {"bound": "hbm", "kernel": "k_pool_fwd", "achieved": pool_gbs,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": pool_gbs,
                          "peak": peak, "unit": "GB/s",
                          "frac": pool_gbs / peak if peak else None,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peak else None,
-                         "traffic": None, "algorithmic_bytes_per_launch": pool_bytes,
-                         "avg_launch_ms": ph["pool"]},
+                         "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured)"
+                                         if "note" not in peaks else "fallback 6650 GB/s"),
+                         "traffic": TRAFFIC.get(dom), "algorithmic_bytes_per_launch": pool_bytes,
+                         "bytes_definition": "compulsory: each distinct table row once "
+                                             "(DESIGN.md §4)",
+                         "avg_launch_ms": kernels[dom]["ms"],
+                         "achieved_requested": kernels[dom]["achieved_requested_gbs"]},
+            "kernels": kernels,
             "step_roofline": {"algorithmic_bytes": A, "achieved_gbs": step_gbs,
                               "frac": step_gbs / peak if peak else None},
             "phases_ms": ph,

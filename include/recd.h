@@ -76,6 +76,10 @@ int64_t recd_launch_count(void);
  * the exact fallback path is exercised).  ~0 restores the default. */
 void recd_debug_set_hash_mask(uint64_t mask);
 
+/* Timing hook: record the given cudaEvents right before / after every launch
+ * of the named kernel ("k_pool_fwd", "k_scatter"); NULL name disables. */
+void recd_debug_kernel_events(const char* name, void* before, void* after);
+
 /* ---------------------------------------------------------------- dedup --
  * KJT -> IKJT for `num_groups` feature groups of one batch of B rows.
  * Rows i, j of a group merge iff every feature list in the group is equal

@@ -624,7 +624,9 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       }
       const unsigned g2 =
           (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks * ncb, 8), (int64_t)num_sms() * 16);
+      hook_before("k_scatter", stream);
       k_scatter<C><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+      hook_after("k_scatter", stream);
       note_launch();
     }
   });

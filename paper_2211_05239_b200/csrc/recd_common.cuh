@@ -33,6 +33,8 @@ namespace recd {
 // Number of kernels this library enqueued (host-side counter; reported by
 // bench.py as "gpu_launches").
 void note_launch(int n = 1);
+void hook_before(const char* name, cudaStream_t s);
+void hook_after(const char* name, cudaStream_t s);
 
 int num_sms();
 

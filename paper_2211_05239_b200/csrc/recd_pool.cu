@@ -188,7 +188,9 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
     for (int f = 0; f < p.F; ++f) any_expand |= (p.out[f] != nullptr && p.out[f] != p.pooled[f]);
     int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, 1, {
       const unsigned grid = grid_for(batch_size * p.F * col_blocks<C>(dim));
+      hook_before("k_pool_fwd", stream);
       k_pool_fwd<C><<<grid, 256, 0, stream>>>(p);
+      hook_after("k_pool_fwd", stream);
       note_launch();
       if (any_expand) {
         k_expand<C><<<grid, 256, 0, stream>>>(p);

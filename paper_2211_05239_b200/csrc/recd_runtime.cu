@@ -1,9 +1,21 @@
 // Library-level bookkeeping: version, launch counter, SM count cache.
 #include <atomic>
+#include <string>
 
 #include "recd_common.cuh"
 
 namespace recd {
+
+// Optional timing hook: CUDA events recorded right before / after the launch
+// of one named kernel (bench.py times the dominant kernel live with it).
+static std::string g_hook;
+static cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
+void hook_before(const char* name, cudaStream_t s) {
+  if (g_ev0 && g_hook == name) cudaEventRecord(g_ev0, s);
+}
+void hook_after(const char* name, cudaStream_t s) {
+  if (g_ev1 && g_hook == name) cudaEventRecord(g_ev1, s);
+}
 
 static std::atomic<int64_t> g_launches{0};
 
@@ -31,4 +43,10 @@ extern "C" int64_t recd_launch_count(void) { return recd::g_launches.load(); }
 extern "C" const char* recd_last_error(void) {
   cudaError_t e = cudaPeekAtLastError();
   return e == cudaSuccess ? "" : cudaGetErrorString(e);
+}
+
+extern "C" void recd_debug_kernel_events(const char* name, void* before, void* after) {
+  recd::g_hook = name ? name : "";
+  recd::g_ev0 = name ? (cudaEvent_t)before : nullptr;
+  recd::g_ev1 = name ? (cudaEvent_t)after : nullptr;
 }
