@@ -111,7 +111,8 @@ int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t batch_siz
  *   uvalues/uoffsets host [F] device (jagged rows of feature f)
  *   counts      device int64[2F]
  *   pooled_out  host [F] device float[U_cap x dim]  (may alias out[f] when inverse[f] is NULL)
- *   err         device int64[1]: first bad ID as (f << 40) | position, or RECD_NO_ERROR
+ *   err         device int64[2]: [0] first bad ID as (f << 40) | position, or RECD_NO_ERROR;
+ *               [1] scratch (work counter of the launch)
  */
 int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
                   const float* const* tables, const int64_t* table_rows,

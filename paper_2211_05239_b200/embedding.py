@@ -147,7 +147,7 @@ def pooled_lookup(features: Sequence[JaggedTensor], tables: Sequence[EmbeddingTa
             pooled.append(torch.empty((max(features[f].row_count, 1), D), dtype=torch.float32,
                                       device=dev))
             outs.append(torch.empty((B, D), dtype=torch.float32, device=dev))
-    err = torch.empty(1, dtype=torch.int64, device=dev)
+    err = torch.empty(2, dtype=torch.int64, device=dev)  # [first bad ID, work counter]
     rc = lib.recd_pool_fwd(F, B, D, _lib.POOL_MODES[op], _lib.ptrs([t.weights for t in tables]),
                            _lib.i64s([t.rows for t in tables]),
                            _lib.ptrs([f.values for f in features]),
@@ -155,7 +155,7 @@ def pooled_lookup(features: Sequence[JaggedTensor], tables: Sequence[EmbeddingTa
                            _lib.ptrs(inverses), _lib.ptrs(pooled), _lib.ptrs(outs),
                            err.data_ptr(), _lib.stream_ptr(dev))
     _lib.check(rc, "recd_pool_fwd")
-    e = int(err.item())
+    e = int(err[0].item())
     if e != _lib.RECD_NO_ERROR:
         f, p = e >> 40, e & ((1 << 40) - 1)
         key = keys[f] if keys else tables[f].key

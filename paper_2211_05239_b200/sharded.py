@@ -143,7 +143,7 @@ class ShardedTrainStep:
         self.pooled = [torch.empty((B, D), dtype=f32, device=dev) for _ in self.keys]
         self.out = [torch.empty((B, D), dtype=f32, device=dev) for _ in self.keys]
         self.grad_out = [torch.empty((B, D), dtype=f32, device=dev) for _ in self.keys]
-        self.err = torch.empty(1, dtype=i64, device=dev)
+        self.err = torch.empty(2, dtype=i64, device=dev)  # [first bad ID, work counter]
         self.meta_send = torch.zeros((R, 2 * F), dtype=i64, device=dev)
         self.meta_recv = torch.zeros((R, 2 * F), dtype=i64, device=dev)
         # batched-copy descriptor staging (one pinned host + device table per call site)

@@ -68,7 +68,7 @@ class TrainStep:
         self.pooled = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
         self.out = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
         self.grad_out = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
-        self.err = torch.empty(1, dtype=i64, device=dev)
+        self.err = torch.empty(2, dtype=i64, device=dev)  # [first bad ID, work counter]
         self.dedup_scratch = torch.empty(
             max(self.lib.recd_dedup_scratch_bytes(len(self.groups), F, B), 256),
             dtype=torch.uint8, device=dev)

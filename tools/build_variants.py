@@ -6,9 +6,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
-    "s_clob": ["RECD_CPASYNC_CLOBBER=1"],
-    "s_noclob": ["RECD_CPASYNC_CLOBBER=0"],
-    "s_vw2": ["RECD_CPASYNC_CLOBBER=0", "RECD_BWD_VW=2"],
+    "s2m2": ["RECD_POOL_STREAM=1", "RECD_STREAM_G=2", "RECD_STREAM_MINB=2"],
+    "s3m2": ["RECD_POOL_STREAM=1", "RECD_STREAM_G=3", "RECD_STREAM_MINB=2"],
+    "s4m1": ["RECD_POOL_STREAM=1", "RECD_STREAM_G=4", "RECD_STREAM_MINB=1"],
+    "s2m3v2": ["RECD_POOL_STREAM=1", "RECD_STREAM_G=2", "RECD_STREAM_MINB=3", "RECD_POOL_VW=2"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
