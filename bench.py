@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--dist", choices=["geometric", "fixed"], default="geometric")
     ap.add_argument("--change-prob", type=float, default=0.15)
     ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--shards", type=int, default=0,
+                    help="N>1: row shards per table (0 = N, one per rank)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -450,7 +452,8 @@ def main():
 
 
 def run_sharded(args, world, rank, local, dev):
-    """N > 1: row-sharded tables (owner = id mod N) + data-parallel batch;
+    """N > 1: every table row-sharded into S shards (id mod S), the
+    (table, shard) pairs placed on ranks LPT-first, + data-parallel batch;
     each rank deduplicates its own 65,536-row chunk of the global batch and
     the NCCL exchange carries only deduplicated IDs, partially pooled rows and
     unique-row gradients (paper_2211_05239_b200/sharded.py)."""
@@ -458,16 +461,21 @@ def run_sharded(args, world, rank, local, dev):
     import torch.distributed as dist
 
     import paper_2211_05239_b200 as R
-    from paper_2211_05239_b200.sharded import ShardedTrainStep, shard_rows
+    from paper_2211_05239_b200.sharded import ShardedTrainStep
 
     t_setup = time.perf_counter()
     batch = make_batch(args, rank, world)
     keys = list(batch.keys)
-    lrows = shard_rows(args.rows, world, rank)
-    tables = {k: R.EmbeddingTable.create_on_device(f"{k}/shard{rank}", lrows, args.dim, seed=i,
-                                                   device=dev) for i, k in enumerate(keys)}
+    S = args.shards or world
+
+    def make_table(k, j, n):
+        return R.EmbeddingTable.create_on_device(f"{k}/shard{j}", n, args.dim,
+                                                 seed=1000 * keys.index(k) + j, device=dev)
+
     caps = {k: batch.values[k].size for k in keys}
-    step = ShardedTrainStep(keys, args.batch, caps, tables, "sum", args.lr, device=dev)
+    step = ShardedTrainStep(keys, args.batch, caps, {k: args.rows for k in keys}, args.dim,
+                            make_table, "sum", args.lr, shards=S, device=dev)
+    lrows = sum(t.rows for t in step.tables.values())
     step.load_batch(batch.values, batch.offsets)
     step.fill_grad_out(1 + rank)
     torch.cuda.synchronize()
@@ -510,9 +518,9 @@ def run_sharded(args, world, rank, local, dev):
     ph = dict(zip(names, tph.tolist()))
     # per-rank communication volume of the step (bytes sent)
     pl = step.plan
-    sent = 8 * int(pl.send_ids.sum()) + 8 * world * int(pl.send_rows.sum())  # ids + row counts
+    sent = 8 * int(pl.send_ids.sum()) + 8 * int(pl.send_rows.sum())  # ids + row counts
     sent += 4 * D * int(pl.recv_rows.sum())  # partial pooled rows returned
-    sent += 4 * D * world * int(pl.send_rows.sum())  # unique-row gradients
+    sent += 4 * D * int(pl.send_rows.sum())  # unique-row gradients (one copy per shard)
     N_kjt = int(sum(caps.values()))
 
     e2e = None
@@ -542,8 +550,10 @@ def run_sharded(args, world, rank, local, dev):
                       "of the dedup counts; max over ranks"}
     if rank == 0:
         cfg = config_dict(args, "gpu")
-        cfg["parallelism"] = f"dp{world} x row-sharded tables (owner = id mod {world})"
-        cfg["table_rows_per_rank"] = lrows
+        cfg["parallelism"] = (f"dp{world} x {S}-way row-sharded tables (shard = id mod {S}), "
+                              f"(table, shard) pairs placed LPT")
+        cfg["table_rows_rank0"] = lrows
+        cfg["pairs_rank0"] = len(step.mine)
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

@@ -185,16 +185,18 @@ int recd_sparse_sgd(int32_t num_features, int64_t max_rows, int32_t dim, float* 
  *   values grouped by owner (owner-major, then unique row, then position);
  *   rowcnt_out[f][o * batch_size + u] = values of row u owned by o;
  *   totals_out[f * R + o] (device) = IDs of f owned by o.
- * combine:   pooled_out[f][u] = sum over o = 0..R-1 (in that order) of
- *   partial[f][(o * batch_size + u) * dim ...]; avg divides by the row length. */
+ * combine:   pooled_out[f][u] = sum over j = 0..num_blocks-1 (in that order) of
+ *   blocks[f * num_blocks + j][u * dim ...] (the partial rows of shard j of
+ *   feature f, F * num_blocks <= 256); avg divides by the row length;
+ *   batch_size bounds the unique rows (launch geometry). */
 size_t recd_shard_scratch_bytes(int32_t num_features, int32_t num_ranks, int64_t batch_size);
 int recd_shard_bucketize(int32_t num_features, int32_t num_ranks, int64_t batch_size,
                          const int64_t* const* uvalues, const int64_t* const* uoffsets,
                          const int64_t* counts, int64_t* const* ids_out, int64_t* const* rowcnt_out,
                          int64_t* totals_out, void* scratch, size_t scratch_bytes,
                          recd_stream_t stream);
-int recd_shard_combine(int32_t num_features, int32_t num_ranks, int64_t batch_size, int32_t dim,
-                       int32_t mode, const float* const* partial, const int64_t* const* uoffsets,
+int recd_shard_combine(int32_t num_features, int32_t num_blocks, int64_t batch_size, int32_t dim,
+                       int32_t mode, const float* const* blocks, const int64_t* const* uoffsets,
                        const int64_t* counts, float* const* pooled_out, recd_stream_t stream);
 
 /* Batched copy of num_segments (src, dst, bytes) device segments in one

@@ -121,13 +121,14 @@ __global__ void __launch_bounds__(256) k_shard_scatter(const __grid_constant__ S
   }
 }
 
+constexpr int SH_MAXBLK = 256;
+
 struct CombineParams {
   int F;
-  int R;
+  int R;  // partial blocks per feature
   int D;
   int mode;
-  int64_t B;  // row stride between owners' partial blocks
-  const float* ret[RECD_MAX_FEAT];  // [R][B][D]
+  const float* blk[SH_MAXBLK];      // block (f, o) = blk[f * R + o], rows indexed by u
   float* pooled[RECD_MAX_FEAT];     // [U][D]
   const int64_t* uoffsets[RECD_MAX_FEAT];
   const int64_t* counts;            // [2F] local counts
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(256) k_shard_combine(const __grid_constant__ C
     float acc[V], x[V];
     C::zero(acc);
     for (int o = 0; o < p.R; ++o) {
-      C::ld(p.ret[f] + ((int64_t)o * p.B + u) * p.D + cw.lo, cw.ok, x);
+      C::ld(p.blk[f * p.R + o] + u * p.D + cw.lo, cw.ok, x);
 #pragma unroll
       for (int e = 0; e < V; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
     }
@@ -238,24 +239,28 @@ extern "C" int recd_shard_bucketize(int32_t num_features, int32_t num_ranks, int
   return RECD_OK;
 }
 
-extern "C" int recd_shard_combine(int32_t num_features, int32_t num_ranks, int64_t batch_size,
-                                  int32_t dim, int32_t mode, const float* const* partial,
+extern "C" int recd_shard_combine(int32_t num_features, int32_t num_blocks, int64_t batch_size,
+                                  int32_t dim, int32_t mode, const float* const* blocks,
                                   const int64_t* const* uoffsets, const int64_t* counts,
                                   float* const* pooled_out, recd_stream_t stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   const int F = num_features;
-  if (F <= 0 || F > RECD_MAX_FEAT || num_ranks <= 0 || dim <= 0 || !counts) return RECD_ERR_ARG;
+  if (F <= 0 || F > RECD_MAX_FEAT || num_blocks <= 0 || (int64_t)F * num_blocks > SH_MAXBLK ||
+      dim <= 0 || !counts || !blocks)
+    return RECD_ERR_ARG;
   if (mode != RECD_POOL_SUM && mode != RECD_POOL_AVG) return RECD_ERR_UNSUPPORTED;
   CombineParams p;
   memset(&p, 0, sizeof(p));
   p.F = F;
-  p.R = num_ranks;
+  p.R = num_blocks;
   p.D = dim;
   p.mode = mode;
-  p.B = batch_size;
   p.counts = counts;
+  for (int i = 0; i < F * num_blocks; ++i) {
+    if (!blocks[i]) return RECD_ERR_ARG;
+    p.blk[i] = blocks[i];
+  }
   for (int f = 0; f < F; ++f) {
-    p.ret[f] = partial[f];
     p.pooled[f] = pooled_out[f];
     p.uoffsets[f] = uoffsets[f];
   }

@@ -1,32 +1,38 @@
 """Row-sharded multi-GPU training step of the IKJT hot path.
 
-SURVEY.md §8(e): the batch is data-parallel (rank r owns rows
-[r*B, (r+1)*B) of the global batch, deduplicated locally -- exactly
-`slice_ikjt_rows` / `split_batch`, trainer_sim.py:394-446) and every embedding
-table is row-sharded over the R ranks: owner(id) = id mod R, local row
-id div R.  The reference only simulates ranks and shards table-wise
+SURVEY.md §8(e): the batch is data-parallel (rank r owns rows [r*B, (r+1)*B)
+of the global batch and deduplicates them locally -- exactly `slice_ikjt_rows`
+/ `split_batch`, trainer_sim.py:394-446) and every embedding table is
+row-sharded: shard j of table f holds the IDs with id mod S == j (local row
+id div S).  The F*S (table, shard) pairs are placed on the R ranks
+longest-processing-time first, so S trades exchange volume (S partial rows per
+unique row) against load balance; S = R with one shard per rank is plain
+row-wise sharding.  The reference only simulates ranks and shards table-wise
 (trainer_sim.py:202-214, 281-305); here the exchange is real (NCCL over
 NVLink) and carries only
 
-  forward   deduplicated IDs (per owner, per unique row)   source -> owner
-            partially pooled rows, one per unique row       owner  -> source
-  backward  gradient rows of the unique rows                source -> owner
+  forward   deduplicated IDs (per shard, per unique row)    source -> owner
+            partially pooled rows, one per (unique row, shard) owner -> source
+  backward  gradient rows of the unique rows                 source -> owners
 
-The inverse_lookup never travels (trainer_sim.py:268-275).  Owners pool
-their share of every unique row (recd_pool_fwd over the received jagged
-lists), sources add the R partials in fixed owner order (recd_shard_combine)
-and expand; the backward computes grad_u at the source (recd_grad_unique) and
-the owners run the deterministic sorted scatter-add + SGD on their shard
-(recd_sparse_sgd).  Results are deterministic; versus one GPU the pooled sums
-change fp32 association (partial sums), so parity is within the north_star
-1e-5 tolerance, while IDs / inverse stay bit-exact.
+The inverse_lookup never travels (trainer_sim.py:268-275).  Owners pool their
+share of every unique row (recd_pool_fwd over the received jagged lists),
+sources add the S partials in fixed shard order (recd_shard_combine) and
+expand; the backward computes grad_u at the source (recd_grad_unique) and the
+owners run the deterministic sorted scatter-add + SGD on their shards
+(recd_sparse_sgd).  Partial-row and gradient exchanges are issued per feature
+group as async NCCL all-to-alls, overlapping the next group's owner compute.
+Exchange buffers are sized exactly from the step's count exchange (grow-only).
+Results are deterministic; versus one GPU the pooled sums change fp32
+association (partial sums), so parity is within the north_star 1e-5
+tolerance, while IDs / inverse stay bit-exact.
 """
 
 from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import Sequence
+from typing import Callable, Sequence
 
 import numpy as np
 import torch
@@ -35,79 +41,110 @@ import torch.distributed as dist
 from . import _lib
 from .embedding import EmbeddingTable
 
-__all__ = ["ShardedTrainStep", "ExchangePlan", "plan_exchange", "shard_rows"]
+__all__ = ["ShardedTrainStep", "ExchangePlan", "plan_exchange", "shard_rows", "place_pairs"]
 
 
-def shard_rows(rows: int, num_ranks: int, rank: int) -> int:
-    """Rows of a table held by `rank` under owner(id) = id mod R."""
-    return (rows - rank + num_ranks - 1) // num_ranks
+def shard_rows(rows: int, num_shards: int, shard: int) -> int:
+    """Rows of table shard `shard` under shard(id) = id mod S (local row id div S)."""
+    return (rows - shard + num_shards - 1) // num_shards
+
+
+def place_pairs(weights: Sequence[float], num_ranks: int) -> list[int]:
+    """Longest-processing-time placement of (table, shard) pairs on ranks.
+    Deterministic (ties: lower pair index first, then lower rank), so every
+    rank computes the same placement from the same weights."""
+    order = sorted(range(len(weights)), key=lambda p: (-weights[p], p))
+    load = [0.0] * num_ranks
+    place = [0] * len(weights)
+    for p in order:
+        r = min(range(num_ranks), key=lambda q: (load[q], q))
+        place[p] = r
+        load[r] += weights[p]
+    return place
 
 
 @dataclass
 class ExchangePlan:
     """Host-side split sizes of one step's exchanges (from the count all-to-all).
 
-    send_ids[o][f]  IDs of feature f this rank sends to owner o
-    send_rows[f]    unique rows of feature f here (sent to every owner)
-    recv_ids[s][f]  IDs of feature f received from source s
-    recv_rows[s][f] unique rows of feature f at source s
-    """
+    Pairs p = f * S + j.  send_ids[p] / send_rows[p]: IDs / unique rows this
+    rank sends for pair p (to its owner); recv_ids[s, p] / recv_rows[s, p]:
+    what source s sends this rank for pair p (0 for pairs owned elsewhere)."""
 
     R: int
-    F: int
+    P: int
     send_ids: np.ndarray
     send_rows: np.ndarray
     recv_ids: np.ndarray
     recv_rows: np.ndarray
 
-    def send_id_base(self, f: int, o: int) -> int:
-        return int(self.send_ids[:o, f].sum())
+    def owner_rows(self, p: int) -> int:
+        return int(self.recv_rows[:, p].sum())
 
-    def recv_id_base(self, f: int, s: int) -> int:
-        return int(self.recv_ids[:s, f].sum())
+    def owner_ids(self, p: int) -> int:
+        return int(self.recv_ids[:, p].sum())
 
-    def recv_row_base(self, f: int, s: int) -> int:
-        return int(self.recv_rows[:s, f].sum())
+    def recv_row_base(self, p: int, s: int) -> int:
+        return int(self.recv_rows[:s, p].sum())
 
-    def owner_rows(self, f: int) -> int:
-        return int(self.recv_rows[:, f].sum())
-
-    def owner_ids(self, f: int) -> int:
-        return int(self.recv_ids[:, f].sum())
+    def recv_id_base(self, p: int, s: int) -> int:
+        return int(self.recv_ids[:s, p].sum())
 
 
 def plan_exchange(send_meta: np.ndarray, recv_meta: np.ndarray) -> ExchangePlan:
-    """send_meta / recv_meta: [R, 2F] int64 rows exchanged by the count
-    all-to-all: [o, f] = IDs of f for owner o, [o, F + f] = rows of f."""
-    R, two_f = send_meta.shape
-    F = two_f // 2
-    return ExchangePlan(R, F, send_meta[:, :F].copy(), send_meta[0, F:].copy(),
-                        recv_meta[:, :F].copy(), recv_meta[:, F:].copy())
+    """send_meta / recv_meta: [R, 2P] int64 rows exchanged by the count
+    all-to-all: [d, p] = IDs of pair p for rank d, [d, P + p] = its rows
+    (zero unless d owns p)."""
+    R, two_p = send_meta.shape
+    P = two_p // 2
+    return ExchangePlan(R, P, send_meta[:, :P].sum(axis=0), send_meta[:, P:].sum(axis=0),
+                        recv_meta[:, :P].copy(), recv_meta[:, P:].copy())
 
 
 class ShardedTrainStep:
-    """One rank's view of the row-sharded step (all buffers preallocated at
-    worst case; host syncs only for the exchange split sizes)."""
+    """One rank's view of the sharded step.  `make_table(key, shard, rows)`
+    returns the EmbeddingTable of a (table, shard) pair placed on this rank;
+    `table_rows[key]` is the full table's row count."""
 
     def __init__(self, keys: Sequence[str], batch_size: int, value_caps: dict[str, int],
-                 local_tables: dict[str, EmbeddingTable], op: str = "sum", lr: float = 0.01,
-                 group=None, device=None):
-        self.lib = _lib.load()
+                 table_rows: dict[str, int], dim: int,
+                 make_table: Callable[[str, int, int], EmbeddingTable], op: str = "sum",
+                 lr: float = 0.01, shards: int | None = None, group=None, device=None,
+                 ngroups: int = 4):
+        self.lib = L = _lib.load()
         self.group = group
         self.R = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.keys = list(keys)
         self.F = len(self.keys)
+        self.S = int(shards or self.R)
         self.B = int(batch_size)
+        self.D = int(dim)
         self.op = op
         self.mode_id = _lib.POOL_MODES[op]
         self.lr = float(lr)
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
-        self.tables = [local_tables[k] for k in self.keys]
-        self.D = self.tables[0].dim
-        R, B, D, F, dev = self.R, self.B, self.D, self.F, self.dev
+        R, S, B, D, F, dev = self.R, self.S, self.B, self.D, self.F, self.dev
+        if not 1 <= S or F * S > 256:
+            raise ValueError("need 1 <= shards and features x shards <= 256")
         i64, f32 = torch.int64, torch.float32
         self.caps = [max(int(value_caps[k]), 1) for k in self.keys]
+        # identical placement on every rank: weights from the global value counts
+        tot = torch.tensor(self.caps, dtype=torch.float64, device=dev)
+        dist.all_reduce(tot, group=group)
+        tot = tot.cpu().tolist()
+        self.place = place_pairs([tot[p // S] / S for p in range(F * S)], R)
+        self.mine = [p for p in range(F * S) if self.place[p] == self.rank]
+        if len(self.mine) > 64:
+            raise ValueError("more than 64 (table, shard) pairs on one rank")
+        self.by_dest = [[p for p in range(F * S) if self.place[p] == d] for d in range(R)]
+        self.tables = {}
+        for p in self.mine:
+            k = self.keys[p // S]
+            t = make_table(k, p % S, shard_rows(int(table_rows[k]), S, p % S))
+            if t.dim != D:
+                raise ValueError("all tables must share one embedding dim")
+            self.tables[p] = t
         # local KJT + IKJT
         self.in_values = [torch.zeros(c, dtype=i64, device=dev) for c in self.caps]
         self.in_offsets = [torch.zeros(B, dtype=i64, device=dev) for _ in self.keys]
@@ -116,57 +153,65 @@ class ShardedTrainStep:
         self.uoffsets = [torch.empty(B, dtype=i64, device=dev) for _ in self.keys]
         self.uvalues = [torch.empty(c, dtype=i64, device=dev) for c in self.caps]
         self.counts = torch.zeros(2 * F, dtype=i64, device=dev)
-        # bucketize (send side)
+        # IDs bucketized by shard (send side)
         self.ids_send = [torch.empty(c, dtype=i64, device=dev) for c in self.caps]
-        self.rowcnt_send = [torch.empty(R * B, dtype=i64, device=dev) for _ in self.keys]
-        self.totals = torch.zeros(F * R, dtype=i64, device=dev)
-        # owner side (worst case: every source sends everything)
-        self.ocaps = [R * c for c in self.caps]
-        self.ids_recv = [torch.empty(c, dtype=i64, device=dev) for c in self.ocaps]
-        self.rc_recv = [torch.zeros(R * B, dtype=i64, device=dev) for _ in self.keys]
-        self.ro = [torch.zeros(R * B, dtype=i64, device=dev) for _ in self.keys]
-        self.part = [torch.empty((R * B, D), dtype=f32, device=dev) for _ in self.keys]
-        self.grad_recv = [torch.empty((R * B, D), dtype=f32, device=dev) for _ in self.keys]
-        self.counts_owner = torch.zeros(2 * F, dtype=i64, device=dev)
-        # packed exchange buffers: one NCCL collective per direction
-        #   A  (int64) per peer: [row counts of f = 0..F-1][IDs of f = 0..F-1]
-        #   B  (fp32)  per peer: partially pooled rows of f = 0..F-1
-        #   G  (fp32)  this rank's unique-row gradients of f = 0..F-1 (all-gathered)
-        capA = R * (F * B + sum(self.caps))
-        self.sendA = torch.empty(capA, dtype=i64, device=dev)
-        self.recvA = torch.empty(capA, dtype=i64, device=dev)
-        self.sendB = torch.empty((R * F * B, D), dtype=f32, device=dev)
-        self.recvB = torch.empty((R * F * B, D), dtype=f32, device=dev)
-        self.gradG = torch.empty((F * B, D), dtype=f32, device=dev)
-        self.recvG = torch.empty((R * F * B, D), dtype=f32, device=dev)
-        # source side outputs
+        self.rowcnt_send = [torch.empty(S * B, dtype=i64, device=dev) for _ in self.keys]
+        self.totals = torch.zeros(F * S, dtype=i64, device=dev)  # [f * S + j]
+        # source outputs
         self.pooled = [torch.empty((B, D), dtype=f32, device=dev) for _ in self.keys]
         self.out = [torch.empty((B, D), dtype=f32, device=dev) for _ in self.keys]
         self.grad_out = [torch.empty((B, D), dtype=f32, device=dev) for _ in self.keys]
+        self.gradG = torch.empty((F * B, D), dtype=f32, device=dev)
         self.err = torch.empty(2, dtype=i64, device=dev)  # [first bad ID, work counter]
-        self.meta_send = torch.zeros((R, 2 * F), dtype=i64, device=dev)
-        self.meta_recv = torch.zeros((R, 2 * F), dtype=i64, device=dev)
-        # batched-copy descriptor staging (one pinned host + device table per call site)
-        nseg = 2 * R * F
-        db = self.lib.recd_batched_copy_desc_bytes(nseg)
-        self.cp_host = [torch.empty(db, dtype=torch.uint8).pin_memory() for _ in range(4)]
-        self.cp_dev = [torch.empty(db, dtype=torch.uint8, device=dev) for _ in range(4)]
-        L = self.lib
-        self.s_dedup = torch.empty(max(L.recd_dedup_scratch_bytes(F, F, B), 256), dtype=torch.uint8,
-                                   device=dev)
-        self.s_shard = torch.empty(max(L.recd_shard_scratch_bytes(F, R, B), 256), dtype=torch.uint8,
-                                   device=dev)
-        self.s_grad = torch.empty(max(L.recd_grad_unique_scratch_bytes(F, B), 256), dtype=torch.uint8,
-                                  device=dev)
-        self.s_sgd = torch.empty(max(L.recd_sparse_sgd_scratch_bytes(F, _lib.i64s(self.ocaps)), 256),
-                                 dtype=torch.uint8, device=dev)
-        self.s_scan = torch.empty(
-            max(L.recd_exclusive_scan_scratch_bytes(F, _lib.i64s([R * B] * F)), 256),
-            dtype=torch.uint8, device=dev)
-        self._args()
+        place = torch.tensor(self.place, dtype=i64, device=dev)
+        self.pmask = (place[None, :] == torch.arange(R, device=dev)[:, None]).to(i64)  # [R, P]
+        self.pair_feature = torch.arange(F, device=dev).repeat_interleave(S)      # f(p)
+        self.meta_send = torch.zeros((R, 2 * F * S), dtype=i64, device=dev)
+        self.meta_recv = torch.zeros((R, 2 * F * S), dtype=i64, device=dev)
+        self.s_dedup = torch.empty(max(L.recd_dedup_scratch_bytes(F, F, B), 256),
+                                   dtype=torch.uint8, device=dev)
+        self.s_shard = torch.empty(max(L.recd_shard_scratch_bytes(F, S, B), 256),
+                                   dtype=torch.uint8, device=dev)
+        self.s_grad = torch.empty(max(L.recd_grad_unique_scratch_bytes(F, B), 256),
+                                  dtype=torch.uint8, device=dev)
+        self._bufs: dict = {}
+        P = _lib.ptrs
+        self.a_gsizes = _lib.i32s([1] * F)
+        self.a_in_values, self.a_in_offsets = P(self.in_values), P(self.in_offsets)
+        self.a_nvalues = _lib.i64s(self.nvalues)
+        self.a_inverse, self.a_uoffsets, self.a_uvalues = P(self.inverse), P(self.uoffsets), P(self.uvalues)
+        self.a_ids_send, self.a_rowcnt = P(self.ids_send), P(self.rowcnt_send)
+        self.a_grad_out = P(self.grad_out)
+        # contiguous feature groups: the exchange of group g overlaps the owner
+        # compute of group g + 1
+        ng = max(1, min(ngroups, F))
+        bounds = [round(i * F / ng) for i in range(ng + 1)]
+        self.groups = [list(range(bounds[i], bounds[i + 1])) for i in range(ng)
+                       if bounds[i + 1] > bounds[i]]
+        self.g_idx = [torch.tensor(g + [F + f for f in g], dtype=i64, device=dev)
+                      for g in self.groups]
+        self.g_counts = [torch.zeros(2 * len(g), dtype=i64, device=dev) for g in self.groups]
+        self.g_mine = [[p for p in self.mine if p // S in g] for g in self.groups]
+        # batched-copy descriptor staging: one pinned host + device table per call site
+        # (0: pack IDs, 1: unpack IDs, then per group: pack partials, pack grads, unpack grads)
+        nsite = 2 + 3 * len(self.groups)
+        db = L.recd_batched_copy_desc_bytes(2 * R * F * S + 8)
+        self.cp_host = [torch.empty(db, dtype=torch.uint8).pin_memory() for _ in range(nsite)]
+        self.cp_dev = [torch.empty(db, dtype=torch.uint8, device=dev) for _ in range(nsite)]
         self.plan: ExchangePlan | None = None
         self.trace = False           # record CUDA events between sub-phases
         self.marks: list = []
+
+    # -------------------------------------------------------------- utils
+    def _buf(self, name: str, n: int, dtype=torch.int64, cols: int = 0) -> torch.Tensor:
+        """Grow-only device buffer of at least max(n, 1) rows."""
+        n = max(int(n), 1)
+        b = self._bufs.get(name)
+        if b is None or b.shape[0] < n:
+            shape = (n + n // 4 + 1, cols) if cols else (n + n // 4 + 1,)
+            b = torch.empty(shape, dtype=dtype, device=self.dev)
+            self._bufs[name] = b
+        return b
 
     def _mark(self, name: str):
         if self.trace:
@@ -182,20 +227,17 @@ class ShardedTrainStep:
             out[n1] = out.get(n1, 0.0) + e0.elapsed_time(e1)
         return out
 
-    def _args(self):
-        P, I = _lib.ptrs, _lib.i64s
-        self.a_gsizes = _lib.i32s([1] * self.F)
-        self.a_in_values, self.a_in_offsets = P(self.in_values), P(self.in_offsets)
-        self.a_nvalues = I(self.nvalues)
-        self.a_inverse, self.a_uoffsets, self.a_uvalues = P(self.inverse), P(self.uoffsets), P(self.uvalues)
-        self.a_ids_send, self.a_rowcnt = P(self.ids_send), P(self.rowcnt_send)
-        self.a_tables = P([t.weights for t in self.tables])
-        self.a_rows = I([t.rows for t in self.tables])
-        self.a_ids_recv, self.a_ro, self.a_rc = P(self.ids_recv), P(self.ro), P(self.rc_recv)
-        self.a_part = P(self.part)
-        self.a_pooled, self.a_out = P(self.pooled), P(self.out)
-        self.a_grad_out, self.a_grad_recv = P(self.grad_out), P(self.grad_recv)
-        self.a_ocaps = I(self.ocaps)
+    def _copy(self, site: int, segs):
+        """segs: [(src_ptr, dst_ptr, bytes)] -> one batched-copy launch."""
+        segs = [x for x in segs if x[2] > 0]
+        if not segs:
+            return
+        rc = self.lib.recd_batched_copy(len(segs), _lib.ptrs([x[0] for x in segs]),
+                                        _lib.ptrs([x[1] for x in segs]),
+                                        _lib.i64s([x[2] for x in segs]),
+                                        self.cp_host[site].data_ptr(), self.cp_dev[site].data_ptr(),
+                                        _lib.stream_ptr(self.dev))
+        _lib.check(rc, "recd_batched_copy")
 
     # ------------------------------------------------------------- inputs
     def load_batch(self, values, offsets):
@@ -215,31 +257,19 @@ class ShardedTrainStep:
         for t in self.grad_out:
             t.normal_(generator=g)
 
-    # --------------------------------------------------------- exchanges
-    def _copy(self, site: int, segs):
-        """segs: [(src_ptr, dst_ptr, bytes)] -> one batched-copy launch."""
-        if not segs:
-            return
-        rc = self.lib.recd_batched_copy(len(segs), _lib.ptrs([x[0] for x in segs]),
-                                        _lib.ptrs([x[1] for x in segs]),
-                                        _lib.i64s([x[2] for x in segs]),
-                                        self.cp_host[site].data_ptr(), self.cp_dev[site].data_ptr(),
-                                        _lib.stream_ptr(self.dev))
-        _lib.check(rc, "recd_batched_copy")
-
+    # ---------------------------------------------------------------- step
     def _exchange_counts(self) -> ExchangePlan:
-        R, F = self.R, self.F
-        tot = self.totals.view(F, R)  # [f, o]
-        self.meta_send[:, :F].copy_(tot.t())
-        self.meta_send[:, F:].copy_(self.counts[:F].unsqueeze(0).expand(R, F))
+        P = self.F * self.S
+        rows = self.counts[self.pair_feature]  # U_f(p)
+        torch.mul(self.pmask, self.totals[None, :], out=self.meta_send[:, :P])
+        torch.mul(self.pmask, rows[None, :], out=self.meta_send[:, P:])
         dist.all_to_all_single(self.meta_recv, self.meta_send, group=self.group)
         host = torch.stack([self.meta_send, self.meta_recv]).cpu().numpy()
         return plan_exchange(host[0], host[1])
 
-    # ---------------------------------------------------------------- step
     def forward(self):
         L, s = self.lib, _lib.stream_ptr(self.dev)
-        R, B, D, F = self.R, self.B, self.D, self.F
+        R, S, B, D, F = self.R, self.S, self.B, self.D, self.F
         if self.op == "max":
             raise ValueError("the row-sharded path supports sum/avg pooling")
         self.marks = []
@@ -250,124 +280,206 @@ class ShardedTrainStep:
                           self.s_dedup.data_ptr(), self.s_dedup.numel(), s)
         _lib.check(rc, "recd_dedup")
         self._mark("dedup")
-        # 2. IDs per owner
-        rc = L.recd_shard_bucketize(F, R, B, self.a_uvalues, self.a_uoffsets, self.counts.data_ptr(),
+        # 2. unique IDs bucketized by shard: ids_send[f] = [shard 0][shard 1]..
+        rc = L.recd_shard_bucketize(F, S, B, self.a_uvalues, self.a_uoffsets, self.counts.data_ptr(),
                                     self.a_ids_send, self.a_rowcnt, self.totals.data_ptr(),
                                     self.s_shard.data_ptr(), self.s_shard.numel(), s)
         _lib.check(rc, "recd_shard_bucketize")
         self._mark("bucketize")
         # 3. split sizes (the one host sync of the step)
         pl = self.plan = self._exchange_counts()
-        # 4. IDs + per-row counts to the owners: pack [o][counts f..][IDs f..],
-        #    one all-to-all, unpack per feature in source order
-        U = [int(x) for x in pl.send_rows]
+        mine, by_dest = self.mine, self.by_dest
+        sid = [int(x) for x in pl.send_ids]
+        U = [int(pl.send_rows[f * S]) for f in range(F)]
+        ibase = [0] * (F * S)
+        for f in range(F):
+            for j in range(1, S):
+                ibase[f * S + j] = ibase[f * S + j - 1] + sid[f * S + j - 1]
+        # 4. IDs + per-row counts to the owners, packed per destination as
+        #    [row counts of its pairs][IDs of its pairs]; one all-to-all
+        sendA = self._buf("sendA", sum(U[p // S] + sid[p] for p in range(F * S)))
         segs, send_split, pos = [], [], 0
-        for o in range(R):
+        for d in range(R):
             start = pos
-            for f in range(F):
-                segs.append((self.rowcnt_send[f].data_ptr() + 8 * o * B,
-                             self.sendA.data_ptr() + 8 * pos, 8 * U[f]))
+            for p in by_dest[d]:
+                f, j = divmod(p, S)
+                segs.append((self.rowcnt_send[f].data_ptr() + 8 * j * B,
+                             sendA.data_ptr() + 8 * pos, 8 * U[f]))
                 pos += U[f]
-            for f in range(F):
-                n = int(pl.send_ids[o, f])
-                segs.append((self.ids_send[f].data_ptr() + 8 * pl.send_id_base(f, o),
-                             self.sendA.data_ptr() + 8 * pos, 8 * n))
-                pos += n
+            for p in by_dest[d]:
+                segs.append((self.ids_send[p // S].data_ptr() + 8 * ibase[p],
+                             sendA.data_ptr() + 8 * pos, 8 * sid[p]))
+                pos += sid[p]
             send_split.append(pos - start)
         self._copy(0, segs)
         recv_split = [int(pl.recv_rows[src].sum() + pl.recv_ids[src].sum()) for src in range(R)]
-        dist.all_to_all_single(self.recvA[:sum(recv_split)], self.sendA[:pos], recv_split,
-                               send_split, group=self.group)
+        recvA = self._buf("recvA", sum(recv_split))
+        dist.all_to_all_single(recvA[:sum(recv_split)], sendA[:pos], recv_split, send_split,
+                               group=self.group)
+        # owner side, exact sizes: unpack per pair in source order
+        self.orows = {p: pl.owner_rows(p) for p in mine}
+        self.oids = {p: pl.owner_ids(p) for p in mine}
+        rc_recv = {p: self._buf(f"rc{p}", self.orows[p]) for p in mine}
+        self.ro = {p: self._buf(f"ro{p}", self.orows[p]) for p in mine}
+        self.ids_recv = {p: self._buf(f"ids{p}", self.oids[p]) for p in mine}
         segs, pos = [], 0
         for src in range(R):
-            for f in range(F):
-                n = int(pl.recv_rows[src, f])
-                segs.append((self.recvA.data_ptr() + 8 * pos,
-                             self.rc_recv[f].data_ptr() + 8 * pl.recv_row_base(f, src), 8 * n))
+            for p in mine:
+                n = int(pl.recv_rows[src, p])
+                segs.append((recvA.data_ptr() + 8 * pos,
+                             rc_recv[p].data_ptr() + 8 * pl.recv_row_base(p, src), 8 * n))
                 pos += n
-            for f in range(F):
-                n = int(pl.recv_ids[src, f])
-                segs.append((self.recvA.data_ptr() + 8 * pos,
-                             self.ids_recv[f].data_ptr() + 8 * pl.recv_id_base(f, src), 8 * n))
+            for p in mine:
+                n = int(pl.recv_ids[src, p])
+                segs.append((recvA.data_ptr() + 8 * pos,
+                             self.ids_recv[p].data_ptr() + 8 * pl.recv_id_base(p, src), 8 * n))
                 pos += n
         self._copy(1, segs)
         self._mark("exchange_ids")
         # 5. owner: row offsets of the received jagged lists, owner counts
-        orows = [pl.owner_rows(f) for f in range(F)]
-        oids = [pl.owner_ids(f) for f in range(F)]
-        self.counts_owner.copy_(torch.tensor(orows + oids, dtype=torch.int64))
-        rc = L.recd_exclusive_scan(F, self.a_rc, self.a_ro, _lib.i64s([max(n, 1) for n in orows]),
-                                   None, None, self.s_scan.data_ptr(), self.s_scan.numel(), s)
-        _lib.check(rc, "recd_exclusive_scan")
-        # 6. owner: partial pooled rows (sum of the owned share of every row)
-        rc = L.recd_pool_fwd(F, R * B, D, _lib.POOL_MODES["sum"],
-                             self.a_tables, self.a_rows, self.a_ids_recv, self.a_ro,
-                             self.counts_owner.data_ptr(), None, self.a_part, None,
-                             self.err.data_ptr(), s)
-        _lib.check(rc, "recd_pool_fwd(owner)")
-        self._mark("owner_pool")
-        # 7. partial rows back to the sources: pack [s][f rows], one all-to-all;
-        #    the source receives [o][f][U_f rows] and sums the owners in order
+        if mine:
+            cap = [max(self.orows[p], 1) for p in mine]
+            scr = self._buf("scan", L.recd_exclusive_scan_scratch_bytes(len(mine), _lib.i64s(cap)),
+                            torch.uint8)
+            rc = L.recd_exclusive_scan(len(mine), _lib.ptrs([rc_recv[p] for p in mine]),
+                                       _lib.ptrs([self.ro[p] for p in mine]), _lib.i64s(cap),
+                                       None, None, scr.data_ptr(), scr.numel(), s)
+            _lib.check(rc, "recd_exclusive_scan")
+        host = [self.orows[p] for gp in self.g_mine for p in gp] + \
+               [self.oids[p] for gp in self.g_mine for p in gp]
+        oc = torch.tensor(host or [0], dtype=torch.int64).to(self.dev)
+        self.counts_owner, n_m, o0 = [], len(host) // 2, 0
+        for gi, gp in enumerate(self.g_mine):
+            self.counts_owner.append(torch.cat([oc[o0:o0 + len(gp)], oc[n_m + o0:n_m + o0 + len(gp)]]))
+            o0 += len(gp)
+            torch.index_select(self.counts, 0, self.g_idx[gi], out=self.g_counts[gi])
+        self._mark("owner_scan")
+        # 6-7. per feature group: owner partial pooling, packed partial rows back
+        #      to the sources (async all-to-all on NCCL's stream overlaps the
+        #      next group's pooling)
         row = 4 * D
-        segs, send_split, pos = [], [], 0
-        for src in range(R):
-            start = pos
-            for f in range(F):
-                n = int(pl.recv_rows[src, f])
-                segs.append((self.part[f].data_ptr() + row * pl.recv_row_base(f, src),
-                             self.sendB.data_ptr() + row * pos, row * n))
-                pos += n
-            send_split.append((pos - start) * D)
-        self._copy(2, segs)
-        tot_u = sum(U)
-        dist.all_to_all_single(self.recvB.view(-1)[:R * tot_u * D], self.sendB.view(-1)[:pos * D],
-                               [tot_u * D] * R, send_split, group=self.group)
-        self._mark("exchange_pooled")
-        # 8. source: owner-order sum (+ avg scaling), expansion.  Feature f of
-        #    owner o starts at row o * tot_u + sum(U[:f]) of recvB.
-        ret = [self.recvB[sum(U[:f]):] for f in range(F)]
-        rc = L.recd_shard_combine(F, R, max(tot_u, 1), D, self.mode_id, _lib.ptrs(ret),
-                                  self.a_uoffsets, self.counts.data_ptr(), self.a_pooled, s)
-        _lib.check(rc, "recd_shard_combine")
-        rc = L.recd_expand(F, B, D, self.a_inverse, self.a_pooled, self.a_out, s)
-        _lib.check(rc, "recd_expand")
-        self._mark("combine_expand")
+        works = []
+        for gi, g in enumerate(self.groups):
+            gp = self.g_mine[gi]
+            part = {p: self._buf(f"part{p}", self.orows[p], torch.float32, D) for p in gp}
+            if gp:
+                rc = L.recd_pool_fwd(len(gp), R * B, D, _lib.POOL_MODES["sum"],
+                                     _lib.ptrs([self.tables[p].weights for p in gp]),
+                                     _lib.i64s([self.tables[p].rows for p in gp]),
+                                     _lib.ptrs([self.ids_recv[p] for p in gp]),
+                                     _lib.ptrs([self.ro[p] for p in gp]),
+                                     self.counts_owner[gi].data_ptr(), None,
+                                     _lib.ptrs([part[p] for p in gp]), None,
+                                     self.err.data_ptr(), s)
+                _lib.check(rc, "recd_pool_fwd(owner)")
+            sendB = self._buf(f"sendB{gi}", sum(self.orows[p] for p in gp), torch.float32, D)
+            segs, send_split, pos = [], [], 0
+            for src in range(R):
+                start = pos
+                for p in gp:
+                    n = int(pl.recv_rows[src, p])
+                    segs.append((part[p].data_ptr() + row * pl.recv_row_base(p, src),
+                                 sendB.data_ptr() + row * pos, row * n))
+                    pos += n
+                send_split.append((pos - start) * D)
+            self._copy(2 + gi, segs)
+            # from owner o: the pairs of this group it owns, U_f rows each
+            recv_split, blocks, rpos = [], {}, 0
+            for o in range(R):
+                start = rpos
+                for p in by_dest[o]:
+                    if p // S in g:
+                        blocks[p] = rpos
+                        rpos += U[p // S]
+                recv_split.append((rpos - start) * D)
+            recvB = self._buf(f"recvB{gi}", rpos, torch.float32, D)
+            work = dist.all_to_all_single(recvB.view(-1)[:rpos * D], sendB.view(-1)[:pos * D],
+                                          recv_split, send_split, group=self.group, async_op=True)
+            works.append((work, recvB, blocks))
+        self._mark("owner_pool")
+        # 8. per group: shard-order sum (+ avg scaling), expansion
+        for gi, g in enumerate(self.groups):
+            work, recvB, blocks = works[gi]
+            work.wait()
+            blk = [recvB[blocks[f * S + j]:] for f in g for j in range(S)]
+            rc = L.recd_shard_combine(len(g), S, B, D, self.mode_id, _lib.ptrs(blk),
+                                      _lib.ptrs([self.uoffsets[f] for f in g]),
+                                      self.g_counts[gi].data_ptr(),
+                                      _lib.ptrs([self.pooled[f] for f in g]), s)
+            _lib.check(rc, "recd_shard_combine")
+            rc = L.recd_expand(len(g), B, D, _lib.ptrs([self.inverse[f] for f in g]),
+                               _lib.ptrs([self.pooled[f] for f in g]),
+                               _lib.ptrs([self.out[f] for f in g]), s)
+            _lib.check(rc, "recd_expand")
+        self._U = U
+        self._mark("exchange_combine")
 
     def backward(self):
         L, s = self.lib, _lib.stream_ptr(self.dev)
-        R, B, D, F = self.R, self.B, self.D, self.F
-        pl = self.plan
-        U = [int(x) for x in pl.send_rows]
-        # grad_u of every feature written packed: feature f at row sum(U[:f])
-        gptr = [self.gradG[sum(U[:f]):] for f in range(F)]
+        R, S, B, D, F = self.R, self.S, self.B, self.D, self.F
+        pl, U, by_dest = self.plan, self._U, self.by_dest
+        gbase = np.concatenate([[0], np.cumsum(U)]).astype(np.int64).tolist()
         rc = L.recd_grad_unique(F, B, D, self.mode_id, self.a_uoffsets, self.counts.data_ptr(),
-                                self.a_inverse, self.a_grad_out, _lib.ptrs(gptr),
+                                self.a_inverse, self.a_grad_out,
+                                _lib.ptrs([self.gradG[gbase[f]:] for f in range(F)]),
                                 self.s_grad.data_ptr(), self.s_grad.numel(), s)
         _lib.check(rc, "recd_grad_unique")
         self._mark("grad_unique")
-        # every owner needs every source's unique-row grads: one all-gather
-        # (padded to the largest source), then unpack per feature in source order
-        rows_of = pl.recv_rows.sum(axis=1).astype(np.int64)  # per source
-        mx = int(rows_of.max())
-        dist.all_gather_into_tensor(self.recvG.view(-1)[:R * mx * D], self.gradG.view(-1)[:mx * D],
-                                    group=self.group)
-        row = 4 * D
-        segs = []
-        for src in range(R):
-            pos = src * mx
-            for f in range(F):
-                n = int(pl.recv_rows[src, f])
-                segs.append((self.recvG.data_ptr() + row * pos,
-                             self.grad_recv[f].data_ptr() + row * pl.recv_row_base(f, src), row * n))
-                pos += n
-        self._copy(3, segs)
-        self._mark("exchange_grads")
-        rc = L.recd_sparse_sgd(F, R * B, D, self.a_tables, self.a_rows, self.a_ids_recv, self.a_ro,
-                               self.a_ocaps, self.counts_owner.data_ptr(), self.a_grad_recv,
-                               C.c_float(self.lr), 1, None, None, None, self.s_sgd.data_ptr(),
-                               self.s_sgd.numel(), s)
-        _lib.check(rc, "recd_sparse_sgd")
-        self._mark("owner_sgd")
+        # per group, to every owner of one of its pairs: that feature's
+        # unique-row gradients; all issued now so they run back to back while
+        # the owners scatter the earlier groups
+        row, ng = 4 * D, len(self.groups)
+        works = []
+        for gi, g in enumerate(self.groups):
+            n_send = sum(U[p // S] for d in range(R) for p in by_dest[d] if p // S in g)
+            sendG = self._buf(f"sendG{gi}", n_send, torch.float32, D)
+            segs, send_split, pos = [], [], 0
+            for d in range(R):
+                start = pos
+                for p in by_dest[d]:
+                    f = p // S
+                    if f in g:
+                        segs.append((self.gradG.data_ptr() + row * gbase[f],
+                                     sendG.data_ptr() + row * pos, row * U[f]))
+                        pos += U[f]
+                send_split.append((pos - start) * D)
+            self._copy(2 + ng + gi, segs)
+            gp = self.g_mine[gi]
+            recv_split = [sum(int(pl.recv_rows[src, p]) for p in gp) * D for src in range(R)]
+            nrecv = sum(recv_split) // D
+            recvG = self._buf(f"recvG{gi}", nrecv, torch.float32, D)
+            work = dist.all_to_all_single(recvG.view(-1)[:nrecv * D], sendG.view(-1)[:pos * D],
+                                          recv_split, send_split, group=self.group, async_op=True)
+            works.append((work, recvG))
+        for gi, g in enumerate(self.groups):
+            work, recvG = works[gi]
+            work.wait()
+            gp = self.g_mine[gi]
+            if not gp:
+                continue
+            # received [source][pair][row]; each pair's SGD wants [source][row]
+            grad = {p: self._buf(f"grad{p}", self.orows[p], torch.float32, D) for p in gp}
+            segs, pos = [], 0
+            for src in range(R):
+                for p in gp:
+                    n = int(pl.recv_rows[src, p])
+                    segs.append((recvG.data_ptr() + row * pos,
+                                 grad[p].data_ptr() + row * pl.recv_row_base(p, src), row * n))
+                    pos += n
+            self._copy(2 + 2 * ng + gi, segs)
+            caps = [max(self.oids[p], 1) for p in gp]
+            scr = self._buf("sgd", L.recd_sparse_sgd_scratch_bytes(len(gp), _lib.i64s(caps)),
+                            torch.uint8)
+            rc = L.recd_sparse_sgd(len(gp), R * B, D,
+                                   _lib.ptrs([self.tables[p].weights for p in gp]),
+                                   _lib.i64s([self.tables[p].rows for p in gp]),
+                                   _lib.ptrs([self.ids_recv[p] for p in gp]),
+                                   _lib.ptrs([self.ro[p] for p in gp]), _lib.i64s(caps),
+                                   self.counts_owner[gi].data_ptr(),
+                                   _lib.ptrs([grad[p] for p in gp]), C.c_float(self.lr), 1,
+                                   None, None, None, scr.data_ptr(), scr.numel(), s)
+            _lib.check(rc, "recd_sparse_sgd")
+        self._mark("exchange_sgd")
 
     def run(self):
         self.forward()

@@ -3,7 +3,8 @@
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/dist_sharded_check.py
 
 Each rank deduplicates its contiguous chunk of one global session-clustered
-batch and owns rows id % R == rank of every table.  Checked against the CPU
+batch; every table is split into S = $SHARDS (default R) shards id % S, the
+(table, shard) pairs placed on ranks by the step's LPT placement.  Checked against the CPU
 oracle (oracle/), on the same inputs:
   * dedup outputs (inverse, unique values/offsets): bit-exact
   * expanded pooled outputs: allclose(rtol=1e-5, atol=1e-5 * max|ref|)
@@ -27,7 +28,7 @@ import oracle  # noqa: E402
 import paper_2211_05239_b200 as R  # noqa: E402
 from paper_2211_05239_b200.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
                                            generate_clustered_batch)
-from paper_2211_05239_b200.sharded import ShardedTrainStep, shard_rows  # noqa: E402
+from paper_2211_05239_b200.sharded import ShardedTrainStep  # noqa: E402
 
 
 def close(a, b):
@@ -52,11 +53,16 @@ def main():
     mine = chunks[rank]
     full = {k: np.random.default_rng(100 + i).uniform(-0.1, 0.1, size=(rows, D)).astype(np.float32)
             for i, k in enumerate(keys)}
-    local_tables = {k: R.EmbeddingTable(k, shard_rows(rows, world, rank), D,
-                                        torch.from_numpy(np.ascontiguousarray(full[k][rank::world]))
-                                        .to(dev)) for k in keys}
+    S = int(os.environ.get("SHARDS", world))
+
+    def make_table(k, j, n):
+        w = torch.from_numpy(np.ascontiguousarray(full[k][j::S])).to(dev)
+        assert w.shape[0] == n
+        return R.EmbeddingTable(k, n, D, w)
+
     caps = {k: mine.values[k].size for k in keys}
-    step = ShardedTrainStep(keys, B, caps, local_tables, op, lr, device=dev)
+    step = ShardedTrainStep(keys, B, caps, {k: rows for k in keys}, D, make_table, op, lr,
+                            shards=S, device=dev)
     step.load_batch(mine.values, mine.offsets)
     grads = [np.random.default_rng(1000 * r + 7).standard_normal((B, D)).astype(np.float32)
              for r in range(world)]
@@ -65,7 +71,8 @@ def main():
     step.run()
     torch.cuda.synchronize()
 
-    res = {"rank": rank, "world": world, "op": op, "ok": True}
+    res = {"rank": rank, "world": world, "shards": S, "op": op, "ok": True,
+           "pairs": step.mine}
     U, N = step.host_counts()
     # forward vs oracle on this rank's chunk
     worst_fwd = 0.0
@@ -83,14 +90,13 @@ def main():
     # backward: gather the shards, compare with the oracle SGD over all ranks
     worst_bwd = 0.0
     for f, k in enumerate(keys):
-        w = local_tables[k].weights
-        pad = torch.zeros((shard_rows(rows, world, 0), D), device=dev)
-        pad[: w.shape[0]] = w
-        parts = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(parts, pad)
-        new = np.empty((rows, D), np.float32)
-        for r in range(world):
-            new[r::world] = parts[r][: shard_rows(rows, world, r)].cpu().numpy()
+        # every row lives on exactly one rank: a sum over ranks reassembles the table
+        new_t = torch.zeros((rows, D), device=dev)
+        for p, t in step.tables.items():
+            if p // S == f:
+                new_t[p % S::S] = t.weights
+        dist.all_reduce(new_t)
+        new = new_t.cpu().numpy()
         g64 = np.zeros((rows, D), np.float64)
         for r in range(world):
             inv, [(uv, uo)] = oracle.build_ikjt_arrays([(chunks[r].values[k], chunks[r].offsets[k])])

@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2211_05239_b200.sharded import plan_exchange, shard_rows
+from paper_2211_05239_b200.sharded import place_pairs, plan_exchange, shard_rows
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -24,28 +24,44 @@ def test_shard_rows_partition():
             assert sizes == [len(range(r, rows, R)) for r in range(R)]
 
 
+def test_place_pairs_lpt():
+    # equal weights spread evenly; heavy pairs go to distinct ranks
+    assert sorted(place_pairs([1.0] * 8, 4)) == [0, 0, 1, 1, 2, 2, 3, 3]
+    pl = place_pairs([10.0, 10.0, 1.0, 1.0, 1.0, 1.0], 2)
+    assert pl[0] != pl[1]
+    load = [0.0, 0.0]
+    for p, r in enumerate(pl):
+        load[r] += [10.0, 10.0, 1.0, 1.0, 1.0, 1.0][p]
+    assert load == [12.0, 12.0]
+    assert place_pairs([3.0, 1.0, 2.0], 1) == [0, 0, 0]
+    assert place_pairs([5.0, 5.0], 4) == [0, 1]   # deterministic tie-break
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    F = 3
+    F, S = 3, 3                                   # more shards than ranks
+    P = F * S
+    place = place_pairs([float(1 + p // S) for p in range(P)], world)
     rng = np.random.default_rng(rank)
-    send = np.zeros((world, 2 * F), np.int64)
-    send[:, :F] = rng.integers(0, 50, size=(world, F))      # IDs for owner o
-    send[:, F:] = rng.integers(1, 20, size=F)[None, :]      # unique rows (same for every owner)
-    gathered = [torch.zeros((world, 2 * F), dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(gathered, torch.from_numpy(send))
-    recv = np.stack([gathered[s].numpy()[rank] for s in range(world)])  # what all_to_all delivers
-    pl = plan_exchange(send, recv)
-    ok = True
-    for f in range(F):
-        # bases are prefix sums, owner totals are the sums
-        ok &= pl.recv_id_base(f, world - 1) + pl.recv_ids[world - 1, f] == pl.owner_ids(f)
-        ok &= pl.owner_rows(f) == sum(gathered[s].numpy()[rank][F + f] for s in range(world))
-        ok &= pl.send_id_base(f, world - 1) + pl.send_ids[world - 1, f] == send[:, f].sum()
-    # global conservation: IDs sent == IDs received
-    tot = torch.tensor([int(send[:, :F].sum()), int(pl.recv_ids.sum())], dtype=torch.int64)
+    ids = rng.integers(0, 50, size=P)             # this rank's IDs per (table, shard)
+    urows = np.repeat(rng.integers(1, 20, size=F), S)
+    mask = (np.array(place)[None, :] == np.arange(world)[:, None]).astype(np.int64)
+    send = np.concatenate([mask * ids[None, :], mask * urows[None, :]], axis=1)
+    recv = torch.zeros((world, 2 * P), dtype=torch.int64)
+    dist.all_to_all_single(recv, torch.from_numpy(send))
+    pl = plan_exchange(send, recv.numpy())
+    ok = bool((pl.send_ids == ids).all() and (pl.send_rows == urows).all())
+    for p in range(P):
+        if place[p] != rank:
+            ok &= pl.owner_rows(p) == 0 and pl.owner_ids(p) == 0
+        ok &= pl.recv_id_base(p, world - 1) + pl.recv_ids[world - 1, p] == pl.owner_ids(p)
+        ok &= pl.recv_row_base(p, world - 1) + pl.recv_rows[world - 1, p] == pl.owner_rows(p)
+    # global conservation: IDs / rows sent == received
+    tot = torch.tensor([int(ids.sum()), int(pl.recv_ids.sum()),
+                        int(urows.sum()), int(pl.recv_rows.sum())], dtype=torch.int64)
     dist.all_reduce(tot)
-    ok &= int(tot[0]) == int(tot[1])
+    ok &= int(tot[0]) == int(tot[1]) and int(tot[2]) == int(tot[3])
     q.put(bool(ok))
     dist.destroy_process_group()
 
@@ -63,11 +79,11 @@ def test_exchange_plan_gloo_world2():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("op", ["sum", "avg"])
-def test_sharded_step_two_gpus(op):
+@pytest.mark.parametrize("op,shards", [("sum", 2), ("avg", 2), ("sum", 1), ("sum", 3)])
+def test_sharded_step_two_gpus(op, shards):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
-    env = dict(os.environ, POOL_OP=op)
+    env = dict(os.environ, POOL_OP=op, SHARDS=str(shards))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node=2", "--master-addr=127.0.0.1",
                         f"--master-port={29600 + os.getpid() % 1000}",
