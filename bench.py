@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--dist", choices=["geometric", "fixed"], default="geometric")
     ap.add_argument("--change-prob", type=float, default=0.15)
     ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="N>1: exchange over NVLink peer memory (graph) or NCCL")
     ap.add_argument("--shards", type=int, default=0,
                     help="N>1: row shards per table (0 = N, one per rank)")
     ap.add_argument("--no-graph", action="store_true")
@@ -461,6 +463,7 @@ def run_sharded(args, world, rank, local, dev):
     import torch.distributed as dist
 
     import paper_2211_05239_b200 as R
+    from paper_2211_05239_b200.peer import PeerShardedStep
     from paper_2211_05239_b200.sharded import ShardedTrainStep
 
     t_setup = time.perf_counter()
@@ -473,8 +476,10 @@ def run_sharded(args, world, rank, local, dev):
                                                  seed=1000 * keys.index(k) + j, device=dev)
 
     caps = {k: batch.values[k].size for k in keys}
-    step = ShardedTrainStep(keys, args.batch, caps, {k: args.rows for k in keys}, args.dim,
-                            make_table, "sum", args.lr, shards=S, device=dev)
+    cls = PeerShardedStep if args.transport == "peer" else ShardedTrainStep
+    step = cls(keys, args.batch, caps, {k: args.rows for k in keys}, args.dim, make_table, "sum",
+               args.lr, shards=S, device=dev)
+    peer = args.transport == "peer"
     lrows = sum(t.rows for t in step.tables.values())
     step.load_batch(batch.values, batch.offsets)
     step.fill_grad_out(1 + rank)
@@ -482,9 +487,13 @@ def run_sharded(args, world, rank, local, dev):
     setup_s = time.perf_counter() - t_setup
     stream = torch.cuda.current_stream(dev)
     B, K, D = args.batch, len(keys), args.dim
+    if peer:
+        step.capture()        # fwd + bwd of every rank: one CUDA graph, no host sync
     for _ in range(max(1, args.warmup)):
-        step.run()
+        step.replay() if peer else step.run()
     torch.cuda.synchronize()
+    if peer:
+        step.check()
     U, N_u = step.host_counts()
 
     sampler = ClockSampler(local) if not args.profile else None
@@ -495,10 +504,12 @@ def run_sharded(args, world, rank, local, dev):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        step.run()
+        step.replay() if peer else step.run()
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
+    if peer:
+        step.check()
     ms = e0.elapsed_time(e1) / args.steps
     clocks = sampler.stop() if sampler else None
     launches_per_step = (R.launch_count() - launches0) // max(args.steps, 1)
@@ -509,7 +520,10 @@ def run_sharded(args, world, rank, local, dev):
 
     # sub-phase breakdown (one traced step per rank, max over ranks)
     step.trace = True
+    l0 = R.launch_count()
     step.run()
+    if peer:   # graph replays do not pass through the host counter: count this eager step
+        launches_per_step = R.launch_count() - l0
     ph = step.phase_ms()
     step.trace = False
     names = list(ph)
@@ -517,10 +531,17 @@ def run_sharded(args, world, rank, local, dev):
     dist.all_reduce(tph, op=dist.ReduceOp.MAX)
     ph = dict(zip(names, tph.tolist()))
     # per-rank communication volume of the step (bytes sent)
-    pl = step.plan
-    sent = 8 * int(pl.send_ids.sum()) + 8 * int(pl.send_rows.sum())  # ids + row counts
-    sent += 4 * D * int(pl.recv_rows.sum())  # partial pooled rows returned
-    sent += 4 * D * int(pl.send_rows.sum())  # unique-row gradients (one copy per shard)
+    if peer:
+        P = step.P
+        meta = step.ctl[128:128 + world * 2 * P].view(world, 2 * P).cpu().numpy()
+        send_ids, send_rows = meta[rank, :P], meta[rank, P:]
+        recv_rows = meta[:, P:][:, step.mine]
+    else:
+        pl = step.plan
+        send_ids, send_rows, recv_rows = pl.send_ids, pl.send_rows, pl.recv_rows
+    sent = 8 * int(send_ids.sum()) + 8 * int(send_rows.sum())  # ids + row offsets / counts
+    sent += 4 * D * int(recv_rows.sum())  # partial pooled rows returned
+    sent += 4 * D * int(send_rows.sum())  # unique-row gradients (one copy per shard)
     N_kjt = int(sum(caps.values()))
 
     e2e = None
@@ -537,7 +558,7 @@ def run_sharded(args, world, rank, local, dev):
             for f, k in enumerate(keys):
                 step.in_values[f][: pin_v[k].numel()].copy_(pin_v[k], non_blocking=True)
                 step.in_offsets[f].copy_(pin_o[k], non_blocking=True)
-            step.run()
+            step.replay() if peer else step.run()
             res.copy_(step.counts, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
         e2e_s = (time.perf_counter() - t0) / n_e2e
@@ -546,12 +567,14 @@ def run_sharded(args, world, rank, local, dev):
         e2e_s = float(t.item())
         e2e = {"value": world * B / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": res.numel() * 8, "ms_per_step": e2e_s * 1e3,
-               "how": "ShardedTrainStep on every rank: pinned-host KJT -> H2D -> step -> D2H "
+               "how": f"{cls.__name__} on every rank: pinned-host KJT -> H2D -> step -> D2H "
                       "of the dedup counts; max over ranks"}
     if rank == 0:
         cfg = config_dict(args, "gpu")
         cfg["parallelism"] = (f"dp{world} x {S}-way row-sharded tables (shard = id mod {S}), "
                               f"(table, shard) pairs placed LPT")
+        cfg["transport"] = ("NVLink peer memory (CUDA IPC), whole step one CUDA graph" if peer
+                            else "NCCL all-to-all, host-planned split sizes")
         cfg["table_rows_rank0"] = lrows
         cfg["pairs_rank0"] = len(step.mine)
         line = {
@@ -567,6 +590,8 @@ def run_sharded(args, world, rank, local, dev):
             "gpu_launches_per_step": launches_per_step, "clocks": clocks, "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
+    if peer:
+        step.close()
     dist.destroy_process_group()
     return 0
 

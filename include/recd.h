@@ -19,8 +19,9 @@
  *   recd_grad_unique /         the two halves of recd_pool_bwd, used by the row-sharded
  *   recd_sparse_sgd            multi-GPU step (grad onto unique rows at the source,
  *                              sorted scatter-add + SGD at the table owner)
- *   recd_shard_bucketize /     row-sharded tables over R ranks: deduplicated IDs per
- *   recd_shard_combine         owner, owner-order sum of partially pooled rows
+ *   recd_shard_* /             row-sharded tables over R ranks: deduplicated IDs per
+ *   recd_peer_*                (table, shard) pair to its owner (over NVLink peer
+ *                              memory), shard-order sum of partially pooled rows
  *                              (the reference only simulates ranks,
  *                              trainer_sim.py:281-305)
  *   recd_jagged_index_select_* <- tensors.jagged_index_select   (tensors.py:363-390)
@@ -180,17 +181,39 @@ int recd_sparse_sgd(int32_t num_features, int64_t max_rows, int32_t dim, float* 
                     recd_stream_t stream);
 
 /* ------------------------------------------------------- row sharding --
- * owner(id) = id mod R, local row = id div R.
- * bucketize: for every feature f, ids_out[f] = the local IDs of its unique
- *   values grouped by owner (owner-major, then unique row, then position);
- *   rowcnt_out[f][o * batch_size + u] = values of row u owned by o;
- *   totals_out[f * R + o] (device) = IDs of f owned by o.
+ * Every table is split into S row shards: shard(id) = id mod S, local row =
+ * id div S; pair p = f * S + j is (table f, shard j), F * S <= 256, S <= 64.
+ * count:    rowoff_out[f][j * batch_size + u] = exclusive offset of row u's
+ *   shard-j values among all shard-j values of f (rows in order, values in
+ *   row order); totals_out[p] (device) = values of f in shard j.
+ * dispatch: every value v of unique row u goes to
+ *   dst_ids[p][id_base[p] + rowoff[f][j][u] + k] = v div S (k = its rank
+ *   among the row's shard-j values), and dst_rowoffs[p][row_base[p] + u] =
+ *   id_base[p] + rowoff[f][j][u] when dst_rowoffs (and dst_rowoffs[p]) is
+ *   set.  id_base / row_base: device int64[P]; id_base NULL = prefix of
+ *   totals over the shards of f, row_base NULL = 0.  Destinations may be peer
+ *   memory (recd_peer_import).
+ * bucketize: count + dispatch into ids_out[f] (shard-major, then unique row,
+ *   then position) and rowcnt_out[f][j * batch_size + u] = values of row u in
+ *   shard j.
  * combine:   pooled_out[f][u] = sum over j = 0..num_blocks-1 (in that order) of
  *   blocks[f * num_blocks + j][u * dim ...] (the partial rows of shard j of
  *   feature f, F * num_blocks <= 256); avg divides by the row length;
  *   batch_size bounds the unique rows (launch geometry). */
-size_t recd_shard_scratch_bytes(int32_t num_features, int32_t num_ranks, int64_t batch_size);
-int recd_shard_bucketize(int32_t num_features, int32_t num_ranks, int64_t batch_size,
+size_t recd_shard_count_scratch_bytes(int32_t num_features, int32_t num_shards,
+                                      int64_t batch_size);
+int recd_shard_count(int32_t num_features, int32_t num_shards, int64_t batch_size,
+                     const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                     const int64_t* counts, int64_t* const* rowoff_out, int64_t* totals_out,
+                     void* scratch, size_t scratch_bytes, recd_stream_t stream);
+int recd_shard_dispatch(int32_t num_features, int32_t num_shards, int64_t batch_size,
+                        const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                        const int64_t* counts, const int64_t* const* rowoff,
+                        const int64_t* totals, const int64_t* id_base, const int64_t* row_base,
+                        int64_t* const* dst_ids, int64_t* const* dst_rowoffs,
+                        recd_stream_t stream);
+size_t recd_shard_scratch_bytes(int32_t num_features, int32_t num_shards, int64_t batch_size);
+int recd_shard_bucketize(int32_t num_features, int32_t num_shards, int64_t batch_size,
                          const int64_t* const* uvalues, const int64_t* const* uoffsets,
                          const int64_t* counts, int64_t* const* ids_out, int64_t* const* rowcnt_out,
                          int64_t* totals_out, void* scratch, size_t scratch_bytes,
@@ -198,6 +221,53 @@ int recd_shard_bucketize(int32_t num_features, int32_t num_ranks, int64_t batch_
 int recd_shard_combine(int32_t num_features, int32_t num_blocks, int64_t batch_size, int32_t dim,
                        int32_t mode, const float* const* blocks, const int64_t* const* uoffsets,
                        const int64_t* counts, float* const* pooled_out, recd_stream_t stream);
+
+/* ------------------------------------------- peer (NVLink) transport --
+ * The sharded step without host synchronisation: every rank exports one
+ * zeroed device allocation (recd_peer_alloc / _export), the others map it
+ * (recd_peer_import), and kernels store straight into peer buffers.
+ * Control block = int64 words at the start of every rank's allocation:
+ *   [0, 64)          arrival flags: word s = last epoch rank s signalled here
+ *   [64]             epoch of this rank's last exchange
+ *   [65]             error: 1 = some peer did not arrive within timeout_ns
+ *   [128, 128+2RP)   meta[s][p] = IDs source s sends to pair p,
+ *                    meta[s][P + p] = unique rows of f(p) at source s
+ *   then this rank's plan, at 128 + 2RP:
+ *     [0, P)           src_id_base[p]  = sum_{s < rank} meta[s][p]
+ *     [P, 2P)          src_row_base[p] = sum_{s < rank} meta[s][P + p]
+ *     [2P, 2P+2Q)      owned-pair counts: rows of owned[q] (all sources), then IDs
+ *     [2P+2Q, +Q*R)    owner_row_base[q * R + s] = sum_{s' < s} meta[s'][P + owned[q]]
+ * exchange: with totals (device int64[P]) stores meta[rank] = (totals,
+ *   counts[p / S] of every pair) into every rank's block, then barriers, then
+ *   writes the plan; with totals NULL it is a bare barrier.  peer_ctl host
+ *   [R]: every rank's control block as mapped here (own included); owned
+ *   host [Q] pair ids.  Never waits longer than timeout_ns; on timeout it sets
+ *   the error word and every later exchange returns at once.
+ * copy_rows: segment i copies ctl[count_idx] rows of row_bytes (multiple of
+ *   16) from src + ctl[src_off_idx] rows to dst + ctl[dst_off_idx] rows (an
+ *   index < 0 reads as 0); segs is a DEVICE array; max_rows bounds every
+ *   count (launch geometry). */
+#define RECD_PEER_HANDLE_BYTES 64
+#define RECD_CTL_META 128
+typedef struct recd_row_seg {
+  const void* src;
+  void* dst;
+  int64_t count_idx;
+  int64_t src_off_idx;
+  int64_t dst_off_idx;
+} recd_row_seg;
+int64_t recd_peer_ctl_words(int32_t num_ranks, int32_t num_pairs, int32_t num_owned);
+int recd_peer_alloc(size_t bytes, void** ptr_out);
+int recd_peer_free(void* ptr);
+int recd_peer_export(const void* ptr, void* handle_out);
+int recd_peer_import(const void* handle, void** ptr_out);
+int recd_peer_close(void* ptr);
+int recd_peer_exchange(int32_t num_ranks, int32_t rank, int32_t num_pairs, int32_t num_shards,
+                       int32_t num_owned, const int32_t* owned, void* const* peer_ctl,
+                       const int64_t* totals, const int64_t* counts, int64_t timeout_ns,
+                       recd_stream_t stream);
+int recd_peer_copy_rows(int32_t num_segments, const recd_row_seg* segs, const int64_t* ctl,
+                        int32_t row_bytes, int64_t max_rows, recd_stream_t stream);
 
 /* Batched copy of num_segments (src, dst, bytes) device segments in one
  * launch (packing of exchange buffers).  host_staging / descs: a host and a

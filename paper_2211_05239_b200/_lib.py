@@ -53,10 +53,22 @@ _SIGS = {
     "recd_sparse_sgd_scratch_bytes": (_sz, [_i32, _p64]),
     "recd_sparse_sgd": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _f32, _i32,
                                _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_shard_count_scratch_bytes": (_sz, [_i32, _i32, _i64]),
+    "recd_shard_count": (_i32, [_i32, _i32, _i64, _pp, _pp, _vp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_shard_dispatch": (_i32, [_i32, _i32, _i64, _pp, _pp, _vp, _pp, _vp, _vp, _vp, _pp, _pp,
+                                   _vp]),
     "recd_shard_scratch_bytes": (_sz, [_i32, _i32, _i64]),
     "recd_shard_bucketize": (_i32, [_i32, _i32, _i64, _pp, _pp, _vp, _pp, _pp, _vp, _vp, _sz,
                                     _vp]),
     "recd_shard_combine": (_i32, [_i32, _i32, _i64, _i32, _i32, _pp, _pp, _vp, _pp, _vp]),
+    "recd_peer_ctl_words": (_i64, [_i32, _i32, _i32]),
+    "recd_peer_alloc": (_i32, [_sz, _pp]),
+    "recd_peer_free": (_i32, [_vp]),
+    "recd_peer_export": (_i32, [_vp, _vp]),
+    "recd_peer_import": (_i32, [_vp, _pp]),
+    "recd_peer_close": (_i32, [_vp]),
+    "recd_peer_exchange": (_i32, [_i32, _i32, _i32, _i32, _i32, _p32, _pp, _vp, _vp, _i64, _vp]),
+    "recd_peer_copy_rows": (_i32, [_i32, _vp, _vp, _i32, _i64, _vp]),
     "recd_batched_copy_desc_bytes": (_sz, [_i32]),
     "recd_batched_copy": (_i32, [_i32, _pp, _pp, _p64, _vp, _vp, _vp]),
     "recd_exclusive_scan_scratch_bytes": (_sz, [_i32, _p64]),

@@ -2,7 +2,8 @@
 
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/dist_sharded_check.py
 
-Each rank deduplicates its contiguous chunk of one global session-clustered
+TRANSPORT=peer runs PeerShardedStep (NVLink peer memory, one CUDA-graph
+replay), else ShardedTrainStep (NCCL).  Each rank deduplicates its contiguous chunk of one global session-clustered
 batch; every table is split into S = $SHARDS (default R) shards id % S, the
 (table, shard) pairs placed on ranks by the step's LPT placement.  Checked against the CPU
 oracle (oracle/), on the same inputs:
@@ -28,6 +29,7 @@ import oracle  # noqa: E402
 import paper_2211_05239_b200 as R  # noqa: E402
 from paper_2211_05239_b200.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
                                            generate_clustered_batch)
+from paper_2211_05239_b200.peer import PeerShardedStep  # noqa: E402
 from paper_2211_05239_b200.sharded import ShardedTrainStep  # noqa: E402
 
 
@@ -61,17 +63,24 @@ def main():
         return R.EmbeddingTable(k, n, D, w)
 
     caps = {k: mine.values[k].size for k in keys}
-    step = ShardedTrainStep(keys, B, caps, {k: rows for k in keys}, D, make_table, op, lr,
-                            shards=S, device=dev)
+    transport = os.environ.get("TRANSPORT", "nccl")
+    cls = PeerShardedStep if transport == "peer" else ShardedTrainStep
+    step = cls(keys, B, caps, {k: rows for k in keys}, D, make_table, op, lr, shards=S, device=dev)
     step.load_batch(mine.values, mine.offsets)
     grads = [np.random.default_rng(1000 * r + 7).standard_normal((B, D)).astype(np.float32)
              for r in range(world)]
     for g in step.grad_out:
         g.copy_(torch.from_numpy(grads[rank]))
-    step.run()
+    if transport == "peer":
+        step.capture(warmup=False)   # one step, through the CUDA graph
+        step.replay()
+        torch.cuda.synchronize()
+        step.check()
+    else:
+        step.run()
     torch.cuda.synchronize()
 
-    res = {"rank": rank, "world": world, "shards": S, "op": op, "ok": True,
+    res = {"rank": rank, "world": world, "shards": S, "transport": transport, "op": op, "ok": True,
            "pairs": step.mine}
     U, N = step.host_counts()
     # forward vs oracle on this rank's chunk

@@ -79,11 +79,13 @@ def test_exchange_plan_gloo_world2():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("op,shards", [("sum", 2), ("avg", 2), ("sum", 1), ("sum", 3)])
-def test_sharded_step_two_gpus(op, shards):
+@pytest.mark.parametrize("transport,op,shards", [
+    ("nccl", "sum", 2), ("nccl", "avg", 2), ("nccl", "sum", 1), ("nccl", "sum", 3),
+    ("peer", "sum", 2), ("peer", "avg", 2), ("peer", "sum", 1), ("peer", "sum", 3)])
+def test_sharded_step_two_gpus(transport, op, shards):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (gpurun --gpus 2)")
-    env = dict(os.environ, POOL_OP=op, SHARDS=str(shards))
+    env = dict(os.environ, POOL_OP=op, SHARDS=str(shards), TRANSPORT=transport)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node=2", "--master-addr=127.0.0.1",
                         f"--master-port={29600 + os.getpid() % 1000}",
