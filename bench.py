@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
                     help="N>1: exchange over NVLink peer memory (graph) or NCCL")
     ap.add_argument("--shards", type=int, default=0,
-                    help="N>1: row shards per table (0 = N, one per rank)")
+                    help="N>1: row shards per table (0 = auto: the fewest that fit HBM)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -464,12 +464,20 @@ def run_sharded(args, world, rank, local, dev):
 
     import paper_2211_05239_b200 as R
     from paper_2211_05239_b200.peer import PeerShardedStep
-    from paper_2211_05239_b200.sharded import ShardedTrainStep
+    from paper_2211_05239_b200.sharded import ShardedTrainStep, auto_shards
 
     t_setup = time.perf_counter()
     batch = make_batch(args, rank, world)
     keys = list(batch.keys)
-    S = args.shards or world
+    if args.shards:
+        S = args.shards
+    else:   # smallest S whose placement fits 60% of HBM (tables are fp32)
+        hbm = torch.cuda.get_device_properties(dev).total_memory
+        S = auto_shards([float(batch.values[k].size) for k in keys],
+                        [4 * args.rows * args.dim] * len(keys), world, 0.6 * hbm)
+        t = torch.tensor([S], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)   # identical on every rank
+        S = int(t.item())
 
     def make_table(k, j, n):
         return R.EmbeddingTable.create_on_device(f"{k}/shard{j}", n, args.dim,

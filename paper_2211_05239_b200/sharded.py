@@ -41,7 +41,8 @@ import torch.distributed as dist
 from . import _lib
 from .embedding import EmbeddingTable
 
-__all__ = ["ShardedTrainStep", "ExchangePlan", "plan_exchange", "shard_rows", "place_pairs"]
+__all__ = ["ShardedTrainStep", "ExchangePlan", "plan_exchange", "shard_rows", "place_pairs",
+           "auto_shards"]
 
 
 def shard_rows(rows: int, num_shards: int, shard: int) -> int:
@@ -61,6 +62,23 @@ def place_pairs(weights: Sequence[float], num_ranks: int) -> list[int]:
         place[p] = r
         load[r] += weights[p]
     return place
+
+
+def auto_shards(weights: Sequence[float], table_bytes: Sequence[int], num_ranks: int,
+                budget_bytes: float) -> int:
+    """Smallest S whose LPT placement keeps every rank's table shards within
+    budget_bytes.  Fewer shards = fewer partial rows per unique row (the
+    exchange and owner work grow with S), so S > 1 only when tables must be
+    split to fit HBM (or to balance a few very hot tables)."""
+    F = len(weights)
+    for S in range(1, num_ranks + 1):
+        place = place_pairs([weights[p // S] / S for p in range(F * S)], num_ranks)
+        load = [0.0] * num_ranks
+        for p, r in enumerate(place):
+            load[r] += table_bytes[p // S] / S
+        if max(load) <= budget_bytes:
+            return S
+    raise ValueError("tables do not fit the HBM budget even fully row-sharded")
 
 
 @dataclass

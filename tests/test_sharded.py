@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2211_05239_b200.sharded import place_pairs, plan_exchange, shard_rows
+from paper_2211_05239_b200.sharded import auto_shards, place_pairs, plan_exchange, shard_rows
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -35,6 +35,15 @@ def test_place_pairs_lpt():
     assert load == [12.0, 12.0]
     assert place_pairs([3.0, 1.0, 2.0], 1) == [0, 0, 0]
     assert place_pairs([5.0, 5.0], 4) == [0, 1]   # deterministic tie-break
+
+
+def test_auto_shards():
+    gb = 1 << 30
+    assert auto_shards([1.0] * 26, [5 * gb] * 26, 8, 100 * gb) == 1      # cfg2 tables fit whole
+    assert auto_shards([1.0] * 4, [60 * gb] * 4, 8, 100 * gb) == 1       # one table per rank
+    assert auto_shards([1.0] * 2, [300 * gb] * 2, 8, 100 * gb) == 3      # must split: 6 x 100 GB
+    with pytest.raises(ValueError):
+        auto_shards([1.0], [2000 * gb], 8, 100 * gb)
 
 
 def _worker(rank, world, port, q):
