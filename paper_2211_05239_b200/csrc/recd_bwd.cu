@@ -30,6 +30,11 @@
 #ifndef RECD_SCATTER_MINB
 #define RECD_SCATTER_MINB 3
 #endif
+// L2 policy of the scatter: 1 = table rows (read + write) evict_first,
+// 2 = also unique-row gradients evict_last, 0 = no hints
+#ifndef RECD_SCATTER_L2
+#define RECD_SCATTER_L2 1
+#endif
 
 namespace recd {
 
@@ -259,6 +264,9 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   uint32_t* rids = s_ids[warp];
   float* ring = &s_ring[warp][0][lane * V];
   const bool apply = p.apply_sgd != 0;
+  constexpr bool HINT = RECD_SCATTER_L2 > 0 && V == 4;
+  const uint64_t pol_stream = HINT ? l2_evict_first() : 0;
+  const uint64_t pol_keep = (HINT && RECD_SCATTER_L2 > 1) ? l2_evict_last() : 0;
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
     const int64_t chunk = (ncb == 1) ? w : w / ncb;
     const int lo_f = (int)(w - chunk * ncb) * C::CB + lane * V;  // this lane's first float
@@ -296,7 +304,12 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
     if (apply) {
 #pragma unroll
       for (int r = 0; r < SC_RS; ++r) {
-        if (r < nruns && ok) cp_async<V * 4>(ring + r * C::CB, table + (uint64_t)rids[r] * D32);
+        if (r < nruns && ok) {
+          if constexpr (HINT)
+            cp_async16_hint(ring + r * C::CB, table + (uint64_t)rids[r] * D32, pol_stream);
+          else
+            cp_async<V * 4>(ring + r * C::CB, table + (uint64_t)rids[r] * D32);
+        }
         cp_async_commit();
       }
     }
@@ -314,8 +327,19 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const uint32_t vv = vwin.get(k0 + t);
-        if (k0 + t < pend)
-          C::ld(p.grow[vv >> 24] + (uint64_t)(vv & 0xffffffu) * D32 + lo_f, ok, x[t]);
+        if (k0 + t < pend) {
+          const float* gp = p.grow[vv >> 24] + (uint64_t)(vv & 0xffffffu) * D32 + lo_f;
+          if constexpr (HINT && RECD_SCATTER_L2 > 1) {
+            if (C::FULL || ok) {
+              const float4 g4 = ld_v4_hint(gp, pol_keep);
+              x[t][0] = g4.x; x[t][1] = g4.y; x[t][2] = g4.z; x[t][3] = g4.w;
+            } else {
+              C::zero(x[t]);
+            }
+          } else {
+            C::ld(gp, ok, x[t]);
+          }
+        }
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
@@ -330,9 +354,16 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
               float wv[V];
 #pragma unroll
               for (int e = 0; e < V; ++e) wv[e] = __fsub_rn(slot[e], __fmul_rn(p.lr, acc[e]));
-              C::st(table + (uint64_t)id * D32, ok, wv);
-              if (r + SC_RS < nruns && ok)
-                cp_async<V * 4>(slot, table + (uint64_t)rids[r + SC_RS] * D32);
+              if constexpr (HINT) {
+                if (C::FULL || ok)
+                  st_v4_hint(table + (uint64_t)id * D32, wv[0], wv[1], wv[2], wv[3], pol_stream);
+                if (r + SC_RS < nruns && ok)
+                  cp_async16_hint(slot, table + (uint64_t)rids[r + SC_RS] * D32, pol_stream);
+              } else {
+                C::st(table + (uint64_t)id * D32, ok, wv);
+                if (r + SC_RS < nruns && ok)
+                  cp_async<V * 4>(slot, table + (uint64_t)rids[r + SC_RS] * D32);
+              }
               cp_async_commit();
             } else {
               const int64_t ri = run_base + r;

@@ -16,6 +16,16 @@
 #ifndef RECD_POOL_MINB
 #define RECD_POOL_MINB 2
 #endif
+// ring variant (sum / avg): K rows in flight per warp through shared memory
+#ifndef RECD_POOL_RING
+#define RECD_POOL_RING 1
+#endif
+#ifndef RECD_RING_K
+#define RECD_RING_K 2
+#endif
+#ifndef RECD_RING_MINB
+#define RECD_RING_MINB 3
+#endif
 
 
 namespace recd {
@@ -140,6 +150,298 @@ __global__ void __launch_bounds__(256, 3) k_pool_dense(const float* A, int64_t n
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ring variant of k_pool_fwd (sum / avg, float4 lanes).  The table rows of a
+// jagged row are streamed in position order through a per-warp shared-memory
+// ring of K slots with cp.async (16 bytes per lane, one 512-byte row slice per
+// warp instruction): rows in flight hold no registers, so a warp keeps K rows
+// in flight at ~80 registers instead of 8 at 128.  numpy's pairwise tree
+// visits the values strictly left to right, so the reduction consumes the
+// ring in order and stays bit-identical to pool_row / leaf_sum.
+// ---------------------------------------------------------------------------
+// Values 1.. of a row (value 0 is loaded directly) stream through the ring in
+// batches of 8 positions.  numpy's pairwise split points h are multiples of 8,
+// so relative to value 1 every leaf of the tree starts on a batch boundary and
+// only the row's last batch can be partial: the reduction consumes whole
+// batches (one wait + one refill per 8 rows, a handful of code sites).
+template <int NB>
+struct RingRows {
+  float* ring;              // this lane's 16 bytes of slot 0 (slot stride 128 floats)
+  const float* Wl;
+  const int64_t* ids;       // IDs of positions 0.. of the streamed values
+  int32_t n;                // streamed values
+  int64_t rows;
+  uint32_t D;
+  int64_t* err;
+  int64_t errpos;           // (feature << 40) | absolute position of streamed value 0
+  int lane;
+  bool ok;
+  int32_t wb;               // IDs of positions [wb, wb + 32) in cur, the next 32 in nxt
+  uint32_t cur, nxt;
+  int32_t b;                // batches consumed
+
+  __device__ __forceinline__ uint32_t load_id(int32_t q) {
+    uint32_t v = 0;
+    if (q < n) {
+      const int64_t id = __ldg(ids + q);
+      if ((uint64_t)id < (uint64_t)rows) {
+        v = (uint32_t)id;
+      } else {
+        atomicMin(reinterpret_cast<unsigned long long*>(err), (unsigned long long)(errpos + q));
+      }
+    }
+    return v;
+  }
+  // positions [8 bi, 8 bi + 8) -> slots of batch bi % NB, one commit group
+  __device__ __forceinline__ void issue(int32_t bi) {
+    const int32_t p0 = bi * 8;
+    if (p0 < n) {  // warp-uniform
+      if (p0 >= wb + 32) {
+        wb += 32;
+        cur = nxt;
+        nxt = load_id(wb + 32 + lane);
+      }
+      float* dst = ring + (bi % NB) * (8 * 128);
+      const int sh = p0 - wb;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t id = __shfl_sync(0xffffffffu, cur, sh + k);
+        if (ok && p0 + k < n) cp_async<16>(dst + k * 128, Wl + (uint64_t)id * D);
+      }
+    }
+    cp_async_commit();
+  }
+  __device__ __forceinline__ void start() {
+    wb = 0;
+    cur = load_id(lane);
+    nxt = load_id(32 + lane);
+    b = 0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) issue(i);
+  }
+  // slots of the next batch (after its copies landed)
+  __device__ __forceinline__ const float* acquire() {
+    cp_async_wait<NB - 1>();
+    return ring + (b % NB) * (8 * 128);
+  }
+  // the batch's values are consumed: reuse its slots for batch b + NB
+  __device__ __forceinline__ void release() {
+    issue(b + NB);
+    ++b;
+  }
+};
+
+__device__ __forceinline__ float4 slot4(const float* s, int k, bool ok) {
+  return ok ? *reinterpret_cast<const float4*>(s + k * 128) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// P(x) over the next m streamed values, m <= 128, starting on a batch boundary
+// (same arithmetic as leaf_sum)
+template <int NB>
+__device__ __forceinline__ void leaf_ring(RingRows<NB>& rr, int32_t m, float (&s)[4]) {
+  if (m < 8) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[e] = -0.0f;
+    const float* sl = rr.acquire();
+    for (int t = 0; t < m; ++t) {
+      const float4 v = slot4(sl, t, rr.ok);
+      s[0] = __fadd_rn(s[0], v.x);
+      s[1] = __fadd_rn(s[1], v.y);
+      s[2] = __fadd_rn(s[2], v.z);
+      s[3] = __fadd_rn(s[3], v.w);
+    }
+    rr.release();
+    return;
+  }
+  float r[8][4];
+  {
+    const float* sl = rr.acquire();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = slot4(sl, k, rr.ok);
+      r[k][0] = v.x;
+      r[k][1] = v.y;
+      r[k][2] = v.z;
+      r[k][3] = v.w;
+    }
+    rr.release();
+  }
+  const int32_t nb = m >> 3;
+  for (int32_t i = 1; i < nb; ++i) {
+    const float* sl = rr.acquire();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = slot4(sl, k, rr.ok);
+      r[k][0] = __fadd_rn(r[k][0], v.x);
+      r[k][1] = __fadd_rn(r[k][1], v.y);
+      r[k][2] = __fadd_rn(r[k][2], v.z);
+      r[k][3] = __fadd_rn(r[k][3], v.w);
+    }
+    rr.release();
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    s[e] = __fadd_rn(__fadd_rn(__fadd_rn(r[0][e], r[1][e]), __fadd_rn(r[2][e], r[3][e])),
+                     __fadd_rn(__fadd_rn(r[4][e], r[5][e]), __fadd_rn(r[6][e], r[7][e])));
+  const int tail = m & 7;
+  if (tail) {
+    const float* sl = rr.acquire();
+    for (int t = 0; t < tail; ++t) {
+      const float4 v = slot4(sl, t, rr.ok);
+      s[0] = __fadd_rn(s[0], v.x);
+      s[1] = __fadd_rn(s[1], v.y);
+      s[2] = __fadd_rn(s[2], v.z);
+      s[3] = __fadd_rn(s[3], v.w);
+    }
+    rr.release();
+  }
+}
+
+// P over any m (pairwise_big's post-order DFS; positions implicit, every leaf
+// starts on a batch boundary because every split point is a multiple of 8)
+template <int NB>
+__device__ __forceinline__ void pairwise_ring(RingRows<NB>& rr, int32_t m, float (&out)[4]) {
+  if (m <= 128) {
+    leaf_ring<NB>(rr, m, out);
+    return;
+  }
+  constexpr int DEPTH = 32;
+  int32_t fm[DEPTH];
+  int fs[DEPTH];
+  float vals[DEPTH][4];
+  int top = 1, vtop = 0;
+  fm[0] = m;
+  fs[0] = 0;
+  while (top > 0) {
+    const int t = top - 1;
+    if (fm[t] <= 128) {
+      float sv[4];
+      leaf_ring<NB>(rr, fm[t], sv);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) vals[vtop][e] = sv[e];
+      ++vtop;
+      --top;
+      continue;
+    }
+    int32_t h = fm[t] / 2;
+    h -= h % 8;
+    if (fs[t] == 0) {
+      fs[t] = 1;
+      fm[top] = h;
+      fs[top] = 0;
+      ++top;
+    } else if (fs[t] == 1) {
+      fs[t] = 2;
+      fm[top] = fm[t] - h;
+      fs[top] = 0;
+      ++top;
+    } else {
+      --vtop;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) vals[vtop - 1][e] = __fadd_rn(vals[vtop - 1][e], vals[vtop][e]);
+      --top;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) out[e] = vals[0][e];
+}
+
+template <class C, int K>
+__global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_constant__ PoolParams p) {
+  static_assert(C::VW == 4, "ring pool streams float4 lane slices");
+  extern __shared__ __align__(16) float s_ring[];
+  __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
+  const int ncb = col_blocks<C>(p.D);
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int f = 0; f < p.F; ++f) {
+      s_pref[f] = acc;
+      acc += p.counts[f] * ncb;
+    }
+    s_pref[p.F] = acc;
+  }
+  __syncthreads();
+  const int64_t total = s_pref[p.F];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  float* ring = s_ring + (int64_t)warp * K * 8 * 128 + lane * 4;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
+    const int f = find_seg(s_pref, p.F, w);
+    const ColWork cw = col_work<C>(w - s_pref[f], p.D, lane);
+    const int64_t u = cw.row;
+    const int64_t U = p.counts[f], N = p.counts[p.Ftot + f];
+    const int64_t* uo = p.uoffsets[f];
+    const int64_t a = uo[u];
+    const int64_t e = (u + 1 < U) ? uo[u + 1] : N;
+    const int64_t n = e - a;
+    float acc[4];
+    if (n <= 0) {
+      C::zero(acc);
+    } else {
+      // value 0 straight into registers, values 1.. through the ring
+      const int64_t id0 = __ldg(p.uvalues[f] + a);
+      uint64_t r0 = 0;
+      if ((uint64_t)id0 < (uint64_t)p.table_rows[f]) {
+        r0 = (uint64_t)id0;
+      } else if (lane == 0) {
+        atomicMin(reinterpret_cast<unsigned long long*>(p.err),
+                  (unsigned long long)(((int64_t)(p.f0 + f) << 40) + a));
+      }
+      if (n > 1) {
+        RingRows<K> rr;
+        rr.ring = ring;
+        rr.Wl = p.tables[f] + cw.lo;
+        rr.ids = p.uvalues[f] + a + 1;
+        rr.n = (int32_t)(n - 1);
+        rr.rows = p.table_rows[f];
+        rr.D = (uint32_t)p.D;
+        rr.err = p.err;
+        rr.errpos = ((int64_t)(p.f0 + f) << 40) + a + 1;
+        rr.lane = lane;
+        rr.ok = C::FULL || cw.ok;
+        rr.start();
+        C::ld(p.tables[f] + cw.lo + r0 * (uint32_t)p.D, cw.ok, acc);
+        float sv[4];
+        pairwise_ring<K>(rr, (int32_t)(n - 1), sv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], sv[k]);
+      } else {
+        C::ld(p.tables[f] + cw.lo + r0 * (uint32_t)p.D, cw.ok, acc);
+      }
+      if (p.mode == RECD_POOL_AVG) {
+        const float fl = (float)n;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = __fdiv_rn(acc[k], fl);
+      }
+    }
+    C::st(p.pooled[f] + u * p.D + cw.lo, cw.ok, acc);
+  }
+  cp_async_wait<0>();
+}
+
+// k_pool_ring for sum / avg with float4 lanes, k_pool_fwd otherwise
+template <class C>
+static int launch_pool_fwd(const PoolParams& p, int mode, unsigned grid, cudaStream_t stream) {
+  if constexpr (C::VW == 4 && RECD_POOL_RING) {
+    if (mode != RECD_POOL_MAX) {
+      constexpr int K = RECD_RING_K;  // batches of 8 rows in flight per warp
+      constexpr int smem = 8 * K * 8 * 128 * (int)sizeof(float);
+      static bool attr[64] = {};
+      int dev = 0;
+      RECD_CUDA_CHECK(cudaGetDevice(&dev));
+      if (dev < 0 || dev >= 64 || !attr[dev]) {
+        RECD_CUDA_CHECK(cudaFuncSetAttribute(k_pool_ring<C, K>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        if (dev >= 0 && dev < 64) attr[dev] = true;
+      }
+      k_pool_ring<C, K><<<grid, 256, smem, stream>>>(p);
+      return RECD_OK;
+    }
+  }
+  k_pool_fwd<C><<<grid, 256, 0, stream>>>(p);
+  return RECD_OK;
+}
+
 static unsigned grid_for(int64_t warps) {
   int64_t blocks = ceil_div(std::max<int64_t>(warps, 1), 8);
   const int64_t cap = (int64_t)num_sms() * 16;
@@ -189,7 +491,8 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
     int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, 1, {
       const unsigned grid = grid_for(batch_size * p.F * col_blocks<C>(dim));
       hook_before("k_pool_fwd", stream);
-      k_pool_fwd<C><<<grid, 256, 0, stream>>>(p);
+      const int lrc = launch_pool_fwd<C>(p, mode, grid, stream);
+      if (lrc != RECD_OK) return lrc;
       hook_after("k_pool_fwd", stream);
       note_launch();
       if (any_expand) {
