@@ -18,9 +18,18 @@
 namespace recd {
 
 constexpr int SORT_NT = 256;
-constexpr int SORT_ITEMS = 8;
+#ifndef RECD_SORT_ITEMS
+#define RECD_SORT_ITEMS 8
+#endif
+constexpr int SORT_ITEMS = RECD_SORT_ITEMS;
 constexpr int SORT_TILE = SORT_NT * SORT_ITEMS;  // 2048
-constexpr int SORT_CHUNK = SORT_TILE * 8;        // 16384
+#ifndef RECD_SORT_CHUNK_TILES
+#define RECD_SORT_CHUNK_TILES 8
+#endif
+#ifndef RECD_SORT_UP_ATOMIC
+#define RECD_SORT_UP_ATOMIC 1
+#endif
+constexpr int SORT_CHUNK = SORT_TILE * RECD_SORT_CHUNK_TILES;  // elements per block
 constexpr int SORT_MAXSEG = 64;
 
 struct SortSegDev {
@@ -62,12 +71,38 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_up(const __grid_constant__ Sor
   const int64_t lo = c * SORT_CHUNK;
   if (lo >= n) return;
   const int64_t hi = min(n, lo + (int64_t)SORT_CHUNK);
-  __shared__ uint32_t sh[256];
-  sh[threadIdx.x] = 0;
-  __syncthreads();
   const uint32_t mask = (1u << p.nbits) - 1u;
   const uint32_t* k = p.kin + sg.base;
   constexpr int U = 8;  // loads in flight per thread
+#if RECD_SORT_UP_ATOMIC
+  // per-warp sub-histograms, plain shared atomics (digits of random keys rarely collide)
+  __shared__ uint32_t shw[SORT_NT / 32][256];
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int w = 0; w < SORT_NT / 32; ++w) shw[w][threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t j0 = lo; j0 < hi; j0 += SORT_NT * U) {
+    uint32_t kk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * SORT_NT + threadIdx.x;
+      kk[u] = j < hi ? __ldg(k + j) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u * SORT_NT + threadIdx.x;
+      if (j < hi) atomicAdd(&shw[warp][(kk[u] >> p.shift) & mask], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < SORT_NT / 32; ++w) tot += shw[w][threadIdx.x];
+  p.hist[sg.hbase + (int64_t)threadIdx.x * sg.nchunks + c] = tot;
+#else
+  __shared__ uint32_t sh[256];
+  sh[threadIdx.x] = 0;
+  __syncthreads();
   for (int64_t j0 = lo; j0 < hi; j0 += SORT_NT * U) {
     uint32_t kk[U];
 #pragma unroll
@@ -86,6 +121,7 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_up(const __grid_constant__ Sor
   }
   __syncthreads();
   p.hist[sg.hbase + (int64_t)threadIdx.x * sg.nchunks + c] = sh[threadIdx.x];
+#endif
 }
 
 constexpr int SCAN_NT = 1024;
