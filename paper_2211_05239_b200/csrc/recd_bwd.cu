@@ -30,8 +30,7 @@
 #ifndef RECD_SCATTER_MINB
 #define RECD_SCATTER_MINB 3
 #endif
-// L2 policy of the scatter: 1 = table rows (read + write) evict_first,
-// 2 = also unique-row gradients evict_last, 0 = no hints
+// L2 policy of the scatter: 1 = table rows (read + write) evict_first, 0 = no hints
 #ifndef RECD_SCATTER_L2
 #define RECD_SCATTER_L2 1
 #endif
@@ -77,6 +76,7 @@ struct BwdParams {
   int32_t* csr_start;     // [nis][B + 1]
   float* gout[RECD_MAX_FEAT];         // grad_u destination per feature ([U x D])
   const float* grow[RECD_MAX_FEAT];   // unique-row gradients read by the scatter
+  const float* seg_grow[RECD_MAX_FEAT];  // per table segment: grow of its only feature, or null
   uint32_t* occ_keys;     // sorted occurrence IDs
   uint32_t* occ_vals;     // tag = (f << 24) | u
   int64_t* run_part;      // [total_rc_chunks] exclusive run counts (grad-output mode)
@@ -249,12 +249,13 @@ constexpr int SC_RS = 8;  // table rows prefetched ahead per warp (shared-memory
 // per-warp shared ring while grad_u rows (L2-resident) are gathered 8 positions
 // at a time across run boundaries; at each run end the row is updated and
 // stored, and its slot refilled with the row of run r + SC_RS.
-template <class C>
+template <class C, bool SINGLE>
 __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid_constant__ BwdParams p) {
   constexpr int V = C::VW;
   __shared__ uint16_t s_starts[8][RC + 2];
   __shared__ uint32_t s_ids[8][RC];
   __shared__ __align__(16) float s_ring[8][SC_RS][C::CB];
+  __shared__ uint32_t s_win[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   const int ncb = col_blocks<C>(p.D);
@@ -266,7 +267,6 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   const bool apply = p.apply_sgd != 0;
   constexpr bool HINT = RECD_SCATTER_L2 > 0 && V == 4;
   const uint64_t pol_stream = HINT ? l2_evict_first() : 0;
-  const uint64_t pol_keep = (HINT && RECD_SCATTER_L2 > 1) ? l2_evict_last() : 0;
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
     const int64_t chunk = (ncb == 1) ? w : w / ncb;
     const int lo_f = (int)(w - chunk * ncb) * C::CB + lane * V;  // this lane's first float
@@ -314,36 +314,39 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
       }
     }
     const int64_t run_base = apply ? 0 : p.run_part[chunk];
-    // 3. flat pass over the positions of the chunk's runs
-    U32Win vwin{Vv, pend, lane, 0, 0};
-    vwin.window(lo + starts[0]);
+    // 3. flat pass over the positions of the chunk's runs, offsets from lo
+    //    (32-bit); the occurrence tags of 32 positions at a time sit in shared
+    //    memory (broadcast reads); SINGLE: one feature per table segment, so the
+    //    gradient base is uniform
+    const int32_t pe = (int32_t)(pend - lo);
+    const uint32_t* __restrict__ Vl = Vv + lo;
+    const float* gs = SINGLE ? p.seg_grow[s] + lo_f : nullptr;
+    uint32_t* win = s_win[warp];
+    int32_t wbase = starts[0];
+    win[lane] = (wbase + lane < pe) ? __ldg(Vl + wbase + lane) : 0u;
+    __syncwarp();
     int r = 0;
-    int64_t bnd = (nruns > 1) ? lo + starts[1] : pend;  // end of run r
+    int32_t bnd = (nruns > 1) ? (int32_t)starts[1] : pe;  // end of run r
     float acc[V];
     C::zero(acc);
     float x[8][V];
-    for (int64_t k0 = lo + starts[0]; k0 < pend; k0 += 8) {
-      vwin.need(k0, 8);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const uint32_t vv = vwin.get(k0 + t);
-        if (k0 + t < pend) {
-          const float* gp = p.grow[vv >> 24] + (uint64_t)(vv & 0xffffffu) * D32 + lo_f;
-          if constexpr (HINT && RECD_SCATTER_L2 > 1) {
-            if (C::FULL || ok) {
-              const float4 g4 = ld_v4_hint(gp, pol_keep);
-              x[t][0] = g4.x; x[t][1] = g4.y; x[t][2] = g4.z; x[t][3] = g4.w;
-            } else {
-              C::zero(x[t]);
-            }
-          } else {
-            C::ld(gp, ok, x[t]);
-          }
-        }
+    for (int32_t k0 = starts[0]; k0 < pe; k0 += 8) {
+      if (k0 + 8 > wbase + 32) {
+        __syncwarp();
+        wbase = k0;
+        win[lane] = (k0 + lane < pe) ? __ldg(Vl + k0 + lane) : 0u;
+        __syncwarp();
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        if (k0 + t < pend) {
+        const uint32_t vv = win[k0 + t - wbase];
+        const float* gp = SINGLE ? gs + (uint64_t)(vv & 0xffffffu) * D32
+                                 : p.grow[vv >> 24] + lo_f + (uint64_t)(vv & 0xffffffu) * D32;
+        if (k0 + t < pe) C::ld(gp, ok, x[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (k0 + t < pe) {
 #pragma unroll
           for (int e = 0; e < V; ++e) acc[e] = __fadd_rn(acc[e], x[t][e]);
           if (k0 + t + 1 == bnd) {  // run r complete (warp-uniform)
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
             }
             ++r;
             C::zero(acc);
-            bnd = (r + 1 < nruns) ? lo + starts[r + 1] : pend;
+            bnd = (r + 1 < nruns) ? (int32_t)starts[r + 1] : pe;
           }
         }
       }
@@ -578,7 +581,12 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   for (int s = 0; s < pl.nts; ++s) first_feat_of_ts[s] = -1;
   for (int f = 0; f < F; ++f)
     if (first_feat_of_ts[pl.feat_ts[f]] < 0) first_feat_of_ts[pl.feat_ts[f]] = f;
+  int feats_of_ts[RECD_MAX_FEAT] = {0};
+  for (int f = 0; f < F; ++f) ++feats_of_ts[pl.feat_ts[f]];
+  bool single = true;
   for (int s = 0; s < pl.nts; ++s) {
+    p.seg_grow[s] = feats_of_ts[s] == 1 ? p.grow[first_feat_of_ts[s]] : nullptr;
+    single &= feats_of_ts[s] == 1;
     p.table[s] = pl.table[s];
     p.ts_base[s] = pl.ts_base[s];
     p.ts_chunk0[s] = pl.ts_chunk0[s];
@@ -656,7 +664,10 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       const unsigned g2 =
           (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks * ncb, 8), (int64_t)num_sms() * 16);
       hook_before("k_scatter", stream);
-      k_scatter<C><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+      if (single)
+        k_scatter<C, true><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+      else
+        k_scatter<C, false><<<std::max(g2, 1u), 256, 0, stream>>>(p);
       hook_after("k_scatter", stream);
       note_launch();
     }
