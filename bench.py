@@ -36,9 +36,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "samples/sec for IKJT dedup + embedding fwd/bwd; achieved HBM GB/s vs peak"
 
-# DRAM bytes (read + write) per launch from one ncu capture of the cfg2 bench
-# (profiles/r1_ncu_dram_cfg2.txt); None until measured for the current build.
-TRAFFIC: dict = {"k_scatter": 10.800e9, "k_pool_fwd": 4.914e9}
+# DRAM bytes (read + write) per launch from one `ncu --set full` capture of the
+# cfg2 bench (profiles/r1_ncu_summary.txt); refreshed when the kernels change.
+TRAFFIC: dict = {"k_scatter": 9.939e9, "k_pool_fwd": 4.899e9}
 LENS = ([8, 16, 32, 64, 128, 256] * 5)[:26]
 
 
@@ -64,7 +64,10 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=2048, help="rows in the CPU sample")
+    ap.add_argument("--cpu-rows", type=int, default=0,
+                    help="rows in the CPU sample (0 = calibrated to --cpu-seconds)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU work of the bounded baseline sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
     return ap.parse_args()
 
@@ -160,7 +163,9 @@ def cpu_time(batch, rows, dim, lr, procs):
         _CPU["offsets"][k] = o
     _CPU["grad"] = rng.standard_normal((rows, dim)).astype(np.float32)
     vocab = int(max(v.max() for v in _CPU["values"].values())) + 1
-    _CPU["table"] = rng.uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32)
+    tab = _CPU.get("table")
+    if tab is None or tab.shape[0] < vocab or tab.shape[1] != dim:   # built once, reused
+        _CPU["table"] = rng.uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32)
     _CPU["lr"] = lr
     keys = list(batch.keys)
     t0 = time.perf_counter()
@@ -171,6 +176,13 @@ def cpu_time(batch, rows, dim, lr, procs):
         with mp.get_context("fork").Pool(procs) as pool:
             pool.map(_cpu_key_work, keys, chunksize=1)
     return time.perf_counter() - t0
+
+
+def calibrated_rows(batch, dim, lr, procs, target_s):
+    """Rows of the CPU sample that take about target_s seconds (rate probed on
+    256 rows, which also builds the shared table)."""
+    t = cpu_time(batch, 256, dim, lr, procs)
+    return int(max(256, min(batch.batch_size, 256 * target_s / max(t, 1e-3))))
 
 
 def host_cores():
@@ -186,7 +198,9 @@ def run_reference(args):
         return 0
     batch = make_batch(args, 0, 1)
     procs = min(host_cores(), args.keys)
-    rows = args.cpu_rows
+    # each step a bounded sample: ~cpu_seconds, capped so K + W steps fit ~3 minutes
+    per_step = min(args.cpu_seconds, 180.0 / (max(1, args.steps) + max(0, args.warmup)))
+    rows = args.cpu_rows or calibrated_rows(batch, args.dim, args.lr, procs, per_step)
     for _ in range(max(0, min(args.warmup, 1))):
         cpu_time(batch, min(rows, 256), args.dim, args.lr, procs)
     times = [cpu_time(batch, rows, args.dim, args.lr, procs) for _ in range(max(1, args.steps))]
@@ -390,7 +404,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
         procs = min(host_cores(), K)
-        rows = args.cpu_rows
+        rows = args.cpu_rows or calibrated_rows(batch, D, args.lr, procs, args.cpu_seconds)
         t = cpu_time(batch, rows, D, args.lr, procs)
         cpu = {"value": rows / t, "unit": "samples/s", "cores": procs, "kind": "port",
                "sample": f"first {rows} of {B} rows x {K} keys, one shared table, oracle/ "
