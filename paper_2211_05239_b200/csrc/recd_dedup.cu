@@ -8,12 +8,12 @@
 //
 // Pipeline (one launch per phase for all groups of the step):
 //   k_rowscan  (group, 256-row chunk) blocks stream the KJT values once
-//              (8 consecutive values per thread, 128-bit loads):
-//              head[i] = row i differs from row i-1 (session-clustered batches
-//              make ~80% of rows non-heads), row hash for every row; the block
-//              also clears its slice of the group's hash table.
-//   k_insert   heads only: open-addressing table (64-bit key, L2 resident),
-//              rep = atomicMin(row) per key  -> deterministic min row.
+//              (8 consecutive values per thread, 128-bit loads) and compare
+//              each row with its predecessor: head[i] = row i differs from row
+//              i-1 (session-clustered batches make ~80% of rows non-heads); the
+//              block also clears its slice of the group's hash table.
+//   k_insert   heads only: warp-cooperative 64-bit row hash, open-addressing
+//              table (64-bit key, L2 resident), rep = atomicMin(row) per key.
 //   k_resolve  heads whose rep != self are fully compared with the rep; a
 //              mismatch (a true 64-bit collision) is marked pending.
 //   k_fallback (cold) exact sequential resolution of pending heads.
@@ -54,6 +54,7 @@ struct DedupParams {
   unsigned long long* tkeys;  // [G][C]
   uint32_t* treps;            // [G][C]
   int32_t* collide;           // [G]
+  int rs_group[RECD_MAX_FEAT];  // k_rowscan: groups in launch order (most values first)
 };
 
 __device__ __forceinline__ int64_t row_begin(const int64_t* off, int64_t i) { return off[i]; }
@@ -80,12 +81,17 @@ __device__ __forceinline__ uint64_t finalize_hash(uint64_t h, uint64_t mask) {
 }
 
 // ---------------------------------------------------------------- rowscan
+// Compare-only pass over the KJT values: block per (group, 256-row chunk),
+// 8 consecutive values per thread (128-bit loads), each compared with the
+// same position of the previous row (q - len; an L1 hit for rows shorter
+// than a tile).  Only run heads need a content hash, and they are ~20% of the
+// rows of a session-clustered batch, so hashing is deferred to k_insert.
 constexpr int RS_NT = 256;
 constexpr int RS_RPB = 256;
 constexpr int RS_IT = 8;  // consecutive values per thread
 
 __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ DedupParams p) {
-  const int g = blockIdx.y;
+  const int g = p.rs_group[blockIdx.y];
   const int tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * RS_RPB;
   if (r0 >= p.B) return;
@@ -95,7 +101,6 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
   __shared__ int64_t s_start[RS_RPB + 1];
   __shared__ int32_t s_len[RS_RPB];
   __shared__ uint32_t s_mism[RS_RPB];
-  __shared__ unsigned long long s_hash[RS_RPB];
 
   {  // clear this block's slice of the group's hash table
     const int64_t lo = r0 * p.C / p.B, hi = r1 * p.C / p.B;
@@ -106,15 +111,11 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
       tr[s] = 0xffffffffu;
     }
   }
-  for (int j = tid; j < n; j += RS_NT) {
-    s_mism[j] = (r0 + j == 0) ? 1u : 0u;
-    s_hash[j] = 0ull;
-  }
+  for (int j = tid; j < n; j += RS_NT) s_mism[j] = (r0 + j == 0) ? 1u : 0u;
   __syncthreads();
 
   const int fbeg = p.group_first[g], fend = p.group_first[g + 1];
   for (int f = fbeg; f < fend; ++f) {
-    const int fi = f - fbeg;
     const int64_t* off = p.offsets[f];
     const int64_t* val = p.values[f];
     const int64_t nv = p.nvalues[f];
@@ -128,21 +129,17 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
       const int64_t len = s_start[j + 1] - s_start[j];
       const int64_t plen = (i > 0) ? (s_start[j] - (j > 0 ? s_start[j - 1] : off[i - 1])) : -1;
       if (plen != len) s_mism[j] = 1u;
-      s_len[j] = (int32_t)len;
-      s_hash[j] += len_hash(len, fi);
+      s_len[j] = (int32_t)min(len, (int64_t)INT32_MAX);
     }
     __syncthreads();
-    // Each thread scans RS_IT consecutive values (one binary search, then a
-    // forward walk over the rows), compares them with the same positions of
-    // the previous row and accumulates the row hash locally; only row changes
-    // touch shared memory.
     const int64_t vbeg = s_start[0], vend = s_start[n];
     const int64_t tb0 = vbeg & ~(int64_t)(RS_IT - 1);  // 64-byte aligned tiles
+    const bool a16 = (reinterpret_cast<uintptr_t>(val) & 15) == 0;
     for (int64_t tb = tb0; tb < vend; tb += (int64_t)RS_NT * RS_IT) {
       const int64_t q0 = tb + (int64_t)tid * RS_IT;
       if (q0 >= vend || q0 + RS_IT <= vbeg) continue;
       int64_t v[RS_IT];
-      if (q0 + RS_IT <= nv && (reinterpret_cast<uintptr_t>(val) & 15) == 0) {
+      if (q0 + RS_IT <= nv && a16) {
         const longlong2* src = reinterpret_cast<const longlong2*>(val + q0);
 #pragma unroll
         for (int k = 0; k < RS_IT / 2; ++k) {
@@ -160,54 +157,94 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
         const int mid = (lo + hi + 1) >> 1;
         if (s_start[mid] <= qs) lo = mid; else hi = mid - 1;
       }
+      // row of every value, then all predecessor loads, then the compares
+      int jk[RS_IT];
       int j = lo;
       int64_t jend = s_start[j + 1];
-      uint64_t h = 0;
 #pragma unroll
       for (int k = 0; k < RS_IT; ++k) {
         const int64_t q = q0 + k;
-        if (q < vbeg || q >= vend) continue;
-        if (q >= jend) {
-          if (h) atomicAdd(&s_hash[j], (unsigned long long)h);
-          h = 0;
-          do { ++j; jend = s_start[j + 1]; } while (q >= jend);
+        jk[k] = -1;
+        if (q >= vbeg && q < vend) {
+          while (q >= jend) jend = s_start[++j + 1];
+          jk[k] = j;
         }
-        const int64_t st = s_start[j];
-        if (s_mism[j] == 0u && __ldg(val + q - s_len[j]) != v[k]) s_mism[j] = 1u;
-        h += elem_hash(v[k], q - st, fi);
       }
-      if (h) atomicAdd(&s_hash[j], (unsigned long long)h);
+      int64_t pv[RS_IT];
+#pragma unroll
+      for (int k = 0; k < RS_IT; ++k)
+        pv[k] = (jk[k] >= 0) ? __ldg(val + max(q0 + k - (int64_t)s_len[jk[k]], (int64_t)0)) : 0;
+#pragma unroll
+      for (int k = 0; k < RS_IT; ++k)
+        if (jk[k] >= 0 && pv[k] != v[k]) s_mism[jk[k]] = 1u;
     }
     __syncthreads();
   }
   uint8_t* head = p.head + (int64_t)g * p.B;
-  uint64_t* hash = p.hash + (int64_t)g * p.B;
-  for (int j = tid; j < n; j += RS_NT) {
-    head[r0 + j] = s_mism[j] ? 1 : 0;
-    hash[r0 + j] = finalize_hash(s_hash[j], p.hash_mask);
-  }
+  for (int j = tid; j < n; j += RS_NT) head[r0 + j] = s_mism[j] ? 1 : 0;
 }
 
 // ----------------------------------------------------------------- insert
+// Warp per 32 rows of a group: the run heads among them are hashed one at a
+// time by the whole warp (lane-strided, coalesced), then every head lane
+// inserts its hash: open addressing, rep = atomicMin(row) per key.
 __global__ void __launch_bounds__(256) k_insert(const __grid_constant__ DedupParams p) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)p.G * p.B) return;
-  const int g = (int)(idx / p.B);
-  if (!p.head[idx]) return;
-  const int64_t i = idx - (int64_t)g * p.B;
-  const unsigned long long h = p.hash[idx];
+  const int64_t wpg = ceil_div(p.B, 32);
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= (int64_t)p.G * wpg) return;
+  const int lane = threadIdx.x & 31;
+  const int g = (int)(w / wpg);
+  const int64_t i = (w - (int64_t)g * wpg) * 32 + lane;
+  const int64_t idx = (int64_t)g * p.B + i;
+  const bool is_head = i < p.B && p.head[idx];
+  unsigned m = __ballot_sync(0xffffffffu, is_head);
+  if (!m) return;
+  const int fbeg = p.group_first[g], fend = p.group_first[g + 1];
+  uint64_t mine = 0;
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const int64_t row = i - lane + src;
+    uint64_t h = 0;
+    for (int f = fbeg; f < fend; ++f) {
+      const int fi = f - fbeg;
+      const int64_t* off = p.offsets[f];
+      const int64_t s = off[row];
+      const int64_t len = row_end(off, row, p.B, p.nvalues[f]) - s;
+      const int64_t* val = p.values[f] + s;
+      if (lane == 0) h += len_hash(len, fi);
+      for (int64_t k0 = 0; k0 < len; k0 += 128) {
+        int64_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t k = k0 + u * 32 + lane;
+          x[u] = (k < len) ? __ldg(val + k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t k = k0 + u * 32 + lane;
+          if (k < len) h += elem_hash(x[u], k, fi);
+        }
+      }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) h += __shfl_xor_sync(0xffffffffu, h, d);
+    if (lane == src) mine = finalize_hash(h, p.hash_mask);
+  }
+  if (!is_head) return;
+  p.hash[idx] = mine;
   unsigned long long* tk = p.tkeys + (int64_t)g * p.C;
   uint32_t* tr = p.treps + (int64_t)g * p.C;
-  const uint64_t m = (uint64_t)p.C - 1;
-  uint64_t s = (h ^ (h >> 29)) & m;
+  const uint64_t msk = (uint64_t)p.C - 1;
+  uint64_t s = (mine ^ (mine >> 29)) & msk;
   while (true) {
-    const unsigned long long k = atomicCAS(&tk[s], 0ull, h);
-    if (k == 0ull || k == h) {
+    const unsigned long long k = atomicCAS(&tk[s], 0ull, (unsigned long long)mine);
+    if (k == 0ull || k == mine) {
       atomicMin(&tr[s], (uint32_t)i);
       p.slot_of[idx] = (uint32_t)s;
       return;
     }
-    s = (s + 1) & m;
+    s = (s + 1) & msk;
   }
 }
 
@@ -522,8 +559,18 @@ extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_
     p.treps = s.treps + (int64_t)g0 * C;
 
     const int64_t rows = (int64_t)p.G * B;
+    {  // groups with the most values first (their blocks are the longest)
+      std::vector<std::pair<int64_t, int>> order;
+      for (int g = 0; g < p.G; ++g) {
+        int64_t nvg = 0;
+        for (int ff = p.group_first[g]; ff < p.group_first[g + 1]; ++ff) nvg += p.nvalues[ff];
+        order.push_back({-nvg, g});
+      }
+      std::stable_sort(order.begin(), order.end());
+      for (int k = 0; k < p.G; ++k) p.rs_group[k] = order[k].second;
+    }
     k_rowscan<<<dim3((unsigned)ceil_div(B, RS_RPB), p.G), RS_NT, 0, stream>>>(p);
-    k_insert<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
+    k_insert<<<(unsigned)ceil_div((int64_t)p.G * ceil_div(B, 32) * 32, 256), 256, 0, stream>>>(p);
     k_resolve<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
     k_fallback<<<p.G, FB_NT, 0, stream>>>(p);
     k_number<<<p.G, NB_NT, 0, stream>>>(p);
