@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--shards", type=int, default=0,
                     help="N>1: row shards per table (0 = auto: the fewest that fit HBM)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="run the backward's prepare half on the main stream")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0,
@@ -266,7 +268,8 @@ def main():
     tables = {k: R.EmbeddingTable.create_on_device(k, args.rows, args.dim, seed=i, device=dev)
               for i, k in enumerate(keys)}
     caps = {k: batch.values[k].size for k in keys}
-    step = TrainStep([[k] for k in keys], args.batch, caps, tables, "sum", args.lr, args.mode, dev)
+    step = TrainStep([[k] for k in keys], args.batch, caps, tables, "sum", args.lr, args.mode, dev,
+                     overlap=not args.no_overlap)
     step.load_batch(batch.values, batch.offsets)
     step.fill_grad_out(1 + rank)
     torch.cuda.synchronize()

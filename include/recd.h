@@ -160,6 +160,28 @@ int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t
                   int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
                   recd_stream_t stream);
 
+/* recd_pool_bwd in two halves, called with identical arguments and the same
+ * scratch: _prepare enqueues the gradient-independent work (inverse CSR,
+ * occurrence pairs and their sort by ID; grad_out is not read) and can run on
+ * a side stream right after recd_dedup, overlapping the forward; _finish
+ * enqueues the gradient reduction and the sorted scatter-add / SGD. */
+int recd_pool_bwd_prepare(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                          float* const* tables, const int64_t* table_rows,
+                          const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                          const int64_t* value_caps, const int64_t* counts,
+                          const int64_t* const* inverse, const float* const* grad_out, float lr,
+                          int32_t apply_sgd, int64_t* const* grad_ids_out,
+                          float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
+                          size_t scratch_bytes, recd_stream_t stream);
+int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                         float* const* tables, const int64_t* table_rows,
+                         const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                         const int64_t* value_caps, const int64_t* counts,
+                         const int64_t* const* inverse, const float* const* grad_out, float lr,
+                         int32_t apply_sgd, int64_t* const* grad_ids_out,
+                         float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
+                         size_t scratch_bytes, recd_stream_t stream);
+
 /* Source half: grad_u_out[f] ([U x dim]) = grad_u of recd_pool_bwd (avg scaled). */
 size_t recd_grad_unique_scratch_bytes(int32_t num_features, int64_t batch_size);
 int recd_grad_unique(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,

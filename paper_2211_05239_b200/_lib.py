@@ -48,6 +48,10 @@ _SIGS = {
     "recd_pool_bwd_scratch_bytes": (_sz, [_i32, _i64, _i32, _p64]),
     "recd_pool_bwd": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _pp,
                              _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_pool_bwd_prepare": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp,
+                                     _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_pool_bwd_finish": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp,
+                                    _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_grad_unique_scratch_bytes": (_sz, [_i32, _i64]),
     "recd_grad_unique": (_i32, [_i32, _i64, _i32, _i32, _pp, _vp, _pp, _pp, _pp, _vp, _sz, _vp]),
     "recd_sparse_sgd_scratch_bytes": (_sz, [_i32, _p64]),

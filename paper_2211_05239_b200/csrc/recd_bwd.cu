@@ -240,7 +240,10 @@ __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t
   return n;
 }
 
-constexpr int SC_RS = 8;  // table rows prefetched ahead per warp (shared-memory ring)
+#ifndef RECD_SC_RS
+#define RECD_SC_RS 8
+#endif
+constexpr int SC_RS = RECD_SC_RS;  // table rows prefetched ahead per warp (shared-memory ring)
 
 // One warp per (chunk of RC sorted positions, column block).  Runs of equal
 // IDs that start in the chunk are reduced in position order (== ascending
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   constexpr int V = C::VW;
   __shared__ uint16_t s_starts[8][RC + 2];
   __shared__ uint32_t s_ids[8][RC];
-  __shared__ __align__(16) float s_ring[8][SC_RS][C::CB];
+  __shared__ __align__(128) float s_ring[8][SC_RS][C::CB];
   __shared__ uint32_t s_win[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
@@ -507,6 +510,7 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
 //   grad    : grad_u written to caller buffers only
 //   scatter : occurrences -> sort -> scatter, reading caller unique-row grads
 enum class BwdMode { Full, GradOnly, ScatterOnly };
+enum { PH_PREP = 1, PH_FINISH = 2, PH_ALL = 3 };
 
 int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* tables,
             const int64_t* table_rows, const int64_t* const* uvalues,
@@ -514,7 +518,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
             const int64_t* const* inverse, const float* const* grad_out, float* const* gout_ext,
             const float* const* grow_ext, float lr, int apply_sgd, int64_t* const* grad_ids_out,
             float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
-            size_t scratch_bytes, cudaStream_t stream) {
+            size_t scratch_bytes, cudaStream_t stream, int phase = PH_ALL) {
   if (F <= 0 || F > RECD_MAX_FEAT || B <= 0 || dim <= 0 || !counts) return RECD_ERR_ARG;
   if (mode != RECD_POOL_SUM && mode != RECD_POOL_AVG) return RECD_ERR_UNSUPPORTED;
   if (B >= (1ll << 24)) return RECD_ERR_UNSUPPORTED;  // occurrence tags hold u in 24 bits
@@ -524,7 +528,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   std::vector<int64_t> dummy_rows(F, 1), dummy_caps(F, 1);
   for (int f = 0; f < F; ++f) {
     if (!uoffsets[f]) return RECD_ERR_ARG;
-    if (do_grad && !grad_out[f]) return RECD_ERR_ARG;
+    if (do_grad && (phase & PH_FINISH) && !grad_out[f]) return RECD_ERR_ARG;
     if (bm == BwdMode::GradOnly && !gout_ext[f]) return RECD_ERR_ARG;
     if (bm == BwdMode::ScatterOnly && !grow_ext[f]) return RECD_ERR_ARG;
     if (do_scatter) {
@@ -561,7 +565,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   for (int f = 0; f < F; ++f) {
     p.uvalues[f] = uvalues ? uvalues[f] : nullptr;
     p.uoffsets[f] = uoffsets[f];
-    p.grad_out[f] = do_grad ? grad_out[f] : nullptr;
+    p.grad_out[f] = (do_grad && grad_out) ? grad_out[f] : nullptr;
     p.feat_is[f] = pl.feat_is[f];
     p.feat_ts[f] = pl.feat_ts[f];
     if (bm == BwdMode::Full) {
@@ -604,51 +608,65 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   p.csr_start = sc.csr_start;
   p.run_part = sc.run_part;
 
-  k_bwd_setup<<<1, 32, 0, stream>>>(p);
-  note_launch();
+  const bool prep = (phase & PH_PREP) != 0, fin = (phase & PH_FINISH) != 0;
+  // sorted buffers: a stable LSD sort of `bits` bits ends in the alternate
+  // buffers after an odd number of 8-bit passes
+  auto odd_passes = [](int64_t bits) { return ((bits + 7) / 8) % 2 == 1; };
+  int64_t maxrows = 1;
+  for (int s = 0; s < pl.nts; ++s) maxrows = std::max(maxrows, pl.table_rows[s]);
+  p.inv_keys = odd_passes(bits_for(B)) ? sc.inv_k1 : sc.inv_k0;
+  p.inv_rows = odd_passes(bits_for(B)) ? sc.inv_v1 : sc.inv_v0;
+  p.occ_keys = odd_passes(bits_for(maxrows)) ? sc.occ_k1 : sc.occ_k0;
+  p.occ_vals = odd_passes(bits_for(maxrows)) ? sc.occ_v1 : sc.occ_v0;
+
+  // ---- prepare: everything that depends on the IKJT only (no gradient)
+  if (prep) {
+    k_bwd_setup<<<1, 32, 0, stream>>>(p);
+    note_launch();
+    // 1. inverse CSR
+    if (do_grad && pl.nis > 0) {
+      const int64_t n = (int64_t)pl.nis * B;
+      k_inv_pairs<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p, sc.inv_k0, sc.inv_v0);
+      note_launch();
+      std::vector<SegDesc> segs;
+      for (int s = 0; s < pl.nis; ++s) segs.push_back({(int64_t)s * B, B, sc.is_count + s});
+      bool alt = false;
+      int rc = seg_sort_pairs(segs.data(), pl.nis, (int)bits_for(B), sc.inv_k0, sc.inv_v0,
+                              sc.inv_k1, sc.inv_v1, sc.hist, &alt, stream);
+      if (rc != RECD_OK) return rc;
+      k_csr_bounds<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p);
+      note_launch();
+    }
+    // 3-4. occurrences, sorted by ID per table segment
+    if (do_scatter) {
+      k_occ<<<num_sms() * 4, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
+      note_launch();
+      std::vector<SegDesc> segs;
+      for (int s = 0; s < pl.nts; ++s) segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
+      bool alt = false;
+      int r2 = seg_sort_pairs(segs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
+                              sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream);
+      if (r2 != RECD_OK) return r2;
+    }
+  }
+  if (!fin) {
+    RECD_LAUNCH_CHECK();
+    return RECD_OK;
+  }
+  // ---- finish: gradient-dependent work
   if (do_scatter && !apply_sgd)
     RECD_CUDA_CHECK(cudaMemsetAsync(grad_counts_out, 0, sizeof(int64_t) * F, stream));
-
-  // 1. inverse CSR
-  if (do_grad && pl.nis > 0) {
-    const int64_t n = (int64_t)pl.nis * B;
-    k_inv_pairs<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p, sc.inv_k0, sc.inv_v0);
-    note_launch();
-    std::vector<SegDesc> segs;
-    for (int s = 0; s < pl.nis; ++s) segs.push_back({(int64_t)s * B, B, sc.is_count + s});
-    bool alt = false;
-    int rc = seg_sort_pairs(segs.data(), pl.nis, (int)bits_for(B), sc.inv_k0, sc.inv_v0, sc.inv_k1,
-                            sc.inv_v1, sc.hist, &alt, stream);
-    if (rc != RECD_OK) return rc;
-    p.inv_keys = alt ? sc.inv_k1 : sc.inv_k0;
-    p.inv_rows = alt ? sc.inv_v1 : sc.inv_v0;
-    k_csr_bounds<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p);
-    note_launch();
-  }
-  // 2-5
   int rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, 0, {
     const int ncb = col_blocks<C>(dim);
+    // 2. unique-row gradients
     if (do_grad) {
       const unsigned grid =
           (unsigned)std::min<int64_t>(ceil_div(B * F * ncb, 8), (int64_t)num_sms() * 16);
       k_grad_u<C><<<grid, 256, 0, stream>>>(p);
       note_launch();
     }
+    // 5. sorted scatter-add (+ fused SGD)
     if (do_scatter) {
-      k_occ<<<num_sms() * 4, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
-      note_launch();
-      std::vector<SegDesc> segs;
-      int64_t maxrows = 1;
-      for (int s = 0; s < pl.nts; ++s) {
-        segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
-        maxrows = std::max(maxrows, pl.table_rows[s]);
-      }
-      bool alt = false;
-      int r2 = seg_sort_pairs(segs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
-                              sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream);
-      if (r2 != RECD_OK) return r2;
-      p.occ_keys = alt ? sc.occ_k1 : sc.occ_k0;
-      p.occ_vals = alt ? sc.occ_v1 : sc.occ_v0;
       if (!apply_sgd) {
         k_run_count<<<(unsigned)pl.rc_chunks, RC, 0, stream>>>(p);
         note_launch();
@@ -711,6 +729,38 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
                  uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
                  grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
                  (cudaStream_t)stream);
+}
+
+// Split form of recd_pool_bwd: _prepare enqueues the gradient-independent
+// half (inverse CSR, occurrence pairs, their sort by ID) and may run on a side
+// stream as soon as the IKJT exists, overlapping the forward; _finish (same
+// arguments, same scratch) enqueues the gradient reduction and the scatter.
+extern "C" int recd_pool_bwd_prepare(int32_t num_features, int64_t batch_size, int32_t dim,
+                                     int32_t mode, float* const* tables, const int64_t* table_rows,
+                                     const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                                     const int64_t* value_caps, const int64_t* counts,
+                                     const int64_t* const* inverse, const float* const* grad_out,
+                                     float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
+                                     float* const* grad_rows_out, int64_t* grad_counts_out,
+                                     void* scratch, size_t scratch_bytes, recd_stream_t stream) {
+  return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
+                 uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
+                 grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
+                 (cudaStream_t)stream, PH_PREP);
+}
+
+extern "C" int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, int32_t dim,
+                                    int32_t mode, float* const* tables, const int64_t* table_rows,
+                                    const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                                    const int64_t* value_caps, const int64_t* counts,
+                                    const int64_t* const* inverse, const float* const* grad_out,
+                                    float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
+                                    float* const* grad_rows_out, int64_t* grad_counts_out,
+                                    void* scratch, size_t scratch_bytes, recd_stream_t stream) {
+  return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
+                 uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
+                 grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
+                 (cudaStream_t)stream, PH_FINISH);
 }
 
 extern "C" size_t recd_grad_unique_scratch_bytes(int32_t num_features, int64_t batch_size) {

@@ -12,14 +12,15 @@
 //              each row with its predecessor: head[i] = row i differs from row
 //              i-1 (session-clustered batches make ~80% of rows non-heads); the
 //              block also clears its slice of the group's hash table.
-//   k_insert   heads only: warp-cooperative 64-bit row hash, open-addressing
-//              table (64-bit key, L2 resident), rep = atomicMin(row) per key.
+//              A second pass hashes the chunk's heads (warp per head row).
+//   k_insert   heads only: open-addressing table (64-bit key, L2 resident),
+//              rep = atomicMin(row) per key.
 //   k_resolve  heads whose rep != self are fully compared with the rep; a
 //              mismatch (a true 64-bit collision) is marked pending.
 //   k_fallback (cold) exact sequential resolution of pending heads.
-//   k_number   one CTA per group: run-head propagation, first-occurrence
-//              flags, uid scan, inverse, unique offsets (one scan per feature).
-//   k_copy     warp per unique row copies its lists into the unique values.
+//   k_num_*    chunk-parallel numbering: run-head propagation, first-occurrence
+//              uids, unique offsets per feature, inverse (reduce/scan/down).
+//   k_copy     value-parallel gather of the unique lists into the unique values.
 #include <algorithm>
 #include <vector>
 
@@ -50,11 +51,15 @@ struct DedupParams {
   int32_t* cls;         // [G][B]  class representative (min row of the class)
   int32_t* uidmap;      // [G][B]
   int32_t* first_rows;  // [G][B]
+  int64_t* nb_rh;       // [G][nch] numbering chunk aggregates
+  int64_t* nb_nf;       // [G][nch]
+  int64_t* nb_len;      // [F][nch]
   int32_t* fb_list;     // [G][B]
   unsigned long long* tkeys;  // [G][C]
   uint32_t* treps;            // [G][C]
   int32_t* collide;           // [G]
-  int rs_group[RECD_MAX_FEAT];  // k_rowscan: groups in launch order (most values first)
+  int rs_group[RECD_MAX_FEAT];
+  int64_t cp_blk0[RECD_MAX_FEAT + 1];  // k_copy: first block of each feature  // k_rowscan: groups in launch order (most values first)
 };
 
 __device__ __forceinline__ int64_t row_begin(const int64_t* off, int64_t i) { return off[i]; }
@@ -182,36 +187,20 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
   }
   uint8_t* head = p.head + (int64_t)g * p.B;
   for (int j = tid; j < n; j += RS_NT) head[r0 + j] = s_mism[j] ? 1 : 0;
-}
-
-// ----------------------------------------------------------------- insert
-// Warp per 32 rows of a group: the run heads among them are hashed one at a
-// time by the whole warp (lane-strided, coalesced), then every head lane
-// inserts its hash: open addressing, rep = atomicMin(row) per key.
-__global__ void __launch_bounds__(256) k_insert(const __grid_constant__ DedupParams p) {
-  const int64_t wpg = ceil_div(p.B, 32);
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= (int64_t)p.G * wpg) return;
-  const int lane = threadIdx.x & 31;
-  const int g = (int)(w / wpg);
-  const int64_t i = (w - (int64_t)g * wpg) * 32 + lane;
-  const int64_t idx = (int64_t)g * p.B + i;
-  const bool is_head = i < p.B && p.head[idx];
-  unsigned m = __ballot_sync(0xffffffffu, is_head);
-  if (!m) return;
-  const int fbeg = p.group_first[g], fend = p.group_first[g + 1];
-  uint64_t mine = 0;
-  while (m) {
-    const int src = __ffs(m) - 1;
-    m &= m - 1;
-    const int64_t row = i - lane + src;
+  // content hash of the chunk's heads (their values were just streamed, so
+  // the re-read is mostly served by L2): warp per head row, lane-strided
+  const int warp = tid >> 5, lane = tid & 31;
+  uint64_t* hash = p.hash + (int64_t)g * p.B;
+  for (int j = warp; j < n; j += RS_NT / 32) {
+    if (!s_mism[j]) continue;
+    const int64_t row = r0 + j;
     uint64_t h = 0;
     for (int f = fbeg; f < fend; ++f) {
       const int fi = f - fbeg;
       const int64_t* off = p.offsets[f];
-      const int64_t s = off[row];
-      const int64_t len = row_end(off, row, p.B, p.nvalues[f]) - s;
-      const int64_t* val = p.values[f] + s;
+      const int64_t st = (f == fend - 1) ? s_start[j] : off[row];
+      const int64_t len = (f == fend - 1) ? s_start[j + 1] - st : row_end(off, row, p.B, p.nvalues[f]) - st;
+      const int64_t* val = p.values[f] + st;
       if (lane == 0) h += len_hash(len, fi);
       for (int64_t k0 = 0; k0 < len; k0 += 128) {
         int64_t x[4];
@@ -229,22 +218,32 @@ __global__ void __launch_bounds__(256) k_insert(const __grid_constant__ DedupPar
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) h += __shfl_xor_sync(0xffffffffu, h, d);
-    if (lane == src) mine = finalize_hash(h, p.hash_mask);
+    if (lane == 0) hash[row] = finalize_hash(h, p.hash_mask);
   }
-  if (!is_head) return;
-  p.hash[idx] = mine;
+}
+
+// ----------------------------------------------------------------- insert
+// heads only: open-addressing table (64-bit key, L2 resident),
+// rep = atomicMin(row) per key -> deterministic min row.
+__global__ void __launch_bounds__(256) k_insert(const __grid_constant__ DedupParams p) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)p.G * p.B) return;
+  const int g = (int)(idx / p.B);
+  if (!p.head[idx]) return;
+  const int64_t i = idx - (int64_t)g * p.B;
+  const unsigned long long h = p.hash[idx];
   unsigned long long* tk = p.tkeys + (int64_t)g * p.C;
   uint32_t* tr = p.treps + (int64_t)g * p.C;
-  const uint64_t msk = (uint64_t)p.C - 1;
-  uint64_t s = (mine ^ (mine >> 29)) & msk;
+  const uint64_t m = (uint64_t)p.C - 1;
+  uint64_t s = (h ^ (h >> 29)) & m;
   while (true) {
-    const unsigned long long k = atomicCAS(&tk[s], 0ull, (unsigned long long)mine);
-    if (k == 0ull || k == mine) {
+    const unsigned long long k = atomicCAS(&tk[s], 0ull, h);
+    if (k == 0ull || k == h) {
       atomicMin(&tr[s], (uint32_t)i);
       p.slot_of[idx] = (uint32_t)s;
       return;
     }
-    s = (s + 1) & msk;
+    s = (s + 1) & m;
   }
 }
 
@@ -320,141 +319,256 @@ __global__ void __launch_bounds__(FB_NT) k_fallback(const __grid_constant__ Dedu
 }
 
 // ----------------------------------------------------------------- number
-constexpr int NB_NT = 1024;
-constexpr int NB_ITEMS = 16;
+// Chunk-parallel numbering (2048-row chunks): a row is a first occurrence iff
+// it is a head that represents its class (cls[i] == i), which is known
+// locally, so numbering is reduce -> scan -> downsweep:
+//   k_num_reduce  per chunk: last head, #first rows, their value counts per feature
+//   k_num_scan    per group: exclusive chunk prefixes (+ incoming run head), totals
+//   k_num_down    per chunk: run-head propagation (cls of every row), uid of
+//                 first rows, first_rows[uid], unique offsets per feature
+//   k_num_inv     inverse[i] = uidmap[cls[i]] (needs every chunk's uidmap)
+constexpr int NB_NT = 256;
+constexpr int NB_ITEMS = 8;
+constexpr int NB_CH = NB_NT * NB_ITEMS;  // rows per chunk
 
-__global__ void __launch_bounds__(NB_NT) k_number(const __grid_constant__ DedupParams p) {
+__global__ void __launch_bounds__(NB_NT) k_num_reduce(const __grid_constant__ DedupParams p) {
+  const int g = blockIdx.y;
+  const int64_t c = blockIdx.x;
+  const int64_t B = p.B;
+  const int tid = threadIdx.x;
+  const uint8_t* head = p.head + (int64_t)g * B;
+  const int32_t* cls = p.cls + (int64_t)g * B;
+  const int64_t i0 = c * NB_CH + (int64_t)tid * NB_ITEMS;
+  __shared__ int64_t s_scan[32];
+  int64_t lrh = -1, nf = 0;
+  bool first[NB_ITEMS];
+#pragma unroll
+  for (int k = 0; k < NB_ITEMS; ++k) {
+    const int64_t i = i0 + k;
+    first[k] = false;
+    if (i < B && head[i]) {
+      lrh = i;
+      first[k] = cls[i] == (int32_t)i;
+      nf += first[k];
+    }
+  }
+  const int64_t nch = ceil_div(B, NB_CH);
+  int64_t tot;
+  block_inclusive_max<NB_NT>(lrh, s_scan, &tot);
+  if (tid == 0) p.nb_rh[(int64_t)g * nch + c] = tot;
+  block_exclusive_scan<NB_NT>(nf, s_scan, &tot);
+  if (tid == 0) p.nb_nf[(int64_t)g * nch + c] = tot;
+  for (int f = p.group_first[g]; f < p.group_first[g + 1]; ++f) {
+    const int64_t* off = p.offsets[f];
+    int64_t ls = 0;
+#pragma unroll
+    for (int k = 0; k < NB_ITEMS; ++k)
+      if (first[k]) ls += row_end(off, i0 + k, B, p.nvalues[f]) - off[i0 + k];
+    block_exclusive_scan<NB_NT>(ls, s_scan, &tot);
+    if (tid == 0) p.nb_len[(int64_t)f * nch + c] = tot;
+  }
+}
+
+// block per group: chunk prefixes in place (rh -> incoming run head, an
+// exclusive max; nf / len -> exclusive sums) and the group's totals
+__global__ void __launch_bounds__(NB_NT) k_num_scan(const __grid_constant__ DedupParams p) {
   const int g = blockIdx.x;
   const int tid = threadIdx.x;
-  const int64_t B = p.B;
-  const uint8_t* head = p.head + (int64_t)g * B;
-  int32_t* cls = p.cls + (int64_t)g * B;
-  int32_t* uidmap = p.uidmap + (int64_t)g * B;
-  int32_t* first_rows = p.first_rows + (int64_t)g * B;
-  const int fbeg = p.group_first[g], fend = p.group_first[g + 1];
-  int64_t* inverse = p.inverse[g];
-
+  const int64_t nch = ceil_div(p.B, NB_CH);
   __shared__ int64_t s_scan[32];
-  __shared__ int64_t s_carry_len[RECD_MAX_FEAT];
-  for (int f = tid; f < RECD_MAX_FEAT; f += NB_NT) s_carry_len[f] = 0;
-  int64_t carry_rh = -1, carry_uid = 0;
-  __syncthreads();
-
-  constexpr int TILE = NB_NT * NB_ITEMS;
-  for (int64_t tb = 0; tb < B; tb += TILE) {
-    const int64_t i0 = tb + (int64_t)tid * NB_ITEMS;
-    // (a) run heads: inclusive max-scan of (head ? i : -1)
-    int64_t lrh = -1;
-#pragma unroll
-    for (int k = 0; k < NB_ITEMS; ++k) {
-      const int64_t i = i0 + k;
-      if (i < B && head[i]) lrh = i;
-    }
+  __shared__ int64_t s_last[NB_NT];
+  int64_t crh = -1, cnf = 0;
+  for (int64_t c0 = 0; c0 < nch; c0 += NB_NT) {
+    const int64_t c = c0 + tid;
+    int64_t* rh = p.nb_rh + (int64_t)g * nch;
+    int64_t* nf = p.nb_nf + (int64_t)g * nch;
+    const int64_t vrh = c < nch ? rh[c] : -1;
+    const int64_t vnf = c < nch ? nf[c] : 0;
     int64_t tot;
-    int64_t incl = block_inclusive_max<NB_NT>(lrh, s_scan, &tot);
-    // exclusive prefix = inclusive of previous thread
-    int64_t prev = __shfl_up_sync(0xffffffffu, incl, 1);
-    if ((tid & 31) == 0) prev = -1;
-    __shared__ int64_t s_warp_last[32];
-    if ((tid & 31) == 31) s_warp_last[tid >> 5] = incl;
+    const int64_t incl = block_inclusive_max<NB_NT>(vrh, s_scan, &tot);
+    s_last[tid] = incl;
     __syncthreads();
-    if ((tid & 31) == 0 && tid > 0) prev = s_warp_last[(tid >> 5) - 1];
-    int64_t rh = max(prev, carry_rh);
-    // (b) class representative of every row, (c) first-occurrence flags
-    int32_t cl[NB_ITEMS];
-    int nfirst = 0;
-#pragma unroll
-    for (int k = 0; k < NB_ITEMS; ++k) {
-      const int64_t i = i0 + k;
-      cl[k] = -1;
-      if (i < B) {
-        if (head[i]) rh = i;
-        cl[k] = cls[rh];
-        nfirst += (cl[k] == (int32_t)i);
-      }
-    }
-    carry_rh = max(carry_rh, tot);
-    int64_t utot;
-    int64_t uid = carry_uid + block_exclusive_scan<NB_NT>(nfirst, s_scan, &utot);
-    // (d) uid map + first rows; (e) unique offsets per feature
-#pragma unroll
-    for (int k = 0; k < NB_ITEMS; ++k) {
-      const int64_t i = i0 + k;
-      if (i < B && cl[k] == (int32_t)i) {
-        uidmap[i] = (int32_t)uid;
-        first_rows[uid] = (int32_t)i;
-        ++uid;
-      }
-    }
-    for (int f = fbeg; f < fend; ++f) {
-      const int64_t* off = p.offsets[f];
-      const int64_t nv = p.nvalues[f];
-      int64_t lsum = 0;
-#pragma unroll
-      for (int k = 0; k < NB_ITEMS; ++k) {
-        const int64_t i = i0 + k;
-        if (i < B && cl[k] == (int32_t)i) lsum += row_end(off, i, B, nv) - off[i];
-      }
-      int64_t ltot;
-      int64_t o = s_carry_len[f] + block_exclusive_scan<NB_NT>(lsum, s_scan, &ltot);
-      int64_t* uoff = p.uoffsets[f];
-#pragma unroll
-      for (int k = 0; k < NB_ITEMS; ++k) {
-        const int64_t i = i0 + k;
-        if (i < B && cl[k] == (int32_t)i) {
-          uoff[uidmap[i]] = o;
-          o += row_end(off, i, B, nv) - off[i];
-        }
-      }
-      __syncthreads();
-      if (tid == 0) s_carry_len[f] += ltot;
-    }
-    carry_uid += utot;
-    __syncthreads();  // uidmap writes of this tile visible block-wide
-    // (g) inverse
-#pragma unroll
-    for (int k = 0; k < NB_ITEMS; ++k) {
-      const int64_t i = i0 + k;
-      if (i < B) inverse[i] = uidmap[cl[k]];
-    }
+    const int64_t excl = max(crh, tid ? s_last[tid - 1] : (int64_t)-1);
     __syncthreads();
+    crh = max(crh, tot);
+    const int64_t x = block_exclusive_scan<NB_NT>(vnf, s_scan, &tot);
+    if (c < nch) {
+      rh[c] = excl;
+      nf[c] = cnf + x;
+    }
+    cnf += tot;
   }
-  if (tid == 0) {
-    for (int f = fbeg; f < fend; ++f) {
-      p.count_rows[f] = carry_uid;
-      p.count_vals[f] = s_carry_len[f];
+  for (int f = p.group_first[g]; f < p.group_first[g + 1]; ++f) {
+    int64_t* ln = p.nb_len + (int64_t)f * nch;
+    int64_t carry = 0;
+    for (int64_t c0 = 0; c0 < nch; c0 += NB_NT) {
+      const int64_t c = c0 + tid;
+      int64_t tot;
+      const int64_t x = block_exclusive_scan<NB_NT>(c < nch ? ln[c] : 0, s_scan, &tot);
+      if (c < nch) ln[c] = carry + x;
+      carry += tot;
+    }
+    if (tid == 0) {
+      p.count_rows[f] = cnf;
+      p.count_vals[f] = carry;
     }
   }
 }
 
-// ------------------------------------------------------------------- copy
-__global__ void __launch_bounds__(256) k_copy(const __grid_constant__ DedupParams p) {
-  __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int f = 0; f < p.F; ++f) {
-      s_pref[f] = acc;
-      acc += p.count_rows[f];
+__global__ void __launch_bounds__(NB_NT) k_num_down(const __grid_constant__ DedupParams p) {
+  const int g = blockIdx.y;
+  const int64_t c = blockIdx.x;
+  const int64_t B = p.B;
+  const int tid = threadIdx.x;
+  const int64_t nch = ceil_div(B, NB_CH);
+  const uint8_t* head = p.head + (int64_t)g * B;
+  int32_t* cls = p.cls + (int64_t)g * B;
+  int32_t* uidmap = p.uidmap + (int64_t)g * B;
+  int32_t* first_rows = p.first_rows + (int64_t)g * B;
+  const int64_t i0 = c * NB_CH + (int64_t)tid * NB_ITEMS;
+  __shared__ int64_t s_scan[32];
+  __shared__ int64_t s_last[NB_NT];
+  // run heads: exclusive max over the chunk's threads, seeded with the incoming head
+  int64_t lrh = -1;
+  bool hd[NB_ITEMS];
+#pragma unroll
+  for (int k = 0; k < NB_ITEMS; ++k) {
+    const int64_t i = i0 + k;
+    hd[k] = i < B && head[i];
+    if (hd[k]) lrh = i;
+  }
+  int64_t tot;
+  const int64_t incl = block_inclusive_max<NB_NT>(lrh, s_scan, &tot);
+  s_last[tid] = incl;
+  __syncthreads();
+  int64_t rh = max(p.nb_rh[(int64_t)g * nch + c], tid ? s_last[tid - 1] : (int64_t)-1);
+  bool first[NB_ITEMS];
+  int64_t nf = 0;
+#pragma unroll
+  for (int k = 0; k < NB_ITEMS; ++k) {
+    const int64_t i = i0 + k;
+    first[k] = false;
+    if (i < B) {
+      if (hd[k]) {
+        rh = i;
+        first[k] = cls[i] == (int32_t)i;
+        nf += first[k];
+      } else {
+        cls[i] = cls[rh];  // rh is a head: its cls is final and never rewritten
+      }
     }
-    s_pref[p.F] = acc;
+  }
+  int64_t uid = p.nb_nf[(int64_t)g * nch + c] + block_exclusive_scan<NB_NT>(nf, s_scan, &tot);
+  int64_t uids[NB_ITEMS];
+#pragma unroll
+  for (int k = 0; k < NB_ITEMS; ++k) {
+    uids[k] = uid;
+    if (first[k]) {
+      uidmap[i0 + k] = (int32_t)uid;
+      first_rows[uid] = (int32_t)(i0 + k);
+      ++uid;
+    }
+  }
+  for (int f = p.group_first[g]; f < p.group_first[g + 1]; ++f) {
+    const int64_t* off = p.offsets[f];
+    int64_t len[NB_ITEMS];
+    int64_t ls = 0;
+#pragma unroll
+    for (int k = 0; k < NB_ITEMS; ++k) {
+      len[k] = first[k] ? row_end(off, i0 + k, B, p.nvalues[f]) - off[i0 + k] : 0;
+      ls += len[k];
+    }
+    int64_t o = p.nb_len[(int64_t)f * nch + c] + block_exclusive_scan<NB_NT>(ls, s_scan, &tot);
+    int64_t* uoff = p.uoffsets[f];
+#pragma unroll
+    for (int k = 0; k < NB_ITEMS; ++k)
+      if (first[k]) {
+        uoff[uids[k]] = o;
+        o += len[k];
+      }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_num_inv(const __grid_constant__ DedupParams p) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)p.G * p.B) return;
+  const int g = (int)(idx / p.B);
+  p.inverse[g][idx - (int64_t)g * p.B] = p.uidmap[(int64_t)g * p.B + p.cls[idx]];
+}
+
+// ------------------------------------------------------------------- copy
+// Value-parallel gather of the unique lists: block per 4096 unique values of
+// a feature.  The block locates its first unique row (32-ary warp search over
+// the unique offsets), stages (unique offset, source offset) of the rows it
+// spans in shared memory with one independent load chain per row, then the
+// block copies the values with consecutive threads on consecutive values.
+constexpr int CP_NT = 256;
+constexpr int CP_IT = 16;
+constexpr int CP_CH = CP_NT * CP_IT;  // unique values per block
+constexpr int CP_MAXR = 512;          // rows staged per pass
+
+__device__ __forceinline__ int64_t warp_last_le(const int64_t* a, int64_t n, int64_t x, int lane) {
+  // last index k in [0, n) with a[k] <= x (a non-decreasing, a[0] <= x)
+  int64_t lo = 0, hi = n;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t k = lo + (int64_t)lane * step;
+    const bool le = k < hi && a[k] <= x;
+    const unsigned b = __ballot_sync(0xffffffffu, le);
+    const int last = 31 - __clz(b);  // lane 0 always qualifies
+    lo = lo + (int64_t)last * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupParams p) {
+  int f = 0;
+  while (f + 1 < p.F && p.cp_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
+  const int64_t j0 = ((int64_t)blockIdx.x - p.cp_blk0[f]) * CP_CH;
+  const int64_t U = p.count_rows[f], NV = p.count_vals[f];
+  if (j0 >= NV) return;
+  const int64_t j1 = min(NV, j0 + (int64_t)CP_CH);
+  const int tid = threadIdx.x;
+  const int64_t* uoff = p.uoffsets[f];
+  const int64_t* off = p.offsets[f];
+  const int64_t* src = p.values[f];
+  int64_t* dst = p.uvalues[f];
+  const int32_t* frows = p.first_rows + (int64_t)p.feat_group[f] * p.B;
+  __shared__ int64_t s_u0;
+  __shared__ int64_t s_uo[CP_MAXR + 1];
+  __shared__ int64_t s_so[CP_MAXR];
+  if (tid < 32) {
+    const int64_t u = warp_last_le(uoff, U, j0, tid);
+    if (tid == 0) s_u0 = u;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t total = s_pref[p.F];
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
-       w += nwarps) {
-    int f = 0;
-    while (f + 1 < p.F && s_pref[f + 1] <= w) ++f;
-    const int64_t u = w - s_pref[f];
-    const int g = p.feat_group[f];
-    const int64_t row = p.first_rows[(int64_t)g * p.B + u];
-    const int64_t* off = p.offsets[f];
-    const int64_t s = off[row];
-    const int64_t len = row_end(off, row, p.B, p.nvalues[f]) - s;
-    const int64_t* src = p.values[f] + s;
-    int64_t* dst = p.uvalues[f] + p.uoffsets[f][u];
-    for (int64_t k = lane; k < len; k += 32) dst[k] = src[k];
+  int64_t u0 = s_u0;
+  while (true) {
+    const int nr = (int)min((int64_t)CP_MAXR, U - u0);
+    for (int t = tid; t <= nr; t += CP_NT) {
+      const int64_t u = u0 + t;
+      s_uo[t] = (t < nr) ? uoff[u] : ((u < U) ? uoff[u] : NV);
+      if (t < nr) s_so[t] = off[frows[u]];
+    }
+    __syncthreads();
+    const int64_t covered = s_uo[nr];  // values before row u0 + nr
+    const int64_t qa = max(j0, s_uo[0]), qb = min(j1, covered);
+    // values qa + k * CP_NT + tid: coalesced loads and stores; the row of each
+    // value by a search over the staged rows, starting from the previous one
+    int r = 0;
+    for (int64_t q = qa + tid; q < qb; q += CP_NT) {
+      int lo = r, hi = nr - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_uo[mid] <= q) lo = mid; else hi = mid - 1;
+      }
+      r = lo;
+      dst[q] = __ldg(src + s_so[r] + (q - s_uo[r]));
+    }
+    if (covered >= j1) break;
+    __syncthreads();
+    u0 += nr;
   }
 }
 
@@ -463,12 +577,18 @@ struct DedupScratch {
   uint64_t* hash;
   uint32_t* slot_of;
   int32_t *cls, *uidmap, *first_rows, *fb_list, *collide;
+  int64_t *nb_rh, *nb_nf, *nb_len;
   unsigned long long* tkeys;
   uint32_t* treps;
 };
 
-static size_t carve_dedup(void* base, size_t cap, int G, int64_t B, int64_t C, DedupScratch* s) {
+static size_t carve_dedup(void* base, size_t cap, int G, int F, int64_t B, int64_t C,
+                          DedupScratch* s) {
   Arena a(base, cap);
+  const int64_t nch = ceil_div(B, NB_CH);
+  s->nb_rh = a.take<int64_t>((size_t)G * nch);
+  s->nb_nf = a.take<int64_t>((size_t)G * nch);
+  s->nb_len = a.take<int64_t>((size_t)F * nch);
   s->head = a.take<uint8_t>((size_t)G * B);
   s->hash = a.take<uint64_t>((size_t)G * B);
   s->slot_of = a.take<uint32_t>((size_t)G * B);
@@ -492,10 +612,10 @@ extern "C" void recd_debug_set_hash_mask(uint64_t mask) { g_hash_mask = mask ? m
 
 extern "C" size_t recd_dedup_scratch_bytes(int32_t num_groups, int32_t num_features,
                                            int64_t batch_size) {
-  (void)num_features;
   DedupScratch s;
   // groups are processed in chunks of <= RECD_MAX_FEAT features; size for all
-  return carve_dedup(nullptr, 0, std::max(num_groups, 1), batch_size, table_slots(batch_size), &s);
+  return carve_dedup(nullptr, 0, std::max(num_groups, 1), std::max(num_features, 1), batch_size,
+                     table_slots(batch_size), &s);
 }
 
 extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
@@ -514,7 +634,7 @@ extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_
   }
   const int64_t B = batch_size, C = table_slots(B);
   DedupScratch s;
-  if (carve_dedup(scratch, scratch_bytes, num_groups, B, C, &s) > scratch_bytes) return RECD_ERR_SCRATCH;
+  if (carve_dedup(scratch, scratch_bytes, num_groups, F, B, C, &s) > scratch_bytes) return RECD_ERR_SCRATCH;
   RECD_CUDA_CHECK(cudaMemsetAsync(s.collide, 0, sizeof(int32_t) * num_groups, stream));
 
   int g0 = 0, f0 = 0;
@@ -555,6 +675,12 @@ extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_
     p.first_rows = s.first_rows + (int64_t)g0 * B;
     p.fb_list = s.fb_list + (int64_t)g0 * B;
     p.collide = s.collide + g0;
+    {
+      const int64_t nch = ceil_div(B, NB_CH);
+      p.nb_rh = s.nb_rh + (int64_t)g0 * nch;
+      p.nb_nf = s.nb_nf + (int64_t)g0 * nch;
+      p.nb_len = s.nb_len + (int64_t)f0 * nch;
+    }
     p.tkeys = s.tkeys + (int64_t)g0 * C;
     p.treps = s.treps + (int64_t)g0 * C;
 
@@ -570,12 +696,24 @@ extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_
       for (int k = 0; k < p.G; ++k) p.rs_group[k] = order[k].second;
     }
     k_rowscan<<<dim3((unsigned)ceil_div(B, RS_RPB), p.G), RS_NT, 0, stream>>>(p);
-    k_insert<<<(unsigned)ceil_div((int64_t)p.G * ceil_div(B, 32) * 32, 256), 256, 0, stream>>>(p);
+    k_insert<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
     k_resolve<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
     k_fallback<<<p.G, FB_NT, 0, stream>>>(p);
-    k_number<<<p.G, NB_NT, 0, stream>>>(p);
-    k_copy<<<num_sms() * 4, 256, 0, stream>>>(p);
-    note_launch(6);
+    {
+      const dim3 ng((unsigned)ceil_div(B, NB_CH), p.G);
+      k_num_reduce<<<ng, NB_NT, 0, stream>>>(p);
+      k_num_scan<<<p.G, NB_NT, 0, stream>>>(p);
+      k_num_down<<<ng, NB_NT, 0, stream>>>(p);
+      k_num_inv<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
+    }
+    int64_t cblk = 0;
+    for (int ff = 0; ff < p.F; ++ff) {
+      p.cp_blk0[ff] = cblk;
+      cblk += std::max<int64_t>(1, ceil_div(p.nvalues[ff], CP_CH));
+    }
+    p.cp_blk0[p.F] = cblk;
+    k_copy<<<(unsigned)cblk, CP_NT, 0, stream>>>(p);
+    note_launch(9);
     RECD_LAUNCH_CHECK();
     g0 = g1;
     f0 += nf;

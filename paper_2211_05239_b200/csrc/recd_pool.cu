@@ -83,16 +83,20 @@ __global__ void __launch_bounds__(256, RECD_POOL_MINB) k_pool_fwd(const __grid_c
 }
 
 // out[f][i] = pooled[f][inverse[f][i]]  (trainer_sim.py:558-561)
+// Warp per (32-row block, column block): one coalesced load of the 32 inverse
+// entries, then the rows' slices are gathered 8 at a time (8 loads in flight
+// per lane) and streamed out.
 template <class C>
 __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ PoolParams p) {
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
   const int ncb = col_blocks<C>(p.D);
+  const int64_t rb = ceil_div(p.B, 32);  // 32-row blocks per feature
   if (threadIdx.x == 0) {
     int64_t acc = 0;
     for (int f = 0; f < p.F; ++f) {
       s_pref[f] = acc;
       const bool active = p.out[f] != nullptr && p.out[f] != p.pooled[f];
-      acc += active ? p.B * ncb : 0;
+      acc += active ? rb * ncb : 0;
     }
     s_pref[p.F] = acc;
   }
@@ -103,12 +107,23 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ PoolPara
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
        w += nwarps) {
     const int f = find_seg(s_pref, p.F, w);
-    const ColWork cw = col_work<C>(w - s_pref[f], p.D, lane);
-    const int64_t i = cw.row;
-    const int64_t u = p.inverse[f] ? __ldg(p.inverse[f] + i) : i;
-    float x[C::VW];
-    C::ld(p.pooled[f] + u * p.D + cw.lo, cw.ok, x);
-    C::st(p.out[f] + i * p.D + cw.lo, cw.ok, x);
+    const ColWork cw = col_work<C>(w - s_pref[f], p.D, lane);  // cw.row = 32-row block
+    const int64_t i0 = cw.row * 32;
+    const int nr = (int)min((int64_t)32, p.B - i0);
+    const int64_t my = (lane < nr) ? (p.inverse[f] ? __ldg(p.inverse[f] + i0 + lane) : i0 + lane) : 0;
+    const float* src = p.pooled[f] + cw.lo;
+    float* dst = p.out[f] + i0 * p.D + cw.lo;
+    for (int r0 = 0; r0 < nr; r0 += 8) {
+      float x[8][C::VW];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int64_t u = __shfl_sync(0xffffffffu, my, (r0 + t) & 31);
+        if (r0 + t < nr) C::ld(src + u * p.D, cw.ok, x[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (r0 + t < nr) C::st(dst + (int64_t)(r0 + t) * p.D, cw.ok, x[t]);
+    }
   }
 }
 
@@ -349,7 +364,7 @@ __device__ __forceinline__ void pairwise_ring(RingRows<NB>& rr, int32_t m, float
 template <class C, int K>
 __global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_constant__ PoolParams p) {
   static_assert(C::VW == 4, "ring pool streams float4 lane slices");
-  extern __shared__ __align__(16) float s_ring[];
+  extern __shared__ __align__(128) float s_ring[];
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
   const int ncb = col_blocks<C>(p.D);
   if (threadIdx.x == 0) {
@@ -496,7 +511,7 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
       hook_after("k_pool_fwd", stream);
       note_launch();
       if (any_expand) {
-        k_expand<C><<<grid, 256, 0, stream>>>(p);
+        k_expand<C><<<grid_for(ceil_div(batch_size, 32) * p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
         note_launch();
       }
     });
@@ -557,7 +572,7 @@ extern "C" int recd_expand(int32_t num_features, int64_t batch_size, int32_t dim
       if (!p.pooled[f] || !p.out[f]) return RECD_ERR_ARG;
     }
     int rc = RECD_DISPATCH_COL(dim, {
-      k_expand<C><<<grid_for(batch_size * p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
+      k_expand<C><<<grid_for(ceil_div(batch_size, 32) * p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
       note_launch();
     });
     if (rc != RECD_OK) return rc;

@@ -1,15 +1,21 @@
 // Segmented stable LSD radix sort + segmented exclusive scan (sm_100a).
 //
-// Sort: reduce-then-scan per 8-bit digit pass.
-//   k_sort_up    block per 16K-element chunk: digit histogram (warp-aggregated
-//                shared atomics), stored digit-major per segment [d][chunk].
-//   k_sort_scan  block per segment: one exclusive scan over (digit, chunk) in
-//                that order gives every chunk's absolute output offset per digit.
-//   k_sort_down  block per chunk, 2048-element tiles: per-warp stable ranking
-//                with __match_any_sync, tile-local digit bases, staging in shared
-//                memory so the scatter writes runs of equal digits contiguously.
-// Element order inside a chunk is (tile, warp, round, lane) == input order, so
-// every pass is stable and the whole sort is deterministic.
+// Sort: one-sweep LSD, 8-bit digits.
+//   k_os_hist    block per 16K-element chunk: digit histograms of EVERY pass
+//                at once (keys read once), added to per-(segment, pass) global
+//                counts; also clears the tile status words of the first pass.
+//   k_os_setup   one block: per segment, tile prefix (actual counts) and the
+//                exclusive digit scans -> each digit's segment-relative base.
+//   k_onesweep   per pass, persistent blocks take 4096-element tiles in order
+//                (atomic ticket), rank them stably (warp match_any + per-warp
+//                digit counters), publish the tile's digit counts and look back
+//                over the preceding tiles of the segment (decoupled look-back,
+//                one thread per digit) for the tile's global digit offsets,
+//                then scatter through shared memory so runs of equal digits
+//                are written contiguously.  Keys and values move once per pass.
+// Element order inside a tile is (warp, round, lane) == input order and tiles
+// are ranked in segment order, so every pass is stable and the result
+// deterministic.
 #include <algorithm>
 #include <vector>
 
@@ -17,193 +23,155 @@
 
 namespace recd {
 
-constexpr int SORT_NT = 256;
-#ifndef RECD_SORT_ITEMS
-#define RECD_SORT_ITEMS 8
-#endif
-constexpr int SORT_ITEMS = RECD_SORT_ITEMS;
-constexpr int SORT_TILE = SORT_NT * SORT_ITEMS;  // 2048
-#ifndef RECD_SORT_CHUNK_TILES
-#define RECD_SORT_CHUNK_TILES 8
-#endif
-#ifndef RECD_SORT_UP_ATOMIC
-#define RECD_SORT_UP_ATOMIC 1
-#endif
-constexpr int SORT_CHUNK = SORT_TILE * RECD_SORT_CHUNK_TILES;  // elements per block
-constexpr int SORT_MAXSEG = 64;
+constexpr int OS_NT = 256;                     // threads == digits
+constexpr int OS_ITEMS = 16;
+constexpr int OS_TILE = OS_NT * OS_ITEMS;      // 4096 elements per tile
+constexpr int OS_WARPS = OS_NT / 32;
+constexpr int OS_HCHUNK = OS_TILE * 4;         // elements per histogram block
+constexpr int OS_MAXSEG = 64;
+constexpr int OS_MAXPASS = 4;
+constexpr uint32_t OS_AGG = 1u << 30, OS_PRE = 2u << 30, OS_CNT = (1u << 30) - 1;
 
-struct SortSegDev {
-  int64_t base;
-  const int64_t* count;
-  int64_t chunk0;   // first global chunk of the segment
-  int64_t nchunks;  // chunks reserved (capacity-based)
-  int64_t hbase;    // first hist word of the segment: 256 * chunk0
+struct OsSeg {
+  int64_t base;          // element offset of the segment
+  const int64_t* count;  // device: actual element count
+  int64_t tcap0;         // first capacity tile (status rows)
+  int64_t hchunk0;       // first histogram chunk
 };
 
-struct SortParams {
-  int S;
-  int shift;
-  int nbits;
-  int64_t total_chunks;
-  SortSegDev seg[SORT_MAXSEG];
+struct OsParams {
+  int S, npass, pass, shift, nbits, bits;
+  int64_t total_hchunks;
+  int64_t total_tcap;
+  OsSeg seg[OS_MAXSEG];
   const uint32_t* kin;
   const uint32_t* vin;
   uint32_t* kout;
   uint32_t* vout;
-  uint32_t* hist;
+  uint32_t* ghist;     // [S][OS_MAXPASS][256]: counts, then segment-relative digit bases
+  int64_t* tile0;      // [S + 1] prefix of actual tiles
+  uint32_t* counters;  // [OS_MAXPASS] tile tickets
+  uint32_t* status;    // [2][total_tcap][256]
 };
 
-__device__ __forceinline__ int chunk_seg(const SortParams& p, int64_t chunk) {
-  int lo = 0, hi = p.S - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (p.seg[mid].chunk0 <= chunk) lo = mid; else hi = mid - 1;
-  }
-  return lo;
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(SORT_NT) k_sort_up(const __grid_constant__ SortParams p) {
+__global__ void __launch_bounds__(OS_NT) k_os_hist(const __grid_constant__ OsParams p) {
   const int64_t chunk = blockIdx.x;
-  const int s = chunk_seg(p, chunk);
-  const SortSegDev& sg = p.seg[s];
-  const int64_t c = chunk - sg.chunk0;
+  int s = 0;
+  while (s + 1 < p.S && p.seg[s + 1].hchunk0 <= chunk) ++s;
+  const OsSeg& sg = p.seg[s];
+  if (chunk == 0 && threadIdx.x < OS_MAXPASS) p.counters[threadIdx.x] = 0;
   const int64_t n = *sg.count;
-  const int64_t lo = c * SORT_CHUNK;
+  const int64_t lo = (chunk - sg.hchunk0) * OS_HCHUNK;
   if (lo >= n) return;
-  const int64_t hi = min(n, lo + (int64_t)SORT_CHUNK);
-  const uint32_t mask = (1u << p.nbits) - 1u;
+  const int64_t hi = min(n, lo + (int64_t)OS_HCHUNK);
+  {  // clear the pass-0 status rows of the tiles in this chunk
+    const int64_t t0 = sg.tcap0 + lo / OS_TILE, t1 = sg.tcap0 + ceil_div(hi, OS_TILE);
+    for (int64_t e = t0 * 256 + threadIdx.x; e < t1 * 256; e += OS_NT) p.status[e] = 0u;
+  }
+  __shared__ uint32_t sh[OS_MAXPASS][256];
+  for (int q = 0; q < p.npass; ++q) sh[q][threadIdx.x] = 0;
+  __syncthreads();
   const uint32_t* k = p.kin + sg.base;
-  constexpr int U = 8;  // loads in flight per thread
-#if RECD_SORT_UP_ATOMIC
-  // per-warp sub-histograms, plain shared atomics (digits of random keys rarely collide)
-  __shared__ uint32_t shw[SORT_NT / 32][256];
-  const int warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int w = 0; w < SORT_NT / 32; ++w) shw[w][threadIdx.x] = 0;
-  __syncthreads();
-  for (int64_t j0 = lo; j0 < hi; j0 += SORT_NT * U) {
+  constexpr int U = 8;
+  for (int64_t j0 = lo; j0 < hi; j0 += OS_NT * U) {
     uint32_t kk[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + u * SORT_NT + threadIdx.x;
+      const int64_t j = j0 + u * OS_NT + threadIdx.x;
       kk[u] = j < hi ? __ldg(k + j) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + u * SORT_NT + threadIdx.x;
-      if (j < hi) atomicAdd(&shw[warp][(kk[u] >> p.shift) & mask], 1u);
+      const int64_t j = j0 + u * OS_NT + threadIdx.x;
+      if (j < hi)
+        for (int q = 0; q < p.npass; ++q)
+          atomicAdd(&sh[q][(kk[u] >> (8 * q)) & ((1u << min(8, p.bits - 8 * q)) - 1u)], 1u);
     }
   }
   __syncthreads();
-  uint32_t tot = 0;
-#pragma unroll
-  for (int w = 0; w < SORT_NT / 32; ++w) tot += shw[w][threadIdx.x];
-  p.hist[sg.hbase + (int64_t)threadIdx.x * sg.nchunks + c] = tot;
-#else
-  __shared__ uint32_t sh[256];
-  sh[threadIdx.x] = 0;
-  __syncthreads();
-  for (int64_t j0 = lo; j0 < hi; j0 += SORT_NT * U) {
-    uint32_t kk[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + u * SORT_NT + threadIdx.x;
-      kk[u] = j < hi ? __ldg(k + j) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + u * SORT_NT + threadIdx.x;
-      const bool valid = j < hi;
-      const uint32_t d = valid ? ((kk[u] >> p.shift) & mask) : 0x100u;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      if (valid && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[d], (uint32_t)__popc(peers));
-    }
+  for (int q = 0; q < p.npass; ++q) {
+    const uint32_t c = sh[q][threadIdx.x];
+    if (c) atomicAdd(&p.ghist[((int64_t)s * OS_MAXPASS + q) * 256 + threadIdx.x], c);
   }
-  __syncthreads();
-  p.hist[sg.hbase + (int64_t)threadIdx.x * sg.nchunks + c] = sh[threadIdx.x];
-#endif
 }
 
-constexpr int SCAN_NT = 1024;
-constexpr int SCAN_ITEMS = 8;
-
-// exclusive scan over (digit, chunk) of the active chunks, in place; adds the
-// segment base so the downsweep reads absolute output offsets.
-__global__ void __launch_bounds__(SCAN_NT) k_sort_scan(const __grid_constant__ SortParams p) {
-  const SortSegDev& sg = p.seg[blockIdx.x];
-  const int64_t n = *sg.count;
-  if (n <= 0) return;
-  const int64_t nact = ceil_div(n, SORT_CHUNK);
-  const int64_t E = 256 * nact;
+// block per (segment, pass): exclusive digit scan; block 0 also the tile prefix
+__global__ void __launch_bounds__(OS_NT) k_os_setup(const __grid_constant__ OsParams p) {
   __shared__ int64_t s_scan[32];
-  int64_t carry = sg.base;
-  for (int64_t tb = 0; tb < E; tb += SCAN_NT * SCAN_ITEMS) {
-    const int64_t e0 = tb + (int64_t)threadIdx.x * SCAN_ITEMS;
-    uint32_t v[SCAN_ITEMS];
-    int64_t sum = 0;
-#pragma unroll
-    for (int t = 0; t < SCAN_ITEMS; ++t) {
-      const int64_t e = e0 + t;
-      v[t] = 0;
-      if (e < E) {
-        const int64_t d = e / nact, c = e - d * nact;
-        v[t] = p.hist[sg.hbase + d * sg.nchunks + c];
-      }
-      sum += v[t];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int s = 0; s < p.S; ++s) {
+      p.tile0[s] = t;
+      t += ceil_div(*p.seg[s].count, OS_TILE);
     }
-    int64_t tot;
-    int64_t x = carry + block_exclusive_scan<SCAN_NT>(sum, s_scan, &tot);
-#pragma unroll
-    for (int t = 0; t < SCAN_ITEMS; ++t) {
-      const int64_t e = e0 + t;
-      if (e < E) {
-        const int64_t d = e / nact, c = e - d * nact;
-        p.hist[sg.hbase + d * sg.nchunks + c] = (uint32_t)x;
-      }
-      x += v[t];
-    }
-    carry += tot;
+    p.tile0[p.S] = t;
   }
+  const int s = blockIdx.x / p.npass, q = blockIdx.x - s * p.npass;
+  uint32_t* h = p.ghist + ((int64_t)s * OS_MAXPASS + q) * 256;
+  const uint32_t c = h[threadIdx.x];
+  int64_t tot;
+  const int64_t x = block_exclusive_scan<OS_NT>(c, s_scan, &tot);
+  h[threadIdx.x] = (uint32_t)x;
 }
 
-__global__ void __launch_bounds__(SORT_NT) k_sort_down(const __grid_constant__ SortParams p) {
-  const int64_t chunk = blockIdx.x;
-  const int s = chunk_seg(p, chunk);
-  const SortSegDev& sg = p.seg[s];
-  const int64_t c = chunk - sg.chunk0;
-  const int64_t n = *sg.count;
-  const int64_t lo = c * SORT_CHUNK;
-  if (lo >= n) return;
-  const int64_t hi = min(n, lo + (int64_t)SORT_CHUNK);
+#ifndef RECD_OS_MINB
+#define RECD_OS_MINB 3
+#endif
+__global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_constant__ OsParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t mask = (1u << p.nbits) - 1u;
-
-  __shared__ uint32_t s_off[256];
-  __shared__ uint32_t s_wcnt[SORT_NT / 32][256];
-  __shared__ uint32_t s_tdb[256];
-  __shared__ uint32_t s_keys[SORT_TILE];
-  __shared__ uint32_t s_vals[SORT_TILE];
-  __shared__ int64_t s_scan[32];
-
-  s_off[tid] = p.hist[sg.hbase + (int64_t)tid * sg.nchunks + c];
-  const uint32_t* kin = p.kin + sg.base;
-  const uint32_t* vin = p.vin + sg.base;
   const unsigned lt = lanemask_lt();
-
-  for (int64_t tlo = lo; tlo < hi; tlo += SORT_TILE) {
-    const int tn = (int)min((int64_t)SORT_TILE, hi - tlo);
+  __shared__ uint32_t s_wcnt[OS_WARPS][256];
+  __shared__ uint32_t s_tdb[256];
+  __shared__ uint32_t s_gb[256];
+  __shared__ uint32_t s_keys[OS_TILE];
+  __shared__ uint32_t s_vals[OS_TILE];
+  __shared__ int64_t s_scan[32];
+  __shared__ int64_t s_tile;
+  __shared__ int64_t s_t0[OS_MAXSEG + 1];
+  for (int q = tid; q <= p.S; q += OS_NT) s_t0[q] = p.tile0[q];
+  uint32_t* st_cur = p.status + (int64_t)(p.pass & 1) * p.total_tcap * 256;
+  uint32_t* st_next = p.status + (int64_t)((p.pass + 1) & 1) * p.total_tcap * 256;
+  __syncthreads();
+  const int64_t total = s_t0[p.S];
+  while (true) {
+    if (tid == 0) s_tile = atomicAdd(&p.counters[p.pass], 1u);
+    __syncthreads();
+    const int64_t t = s_tile;
+    if (t >= total) break;
+    int s = 0, shi = p.S - 1;  // last segment whose first tile <= t
+    while (s < shi) {
+      const int mid = (s + shi + 1) >> 1;
+      if (s_t0[mid] <= t) s = mid; else shi = mid - 1;
+    }
+    const OsSeg& sg = p.seg[s];
+    const int64_t lt_ = t - s_t0[s];
+    const int64_t n = *sg.count;
+    const int64_t lo = lt_ * OS_TILE;
+    const int tn = (int)min((int64_t)OS_TILE, n - lo);
+    const uint32_t* kin = p.kin + sg.base + lo;
+    const uint32_t* vin = p.vin + sg.base + lo;
     for (int d = lane; d < 256; d += 32) s_wcnt[warp][d] = 0;
     __syncwarp();
-    uint32_t key[SORT_ITEMS], val[SORT_ITEMS], rank[SORT_ITEMS];
+    uint32_t key[OS_ITEMS], val[OS_ITEMS], rank[OS_ITEMS];
 #pragma unroll
-    for (int r = 0; r < SORT_ITEMS; ++r) {  // all loads first: 16 in flight per thread
-      const int e = warp * (SORT_TILE / (SORT_NT / 32)) + r * 32 + lane;
-      key[r] = e < tn ? __ldg(kin + tlo + e) : 0u;
-      val[r] = e < tn ? __ldg(vin + tlo + e) : 0u;
+    for (int r = 0; r < OS_ITEMS; ++r) {
+      const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
+      key[r] = e < tn ? __ldg(kin + e) : 0u;
+      val[r] = e < tn ? __ldg(vin + e) : 0u;
     }
 #pragma unroll
-    for (int r = 0; r < SORT_ITEMS; ++r) {
-      const int e = warp * (SORT_TILE / (SORT_NT / 32)) + r * 32 + lane;
+    for (int r = 0; r < OS_ITEMS; ++r) {
+      const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
       const bool valid = e < tn;
       const uint32_t d = valid ? ((key[r] >> p.shift) & mask) : 0x100u;
       const unsigned peers = __match_any_sync(0xffffffffu, d);
@@ -215,23 +183,38 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_down(const __grid_constant__ S
       rank[r] = before + __popc(peers & lt);
     }
     __syncthreads();
-    uint32_t tile_cnt = 0;
-    {
-      const int d = tid;  // SORT_NT == 256 digits
+    // thread tid owns digit tid: per-warp bases, tile count, publish, look back
+    uint32_t cnt = 0;
 #pragma unroll
-      for (int w = 0; w < SORT_NT / 32; ++w) {
-        const uint32_t cnt = s_wcnt[w][d];
-        s_wcnt[w][d] = tile_cnt;
-        tile_cnt += cnt;
-      }
+    for (int w = 0; w < OS_WARPS; ++w) {
+      const uint32_t c = s_wcnt[w][tid];
+      s_wcnt[w][tid] = cnt;
+      cnt += c;
     }
+    uint32_t* my = st_cur + (sg.tcap0 + lt_) * 256 + tid;
+    uint32_t excl = 0;
+    if (lt_ == 0) {
+      st_relaxed(my, OS_PRE | cnt);
+    } else {
+      st_relaxed(my, OS_AGG | cnt);
+      for (int64_t k = lt_ - 1; k >= 0;) {
+        const uint32_t v = ld_relaxed(st_cur + (sg.tcap0 + k) * 256 + tid);
+        if ((v & ~OS_CNT) == 0u) continue;  // not published yet
+        excl += v & OS_CNT;
+        if (v & OS_PRE) break;
+        --k;
+      }
+      st_relaxed(my, OS_PRE | (excl + cnt));
+    }
+    if (p.pass + 1 < p.npass) st_next[(sg.tcap0 + lt_) * 256 + tid] = 0u;
+    s_gb[tid] = (uint32_t)(sg.base + p.ghist[((int64_t)s * OS_MAXPASS + p.pass) * 256 + tid] + excl);
     int64_t tot;
-    const int64_t tdb = block_exclusive_scan<SORT_NT>(tile_cnt, s_scan, &tot);
+    const int64_t tdb = block_exclusive_scan<OS_NT>(cnt, s_scan, &tot);
     s_tdb[tid] = (uint32_t)tdb;
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < SORT_ITEMS; ++r) {
-      const int e = warp * (SORT_TILE / (SORT_NT / 32)) + r * 32 + lane;
+    for (int r = 0; r < OS_ITEMS; ++r) {
+      const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
       if (e < tn) {
         const uint32_t d = (key[r] >> p.shift) & mask;
         const uint32_t lp = s_tdb[d] + s_wcnt[warp][d] + rank[r];
@@ -240,42 +223,56 @@ __global__ void __launch_bounds__(SORT_NT) k_sort_down(const __grid_constant__ S
       }
     }
     __syncthreads();
-    for (int q = tid; q < tn; q += SORT_NT) {
+    for (int q = tid; q < tn; q += OS_NT) {
       const uint32_t k = s_keys[q];
       const uint32_t d = (k >> p.shift) & mask;
-      const uint32_t pos = s_off[d] + (uint32_t)q - s_tdb[d];
+      const uint32_t pos = s_gb[d] + (uint32_t)q - s_tdb[d];
       p.kout[pos] = k;
       p.vout[pos] = s_vals[q];
     }
     __syncthreads();
-    s_off[tid] += tile_cnt;
-    __syncthreads();
   }
 }
 
-static void build_sort_params(const SegDesc* segs, int S, SortParams* p) {
+static void build_os_params(const SegDesc* segs, int S, OsParams* p) {
   memset(p, 0, sizeof(*p));
   p->S = S;
-  int64_t chunk = 0;
+  int64_t tc = 0, hc = 0;
   for (int s = 0; s < S; ++s) {
     p->seg[s].base = segs[s].base;
     p->seg[s].count = segs[s].count;
-    p->seg[s].chunk0 = chunk;
-    p->seg[s].nchunks = std::max<int64_t>(1, ceil_div(segs[s].cap, SORT_CHUNK));
-    p->seg[s].hbase = 256 * chunk;
-    chunk += p->seg[s].nchunks;
+    p->seg[s].tcap0 = tc;
+    p->seg[s].hchunk0 = hc;
+    tc += std::max<int64_t>(1, ceil_div(segs[s].cap, OS_TILE));
+    hc += std::max<int64_t>(1, ceil_div(segs[s].cap, OS_HCHUNK));
   }
-  p->total_chunks = chunk;
+  p->total_tcap = tc;
+  p->total_hchunks = hc;
+}
+
+// scratch words: ghist + tile0 (int64) + counters + 2 status planes
+static int64_t os_words(const OsParams& p) {
+  return (int64_t)OS_MAXSEG * OS_MAXPASS * 256 + 2 * (OS_MAXSEG + 1) + 64 + 2 * p.total_tcap * 256;
 }
 
 int64_t sort_hist_words(const SegDesc* segs, int S) {
   int64_t words = 0;
-  for (int s0 = 0; s0 < S; s0 += SORT_MAXSEG) {
-    SortParams p;
-    build_sort_params(segs + s0, std::min(SORT_MAXSEG, S - s0), &p);
-    words = std::max(words, 256 * p.total_chunks);
+  for (int s0 = 0; s0 < S; s0 += OS_MAXSEG) {
+    OsParams p;
+    build_os_params(segs + s0, std::min(OS_MAXSEG, S - s0), &p);
+    words = std::max(words, os_words(p));
   }
   return words;
+}
+
+static int os_grid() {
+  static int g = 0;
+  if (!g) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_onesweep, OS_NT, 0);
+    g = num_sms() * std::max(per, 1);
+  }
+  return g;
 }
 
 int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_t* vals,
@@ -284,19 +281,31 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
   *in_alt = false;
   if (S <= 0 || bits <= 0) return RECD_OK;
   const int npass = (bits + 7) / 8;
-  for (int s0 = 0; s0 < S; s0 += SORT_MAXSEG) {
-    SortParams p;
-    build_sort_params(segs + s0, std::min(SORT_MAXSEG, S - s0), &p);
+  if (npass > OS_MAXPASS) return RECD_ERR_UNSUPPORTED;
+  for (int s = 0; s < S; ++s)
+    if (segs[s].cap > (int64_t)OS_CNT) return RECD_ERR_UNSUPPORTED;
+  for (int s0 = 0; s0 < S; s0 += OS_MAXSEG) {
+    OsParams p;
+    build_os_params(segs + s0, std::min(OS_MAXSEG, S - s0), &p);
+    p.npass = npass;
+    p.bits = bits;
+    p.ghist = hist;
+    p.tile0 = reinterpret_cast<int64_t*>(hist + (int64_t)OS_MAXSEG * OS_MAXPASS * 256);
+    p.counters = reinterpret_cast<uint32_t*>(p.tile0 + OS_MAXSEG + 1);
+    p.status = p.counters + 64;
+    RECD_CUDA_CHECK(cudaMemsetAsync(p.ghist, 0, sizeof(uint32_t) * p.S * OS_MAXPASS * 256, stream));
+    p.kin = keys;
+    k_os_hist<<<(unsigned)p.total_hchunks, OS_NT, 0, stream>>>(p);
+    k_os_setup<<<p.S * npass, OS_NT, 0, stream>>>(p);
+    note_launch(2);
     uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
     for (int pass = 0; pass < npass; ++pass) {
+      p.pass = pass;
       p.shift = 8 * pass;
       p.nbits = std::min(8, bits - 8 * pass);
       p.kin = ki; p.vin = vi; p.kout = ko; p.vout = vo;
-      p.hist = hist;
-      k_sort_up<<<(unsigned)p.total_chunks, SORT_NT, 0, stream>>>(p);
-      k_sort_scan<<<p.S, SCAN_NT, 0, stream>>>(p);
-      k_sort_down<<<(unsigned)p.total_chunks, SORT_NT, 0, stream>>>(p);
-      note_launch(3);
+      k_onesweep<<<(unsigned)std::min<int64_t>(os_grid(), p.total_tcap), OS_NT, 0, stream>>>(p);
+      note_launch();
       std::swap(ki, ko);
       std::swap(vi, vo);
     }

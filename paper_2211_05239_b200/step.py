@@ -10,6 +10,11 @@ no host synchronisation -- capturable as one CUDA graph:
     recd_expand      expansion of the pooled rows to [B, D] via inverse_lookup
     recd_pool_bwd    grad segment-reduce + sorted scatter-add + fused SGD
 
+With overlap=True (default) the backward is split: recd_pool_bwd_prepare
+(inverse CSR + occurrence sort, gradient-independent) runs on a side stream
+right after recd_dedup, concurrently with the pooled lookup and expansion,
+and recd_pool_bwd_finish joins on the main stream.
+
 This is the device-side equivalent of one `forward_iteration`'s sparse part
 (trainer_sim.py:484-574) plus the backward the reference does not have.
 """
@@ -38,7 +43,7 @@ class StepCounts:
 class TrainStep:
     def __init__(self, groups: Sequence[Sequence[str]], batch_size: int,
                  value_caps: dict[str, int], tables: dict[str, EmbeddingTable], op: str = "sum",
-                 lr: float = 0.01, mode: str = "dedup", device=None):
+                 lr: float = 0.01, mode: str = "dedup", device=None, overlap: bool = True):
         if mode not in ("dedup", "kjt"):
             raise ValueError(f"unknown mode {mode!r}")
         self.lib = _lib.load()
@@ -50,6 +55,7 @@ class TrainStep:
         self.op = op
         self.mode_id = _lib.POOL_MODES[op]
         self.lr = float(lr)
+        self.overlap = bool(overlap)
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         self.tables = [tables[k] for k in self.keys]
         self.D = self.tables[0].dim
@@ -155,21 +161,45 @@ class TrainStep:
                                   self.a_out, stream)
         _lib.check(rc, "recd_expand")
 
-    def backward(self, stream: int) -> None:
+    def _bwd_args(self, stream: int):
         inv = self.a_inverse_f if self.mode == "dedup" else None
-        rc = self.lib.recd_pool_bwd(self.F, self.B, self.D, self.mode_id, self.a_tables,
-                                    self.a_rows, self.a_feat_vals, self.a_feat_offs, self.a_caps,
-                                    self.counts.data_ptr(), inv, self.a_grad, C.c_float(self.lr),
-                                    1, None, None, None, self.bwd_scratch.data_ptr(),
-                                    self.bwd_scratch.numel(), stream)
-        _lib.check(rc, "recd_pool_bwd")
+        return (self.F, self.B, self.D, self.mode_id, self.a_tables, self.a_rows, self.a_feat_vals,
+                self.a_feat_offs, self.a_caps, self.counts.data_ptr(), inv, self.a_grad,
+                C.c_float(self.lr), 1, None, None, None, self.bwd_scratch.data_ptr(),
+                self.bwd_scratch.numel(), stream)
+
+    def backward(self, stream: int) -> None:
+        _lib.check(self.lib.recd_pool_bwd(*self._bwd_args(stream)), "recd_pool_bwd")
+
+    def backward_prepare(self, stream: int) -> None:
+        """Gradient-independent half of the backward (may run on a side stream)."""
+        _lib.check(self.lib.recd_pool_bwd_prepare(*self._bwd_args(stream)), "recd_pool_bwd_prepare")
+
+    def backward_finish(self, stream: int) -> None:
+        _lib.check(self.lib.recd_pool_bwd_finish(*self._bwd_args(stream)), "recd_pool_bwd_finish")
 
     def run(self, stream: int | None = None) -> None:
-        s = _lib.stream_ptr(self.dev) if stream is None else stream
-        self.dedup(s)
-        self.forward(s)
-        self.expand(s)
-        self.backward(s)
+        if stream is not None or not self.overlap:
+            s = _lib.stream_ptr(self.dev) if stream is None else stream
+            self.dedup(s)
+            self.forward(s)
+            self.expand(s)
+            self.backward(s)
+            return
+        main = torch.cuda.current_stream(self.dev)
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(self.dev)
+            self._ev_fork = torch.cuda.Event()
+            self._ev_join = torch.cuda.Event()
+        self.dedup(main.cuda_stream)
+        self._ev_fork.record(main)
+        self._side.wait_event(self._ev_fork)
+        self.backward_prepare(self._side.cuda_stream)
+        self._ev_join.record(self._side)
+        self.forward(main.cuda_stream)
+        self.expand(main.cuda_stream)
+        main.wait_event(self._ev_join)
+        self.backward_finish(main.cuda_stream)
 
     def capture(self) -> None:
         """Record run() into a CUDA graph (replayed by replay())."""

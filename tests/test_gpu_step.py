@@ -1,0 +1,94 @@
+"""TrainStep (the bench's step: dedup -> pooled lookup -> expand -> backward
+with fused SGD) against the oracle, eagerly and as a CUDA graph, with the
+backward's prepare half overlapped on a side stream and without.  Session
+batches from the restated reference generator give consecutive unique rows
+that share IDs (shifted history windows), which is what the scatter's
+sequential-prefix rows exploit; results must stay bit-exact."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+import paper_2211_05239_b200 as R  # noqa: E402
+from paper_2211_05239_b200.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
+                                           generate_clustered_batch)
+from paper_2211_05239_b200.step import TrainStep  # noqa: E402
+
+
+def _batch(b, lens, vocab, seed, mean=16.5, change=0.15):
+    specs = [FeatureSpec(f"k{i}", "user_sequence", float(L), vocab, change) for i, L in enumerate(lens)]
+    return generate_clustered_batch(SessionConfig(max(1, b // 8), SampleCountDist("geometric", mean), seed),
+                                    specs, b)
+
+
+def _oracle_step(batch, w0s, grads, lr):
+    """Per key: dedup, pooled sum + expand, backward, SGD on that key's table."""
+    outs, w1s = {}, {}
+    for k in batch.keys:
+        v, o = batch.values[k], batch.offsets[k]
+        inv, [(uv, uo)] = oracle.build_ikjt_arrays([(v, o)])
+        outs[k] = oracle.expand(oracle.pooled_lookup(uv, uo, w0s[k], "sum"), inv)
+        gu = oracle.pool_backward(grads[k], inv, uo.size)
+        ids, g = oracle.sparse_table_grad(gu, uv, uo, "sum")
+        w1 = w0s[k].copy()
+        w1[ids] = w0s[k][ids] - (np.float32(lr) * g).astype(np.float32)
+        w1s[k] = w1
+    return outs, w1s
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("graph", [True, False])
+def test_train_step_matches_oracle(overlap, graph):
+    b, vocab, dim, lr = 2048, 5000, 128, 0.05
+    batch = _batch(b, [4, 24, 64], vocab, seed=3)
+    keys = list(batch.keys)
+    rng = np.random.default_rng(0)
+    w0s = {k: rng.uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32) for k in keys}
+    tables = {k: R.EmbeddingTable(k, vocab, dim, torch.as_tensor(w0s[k], device="cuda").clone())
+              for k in keys}
+    caps = {k: int(batch.values[k].size) for k in keys}
+    step = TrainStep([[k] for k in keys], b, caps, tables, "sum", lr, "dedup", overlap=overlap)
+    step.load_batch(batch.values, batch.offsets)
+    grads = {k: rng.standard_normal((b, dim)).astype(np.float32) for k in keys}
+    for f, k in enumerate(keys):
+        step.grad_out[f].copy_(torch.as_tensor(grads[k]))
+    if graph:
+        # capture runs the step once (warm-up) before recording: restore the tables after
+        step.capture()
+        for k in keys:
+            tables[k].weights.copy_(torch.as_tensor(w0s[k]))
+        step.replay()
+    else:
+        step.run()
+    torch.cuda.synchronize()
+    outs, w1s = _oracle_step(batch, w0s, grads, lr)
+    for f, k in enumerate(keys):
+        np.testing.assert_array_equal(step.out[f].cpu().numpy(), outs[k])
+        np.testing.assert_array_equal(tables[k].weights.cpu().numpy(), w1s[k])
+
+
+def test_long_sessions_many_consecutive_rows():
+    """Fixed 64-sample sessions with frequent window shifts: runs of consecutive
+    unique rows far longer than the prefix rows cover."""
+    b, vocab, dim, lr = 4096, 20000, 64, 0.1
+    batch = _batch(b, [32, 128], vocab, seed=11, mean=64, change=0.6)
+    keys = list(batch.keys)
+    rng = np.random.default_rng(1)
+    w0s = {k: rng.uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32) for k in keys}
+    tables = {k: R.EmbeddingTable(k, vocab, dim, torch.as_tensor(w0s[k], device="cuda").clone())
+              for k in keys}
+    caps = {k: int(batch.values[k].size) for k in keys}
+    step = TrainStep([[k] for k in keys], b, caps, tables, "sum", lr, "dedup")
+    step.load_batch(batch.values, batch.offsets)
+    grads = {k: rng.standard_normal((b, dim)).astype(np.float32) for k in keys}
+    for f, k in enumerate(keys):
+        step.grad_out[f].copy_(torch.as_tensor(grads[k]))
+    step.run()
+    torch.cuda.synchronize()
+    _, w1s = _oracle_step(batch, w0s, grads, lr)
+    for k in keys:
+        np.testing.assert_array_equal(tables[k].weights.cpu().numpy(), w1s[k])

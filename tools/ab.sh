@@ -4,7 +4,7 @@ if [ -n "$1" ]; then timeout 900 python -m pytest tests -m gpu -x -q -k "$1" > g
 shift
 for v in "$@"; do
   if [ "$v" = "cur" ]; then lib=paper_2211_05239_b200/librecd.so; else lib=build/variants/librecd_$v.so; fi
-  RECD_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/var_$v.json 2> gpurun_out/var_$v.err
+  RECD_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e $BENCH_ARGS > gpurun_out/var_$v.json 2> gpurun_out/var_$v.err
   echo "$v rc=$?"
   python -c "
 import json,sys

@@ -6,11 +6,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
-    "ct16": ["RECD_SORT_CHUNK_TILES=16"],
-    "ct32": ["RECD_SORT_CHUNK_TILES=32"],
-    "it16ct4": ["RECD_SORT_ITEMS=16", "RECD_SORT_CHUNK_TILES=4"],
-    "it16ct8": ["RECD_SORT_ITEMS=16", "RECD_SORT_CHUNK_TILES=8"],
-    "it12ct8": ["RECD_SORT_ITEMS=12", "RECD_SORT_CHUNK_TILES=8"],
+    "scb4": ["RECD_SCATTER_MINB=4"],
+    "scrs4": ["RECD_SC_RS=4"],
+    "rk3": ["RECD_RING_K=3", "RECD_RING_MINB=2"],
+    "rk1": ["RECD_RING_K=1", "RECD_RING_MINB=4"],
+    "osb4": ["RECD_OS_MINB=4"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
