@@ -27,12 +27,16 @@
 #ifndef RECD_BWD_VW
 #define RECD_BWD_VW 4
 #endif
+#ifndef RECD_BWD_FULLOK
+#define RECD_BWD_FULLOK 1
+#endif
 #ifndef RECD_SCATTER_MINB
 #define RECD_SCATTER_MINB 3
 #endif
-// L2 policy of the scatter: 1 = table rows (read + write) evict_first, 0 = no hints
+// L2 policy of the scatter: 1 = table rows (read + write) evict_first, 2 = also
+// unique-row gradient gathers evict_last, 0 = no hints
 #ifndef RECD_SCATTER_L2
-#define RECD_SCATTER_L2 1
+#define RECD_SCATTER_L2 2
 #endif
 
 namespace recd {
@@ -270,6 +274,7 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   const bool apply = p.apply_sgd != 0;
   constexpr bool HINT = RECD_SCATTER_L2 > 0 && V == 4;
   const uint64_t pol_stream = HINT ? l2_evict_first() : 0;
+  const uint64_t pol_keep = (HINT && RECD_SCATTER_L2 >= 2) ? l2_evict_last() : 0;
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
     const int64_t chunk = (ncb == 1) ? w : w / ncb;
     const int lo_f = (int)(w - chunk * ncb) * C::CB + lane * V;  // this lane's first float
@@ -345,7 +350,18 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
         const uint32_t vv = win[k0 + t - wbase];
         const float* gp = SINGLE ? gs + (uint64_t)(vv & 0xffffffu) * D32
                                  : p.grow[vv >> 24] + lo_f + (uint64_t)(vv & 0xffffffu) * D32;
-        if (k0 + t < pe) C::ld(gp, ok, x[t]);
+        if (k0 + t < pe) {
+          if constexpr (HINT && RECD_SCATTER_L2 >= 2) {  // keep unique-row grads in L2
+            if (C::FULL || ok) {
+              const float4 q = ld_v4_hint(gp, pol_keep);
+              x[t][0] = q.x; x[t][1] = q.y; x[t][2] = q.z; x[t][3] = q.w;
+            } else {
+              C::zero(x[t]);
+            }
+          } else {
+            C::ld(gp, ok, x[t]);
+          }
+        }
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
@@ -656,7 +672,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   // ---- finish: gradient-dependent work
   if (do_scatter && !apply_sgd)
     RECD_CUDA_CHECK(cudaMemsetAsync(grad_counts_out, 0, sizeof(int64_t) * F, stream));
-  int rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, 0, {
+  int rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, RECD_BWD_FULLOK, {
     const int ncb = col_blocks<C>(dim);
     // 2. unique-row gradients
     if (do_grad) {

@@ -118,6 +118,28 @@ __global__ void __launch_bounds__(256) k_bulk(const float4* __restrict__ t, uint
   if (acc.x == 1234.5f) out[0] = acc.y + acc.z + acc.w;
 }
 
+// random row read-modify-write (the scatter's table update): U rows in flight
+template <int U>
+__global__ void __launch_bounds__(256) k_rmw(float4* __restrict__ t, uint64_t rows, int64_t per_warp,
+                                             uint64_t seed, float* out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  for (int64_t i = 0; i < per_warp; i += U) {
+    float4 x[U];
+    uint64_t r[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      r[k] = rowof(w, i + k, seed, rows);
+      x[k] = t[r[k] * 32 + lane];
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      x[k].x += 1.f;
+      t[r[k] * 32 + lane] = x[k];
+    }
+  }
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -133,6 +155,20 @@ int main() {
   const int blocks = sms * 8;
   const int64_t per_warp = 4096;
   const double bytes = (double)blocks * 8 * per_warp * 512;
+  auto run_rmw = [&](const char* name, auto kern, uint64_t rows) {
+    float best = 1e30f;
+    for (int it = 0; it < 4; ++it) {
+      cudaEventRecord(e0);
+      kern<<<blocks, 256>>>(t, rows, per_warp / 4, 777 + it, out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (it) best = ms < best ? ms : best;
+    }
+    printf("%8llu MB %-10s %8.0f GB/s (read+write)  %s\n", (unsigned long long)(rows * 512 >> 20), name,
+           2 * bytes / 4 / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+  };
   auto run = [&](const char* name, auto kern, int smem, uint64_t rows) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     float best = 1e30f;
@@ -150,6 +186,8 @@ int main() {
   };
   for (uint64_t mb : {64ull, 1024ull, 8192ull, 32768ull}) {
     const uint64_t rows = (mb << 20) / 512;
+    run_rmw("rmw4", k_rmw<4>, rows);
+    run_rmw("rmw8", k_rmw<8>, rows);
     run("reg8", k_reg<8>, 0, rows);
     run("reg16", k_reg<16>, 0, rows);
     run("ldgsts2", k_ldgsts<2>, 8 * 2 * 8 * 512, rows);
