@@ -182,6 +182,29 @@ int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, int32_t dim, 
                          float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
                          size_t scratch_bytes, recd_stream_t stream);
 
+/* ------------------------------------------------- sequence encoder --
+ * <- trainer_sim.attention_pool (trainer_sim.py:347-391), config 4, over the
+ * unique rows of one dedup group: per unique row u the tokens are the rows'
+ * lists of every feature concatenated (embedding rows of tables[f]);
+ *   out[u] = mean_i softmax(q k^T / sqrt(dim))_i v @ w_o,  q|k|v = x W_{q|k|v},
+ * empty rows -> 0.  QKV on the tcgen05 tensor cores (BF16 in, FP32 accumulate).
+ *   w_qkv_t  device bf16 [3*dim][dim] = [W_q | W_k | W_v]^T (K-major)
+ *   w_o      device fp32 [dim][dim]
+ *   counts   device [2F]: U (all equal) then N_u per feature
+ *   out      device fp32 [>= U][dim];  err as in recd_pool_fwd.  dim: 64 or 128. */
+size_t recd_attention_pool_scratch_bytes(int32_t num_features, int32_t dim,
+                                         const int64_t* value_caps);
+int recd_attention_pool(int32_t num_features, int64_t batch_size, int32_t dim,
+                        const float* const* tables, const int64_t* table_rows,
+                        const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                        const int64_t* value_caps, const int64_t* counts, const void* w_qkv_t,
+                        const float* w_o, float* out, int64_t* err, void* scratch,
+                        size_t scratch_bytes, recd_stream_t stream);
+/* C[m][:] = A[m][:] B^T (bf16 row-major, FP32 accumulate in TMEM), M = *m_count
+ * rows (device), (n, k) in {(192, 64), (384, 128), (128, 128)}. */
+int recd_gemm_bf16_tn(int32_t n, int32_t k, const void* a, const void* b, void* c,
+                      const int64_t* m_count, recd_stream_t stream);
+
 /* Source half: grad_u_out[f] ([U x dim]) = grad_u of recd_pool_bwd (avg scaled). */
 size_t recd_grad_unique_scratch_bytes(int32_t num_features, int64_t batch_size);
 int recd_grad_unique(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,

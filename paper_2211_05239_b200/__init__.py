@@ -31,6 +31,7 @@ from .embedding import (  # noqa: F401
     pooled_lookup,
     pooled_lookup_backward,
 )
+from .encoder import DedupAttentionPool, attention_pool_macs  # noqa: F401
 from ._lib import launch_count, lib_path, load as load_library  # noqa: F401
 
 __version__ = "0.1.0"

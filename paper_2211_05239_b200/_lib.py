@@ -52,6 +52,10 @@ _SIGS = {
                                      _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_pool_bwd_finish": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp,
                                     _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_attention_pool_scratch_bytes": (_sz, [_i32, _i32, _p64]),
+    "recd_attention_pool": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _vp, _vp, _vp,
+                                   _vp, _vp, _sz, _vp]),
+    "recd_gemm_bf16_tn": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "recd_grad_unique_scratch_bytes": (_sz, [_i32, _i64]),
     "recd_grad_unique": (_i32, [_i32, _i64, _i32, _i32, _pp, _vp, _pp, _pp, _pp, _vp, _sz, _vp]),
     "recd_sparse_sgd_scratch_bytes": (_sz, [_i32, _p64]),
