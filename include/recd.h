@@ -64,6 +64,7 @@ enum {
 };
 
 enum { RECD_POOL_SUM = 0, RECD_POOL_AVG = 1, RECD_POOL_MAX = 2 };
+enum { RECD_XF_IDENTITY = 0, RECD_XF_MOD_HASH = 1, RECD_XF_CLAMP = 2 };
 
 /* Value of an error slot when no error occurred. */
 #define RECD_NO_ERROR ((int64_t)0x7f7f7f7f7f7f7f7fLL)
@@ -181,6 +182,17 @@ int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, int32_t dim, 
                          int32_t apply_sgd, int64_t* const* grad_ids_out,
                          float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
                          size_t scratch_bytes, recd_stream_t stream);
+
+/* ------------------------------------------------------- transforms --
+ * <- reader.apply_transform (reader.py:69-83) as used by reader.process
+ * (reader.py:178-217) on IKJT unique values: per feature f,
+ *   out[f][j] = identity | splitmix64(in[f][j]) mod params[f] | clamp(in, 0, params[f])
+ * for j < min(*device_counts[f], num_values[f]) (device_counts may be NULL or
+ * hold NULL entries: num_values[f] elements).  In-place allowed (out == in). */
+int recd_transform(int32_t num_features, const int64_t* const* values_in,
+                   int64_t* const* values_out, const int64_t* num_values,
+                   const int64_t* const* device_counts, const int32_t* ops, const int64_t* params,
+                   recd_stream_t stream);
 
 /* ------------------------------------------------- sequence encoder --
  * <- trainer_sim.attention_pool (trainer_sim.py:347-391), config 4, over the

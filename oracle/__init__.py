@@ -38,3 +38,4 @@ from .embedding import (  # noqa: F401
     sgd_apply,
     attention_pool,
 )
+from .reader import apply_transform, splitmix64  # noqa: F401,E402

@@ -52,6 +52,7 @@ _SIGS = {
                                      _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_pool_bwd_finish": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp,
                                     _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_transform": (_i32, [_i32, _pp, _pp, _p64, _pp, _p32, _p64, _vp]),
     "recd_attention_pool_scratch_bytes": (_sz, [_i32, _i32, _p64]),
     "recd_attention_pool": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _vp, _vp, _vp,
                                    _vp, _vp, _sz, _vp]),

@@ -24,6 +24,7 @@ sys.path.insert(0, REF)
 from sessiondedup import tensors as T  # noqa: E402
 from sessiondedup import trainer_sim as TS  # noqa: E402
 from sessiondedup import datagen as DG  # noqa: E402
+from sessiondedup import reader as RD  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 
@@ -232,7 +233,29 @@ def make_errors():
     np.savez_compressed(OUT / "errors.npz", json=np.array([json.dumps(msgs)]))
 
 
+def make_transforms():
+    """reader.apply_transform (reader.py:69-81) on edge and random int64 IDs,
+    and reader.process on an IKJT: transformed dedup values, expanded, equal
+    the transformed KJT (test_reader.py:176-187)."""
+    rng = np.random.default_rng(11)
+    v = np.concatenate([
+        np.array([0, 1, -1, 2**63 - 1, -2**63, 12345678901234, 10_000_000, 9_999_999], np.int64),
+        rng.integers(-2**63, 2**63 - 1, size=2000, dtype=np.int64),
+        rng.integers(0, 10_000_000, size=2000, dtype=np.int64)])
+    store = {"values": v}
+    cases = [("identity", None), ("mod_hash", 1), ("mod_hash", 1000), ("mod_hash", 10_000_000),
+             ("mod_hash", 2**62 + 7), ("clamp", 1), ("clamp", 5_000_000), ("clamp", 2**62)]
+    for i, (op, param) in enumerate(cases):
+        t = RD.Transform(op=op, key="k", param=param)
+        store[f"c{i}/op"] = np.array([op])
+        store[f"c{i}/param"] = np.array([param if param is not None else 0], np.int64)
+        store[f"c{i}/out"] = np.asarray(RD.apply_transform(v, t), dtype=np.int64)
+    store["ncases"] = np.array([len(cases)])
+    np.savez_compressed(OUT / "transforms.npz", **store)
+
+
 if __name__ == "__main__":
+    make_transforms()
     make_dedup()
     make_datagen()
     make_pool()

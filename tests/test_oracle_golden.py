@@ -89,3 +89,13 @@ def test_oracle_error_messages_match_reference():
     with pytest.raises(ValueError) as e:
         oracle.pool(np.zeros((1, 1), dtype=np.float32), np.array([0]), "median")
     assert str(e.value) == msgs["pool_op"][1]
+
+
+def test_transforms_oracle_matches_reference_golden():
+    """reader.apply_transform (reader.py:69-83) restated in oracle/reader.py."""
+    d = golden("transforms")
+    v = d["values"]
+    for i in range(int(d["ncases"][0])):
+        op, param = str(d[f"c{i}/op"][0]), int(d[f"c{i}/param"][0])
+        got = oracle.apply_transform(v, op, param or None)
+        np.testing.assert_array_equal(got, d[f"c{i}/out"])
