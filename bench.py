@@ -524,9 +524,10 @@ def run_sharded(args, world, rank, local, dev):
                                                  seed=1000 * keys.index(k) + j, device=dev)
 
     caps = {k: batch.values[k].size for k in keys}
+    peer_kw = {"overlap": not args.no_overlap} if args.transport == "peer" else {}
     cls = PeerShardedStep if args.transport == "peer" else ShardedTrainStep
     step = cls(keys, args.batch, caps, {k: args.rows for k in keys}, args.dim, make_table, "sum",
-               args.lr, shards=S, device=dev)
+               args.lr, shards=S, device=dev, **peer_kw)
     peer = args.transport == "peer"
     lrows = sum(t.rows for t in step.tables.values())
     step.load_batch(batch.values, batch.offsets)

@@ -194,6 +194,23 @@ int recd_transform(int32_t num_features, const int64_t* const* values_in,
                    const int64_t* const* device_counts, const int32_t* ops, const int64_t* params,
                    recd_stream_t stream);
 
+/* ------------------------------------------------------- wire format --
+ * <- tensors._serialize / serialize_kjt / serialize_ikjt (tensors.py:463-505):
+ * the canonical little-endian byte stream written into a device buffer
+ * (8-byte aligned).  inverse = NULL for a KJT (flag 0).  Element counts of
+ * each key's offsets / values come from device_counts when given (IKJT: U and
+ * N_u live on the device), else from the host caps.  *total_out (device) =
+ * bytes written, or -1 when out_cap is too small (nothing written).
+ * recd_wire_bound gives a host upper bound; scratch >= 2 KB. */
+int64_t recd_wire_bound(int32_t num_keys, const char* const* key_names, int64_t batch_size,
+                        int32_t has_inverse, const int64_t* offsets_caps, const int64_t* values_caps);
+int recd_wire_serialize(int32_t num_keys, const char* const* key_names, int64_t batch_size,
+                        const int64_t* inverse, const int64_t* const* offsets,
+                        const int64_t* const* values, const int64_t* const* offsets_counts,
+                        const int64_t* const* values_counts, const int64_t* offsets_caps,
+                        const int64_t* values_caps, void* out, int64_t out_cap, int64_t* total_out,
+                        void* scratch, size_t scratch_bytes, recd_stream_t stream);
+
 /* ------------------------------------------------- sequence encoder --
  * <- trainer_sim.attention_pool (trainer_sim.py:347-391), config 4, over the
  * unique rows of one dedup group: per unique row u the tokens are the rows'
@@ -236,6 +253,23 @@ int recd_sparse_sgd(int32_t num_features, int64_t max_rows, int32_t dim, float* 
                     int32_t apply_sgd, int64_t* const* grad_ids_out, float* const* grad_rows_out,
                     int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
                     recd_stream_t stream);
+/* recd_sparse_sgd in two halves (same arguments, same scratch): _prepare sorts
+ * the occurrences by ID (needs only uvalues/uoffsets/counts), _finish reduces
+ * grad_rows and applies the update. */
+int recd_sparse_sgd_prepare(int32_t num_features, int64_t max_rows, int32_t dim, float* const* tables,
+                            const int64_t* table_rows, const int64_t* const* uvalues,
+                            const int64_t* const* uoffsets, const int64_t* value_caps,
+                            const int64_t* counts, const float* const* grad_rows, float lr,
+                            int32_t apply_sgd, int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                            int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                            recd_stream_t stream);
+int recd_sparse_sgd_finish(int32_t num_features, int64_t max_rows, int32_t dim, float* const* tables,
+                           const int64_t* table_rows, const int64_t* const* uvalues,
+                           const int64_t* const* uoffsets, const int64_t* value_caps,
+                           const int64_t* counts, const float* const* grad_rows, float lr,
+                           int32_t apply_sgd, int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                           int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                           recd_stream_t stream);
 
 /* ------------------------------------------------------- row sharding --
  * Every table is split into S row shards: shard(id) = id mod S, local row =

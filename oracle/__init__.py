@@ -39,3 +39,4 @@ from .embedding import (  # noqa: F401
     attention_pool,
 )
 from .reader import apply_transform, splitmix64  # noqa: F401,E402
+from . import wire  # noqa: F401,E402

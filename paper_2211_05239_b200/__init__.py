@@ -31,6 +31,7 @@ from .embedding import (  # noqa: F401
     pooled_lookup,
     pooled_lookup_backward,
 )
+from .wire import serialize_ikjt, serialize_kjt, slice_stream_bytes, values_stream_bytes  # noqa: F401
 from .encoder import DedupAttentionPool, attention_pool_macs  # noqa: F401
 from ._lib import launch_count, lib_path, load as load_library  # noqa: F401
 

@@ -52,6 +52,9 @@ _SIGS = {
                                      _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_pool_bwd_finish": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp,
                                     _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_wire_bound": (_i64, [_i32, C.POINTER(C.c_char_p), _i64, _i32, _p64, _p64]),
+    "recd_wire_serialize": (_i32, [_i32, C.POINTER(C.c_char_p), _i64, _vp, _pp, _pp, _pp, _pp, _p64,
+                                   _p64, _vp, _i64, _vp, _vp, _sz, _vp]),
     "recd_transform": (_i32, [_i32, _pp, _pp, _p64, _pp, _p32, _p64, _vp]),
     "recd_attention_pool_scratch_bytes": (_sz, [_i32, _i32, _p64]),
     "recd_attention_pool": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _vp, _vp, _vp,
@@ -61,6 +64,10 @@ _SIGS = {
     "recd_grad_unique": (_i32, [_i32, _i64, _i32, _i32, _pp, _vp, _pp, _pp, _pp, _vp, _sz, _vp]),
     "recd_sparse_sgd_scratch_bytes": (_sz, [_i32, _p64]),
     "recd_sparse_sgd": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _f32, _i32,
+                               _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_sparse_sgd_prepare": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _f32, _i32,
+                               _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_sparse_sgd_finish": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _f32, _i32,
                                _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_shard_count_scratch_bytes": (_sz, [_i32, _i32, _i64]),
     "recd_shard_count": (_i32, [_i32, _i32, _i64, _pp, _pp, _vp, _pp, _vp, _vp, _sz, _vp]),

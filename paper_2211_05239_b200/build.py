@@ -77,6 +77,21 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: Path | No
     return lib
 
 
+def build_host(force: bool = False) -> Path:
+    """Compile the native host-side packer (CPython C API, g++)."""
+    import sysconfig
+    src = CSRC / "host" / "recd_hostpack.cpp"
+    out = PKG / ("_hostpack" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if force or _stale(out, [src]):
+        cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-shared", "-fPIC",
+               f"-I{sysconfig.get_paths()['include']}", str(src), "-o", str(out)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return out
+
+
 if __name__ == "__main__":
+    build_host(force="--force" in sys.argv)
     lib = build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(lib)

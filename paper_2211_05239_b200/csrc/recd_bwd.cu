@@ -816,3 +816,34 @@ extern "C" int recd_sparse_sgd(int32_t num_features, int64_t max_rows, int32_t d
                  grad_rows, lr, apply_sgd, grad_ids_out, grad_rows_out, grad_counts_out, scratch,
                  scratch_bytes, (cudaStream_t)stream);
 }
+
+// Split form of recd_sparse_sgd (same arguments, same scratch): _prepare
+// (occurrence pairs + sort by ID) needs only the owner's ID lists and can run
+// while the unique-row gradients are still being produced / pushed.
+extern "C" int recd_sparse_sgd_prepare(int32_t num_features, int64_t max_rows, int32_t dim,
+                               float* const* tables, const int64_t* table_rows,
+                               const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                               const int64_t* value_caps, const int64_t* counts,
+                               const float* const* grad_rows, float lr, int32_t apply_sgd,
+                               int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                               int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                               recd_stream_t stream) {
+  return run_bwd(BwdMode::ScatterOnly, num_features, max_rows, dim, RECD_POOL_SUM, tables,
+                 table_rows, uvalues, uoffsets, value_caps, counts, nullptr, nullptr, nullptr,
+                 grad_rows, lr, apply_sgd, grad_ids_out, grad_rows_out, grad_counts_out, scratch,
+                 scratch_bytes, (cudaStream_t)stream, PH_PREP);
+}
+
+extern "C" int recd_sparse_sgd_finish(int32_t num_features, int64_t max_rows, int32_t dim,
+                               float* const* tables, const int64_t* table_rows,
+                               const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                               const int64_t* value_caps, const int64_t* counts,
+                               const float* const* grad_rows, float lr, int32_t apply_sgd,
+                               int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                               int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                               recd_stream_t stream) {
+  return run_bwd(BwdMode::ScatterOnly, num_features, max_rows, dim, RECD_POOL_SUM, tables,
+                 table_rows, uvalues, uoffsets, value_caps, counts, nullptr, nullptr, nullptr,
+                 grad_rows, lr, apply_sgd, grad_ids_out, grad_rows_out, grad_counts_out, scratch,
+                 scratch_bytes, (cudaStream_t)stream, PH_FINISH);
+}

@@ -16,7 +16,9 @@ other rank's exchange buffers (CUDA IPC over NVLink / NVSwitch) and
   recd_shard_combine   source: shard-order sum + avg, then recd_expand
   recd_grad_unique     source: gradient of every unique row
   recd_peer_copy_rows  source -> owners: unique-row gradients
-  recd_sparse_sgd      owner: deterministic sorted scatter-add + SGD
+  recd_sparse_sgd      owner: deterministic sorted scatter-add + SGD (its
+                       _prepare half -- the occurrence sort -- runs on a side
+                       stream from the end of the dispatch, overlapping the rest)
 
 Every size lives on the device, so the whole forward + backward is captured
 once into a CUDA graph and replayed; exchanges are bounded-time barriers (a
@@ -64,8 +66,9 @@ class PeerShardedStep:
                  table_rows: dict[str, int], dim: int,
                  make_table: Callable[[str, int, int], EmbeddingTable], op: str = "sum",
                  lr: float = 0.01, shards: int | None = None, group=None, device=None,
-                 timeout_s: float = 10.0):
+                 timeout_s: float = 10.0, overlap: bool = True):
         self.lib = L = _lib.load()
+        self.overlap = bool(overlap)
         self.group = group
         self.R = R = dist.get_world_size(group)
         self.rank = rank = dist.get_rank(group)
@@ -84,6 +87,8 @@ class PeerShardedStep:
         self.op, self.mode_id, self.lr = op, _lib.POOL_MODES[op], float(lr)
         self.timeout_ns = int(timeout_s * 1e9)
         self.dev = dev = device or torch.device("cuda", torch.cuda.current_device())
+        self._side = torch.cuda.Stream(dev)       # owner-side occurrence sort (overlap)
+        self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
         i64, f32 = torch.int64, torch.float32
         self.caps = [max(int(value_caps[k]), 1) for k in self.keys]
         mine_caps = torch.tensor(self.caps, dtype=i64, device=dev)
@@ -321,6 +326,15 @@ class PeerShardedStep:
         _lib.check(rc, "recd_shard_dispatch")
         self._exchange(s, False)
         self._mark("dispatch_ids")
+        if Q and self.overlap:
+            # the owner's ID lists are complete: sort the occurrences by ID on a
+            # side stream while the forward, grad_unique and the push run
+            main = torch.cuda.current_stream(self.dev)
+            self._ev_fork.record(main)
+            self._side.wait_event(self._ev_fork)
+            _lib.check(L.recd_sparse_sgd_prepare(*self._sgd_args(self._side.cuda_stream)),
+                       "recd_sparse_sgd_prepare")
+            self._ev_join.record(self._side)
         if Q:
             rc = L.recd_pool_fwd(Q, R * B, D, _lib.POOL_MODES["sum"], self.a_tables, self.a_rows,
                                  self.a_own_ids, self.a_own_ro, self.own_counts_ptr, None,
@@ -352,13 +366,17 @@ class PeerShardedStep:
                    "recd_peer_copy_rows")
         self._exchange(s, False)
         self._mark("push_grads")
-        if Q:
-            rc = L.recd_sparse_sgd(Q, R * B, D, self.a_tables, self.a_rows, self.a_own_ids,
-                                   self.a_own_ro, self.a_capid, self.own_counts_ptr,
-                                   self.a_own_grad, C.c_float(self.lr), 1, None, None, None,
-                                   self.s_sgd.data_ptr(), self.s_sgd.numel(), s)
-            _lib.check(rc, "recd_sparse_sgd")
+        if Q and self.overlap:
+            torch.cuda.current_stream(self.dev).wait_event(self._ev_join)
+            _lib.check(L.recd_sparse_sgd_finish(*self._sgd_args(s)), "recd_sparse_sgd_finish")
+        elif Q:
+            _lib.check(L.recd_sparse_sgd(*self._sgd_args(s)), "recd_sparse_sgd")
         self._mark("owner_sgd")
+
+    def _sgd_args(self, s):
+        return (self.Q, self.R * self.B, self.D, self.a_tables, self.a_rows, self.a_own_ids,
+                self.a_own_ro, self.a_capid, self.own_counts_ptr, self.a_own_grad,
+                C.c_float(self.lr), 1, None, None, None, self.s_sgd.data_ptr(), self.s_sgd.numel(), s)
 
     def run(self):
         self.forward()

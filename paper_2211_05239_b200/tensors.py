@@ -224,15 +224,19 @@ def _pack_rows(arrs: Sequence[np.ndarray]) -> tuple[np.ndarray, np.ndarray]:
 
 
 def build_kjt(rows: Sequence, keys: Sequence[str], device=None) -> KJT:
-    """Records -> KJT on the GPU, preserving batch order (tensors.py:246-254)."""
+    """Records -> KJT on the GPU, preserving batch order (tensors.py:246-254).
+    The records are walked once in native code (`_hostpack.pack_rows`,
+    csrc/host/recd_hostpack.cpp) instead of one np.asarray per list."""
     if len(rows) == 0:
         raise ValueError("empty batch")
+    from . import _hostpack  # built by build.build_host(); no Python fallback
     dev = device or default_device()
+    packed = _hostpack.pack_rows(rows, list(keys))
     entries = {}
-    for key in keys:
-        v, o = _pack_rows([_feature_list(r, key) for r in rows])
-        entries[key] = JaggedTensor._trusted(torch.from_numpy(v).to(dev, non_blocking=True),
-                                             torch.from_numpy(o).to(dev, non_blocking=True))
+    for key, (vb, ob) in zip(keys, packed):
+        v = torch.frombuffer(bytearray(vb), dtype=torch.int64) if vb else torch.empty(0, dtype=torch.int64)
+        o = torch.frombuffer(bytearray(ob), dtype=torch.int64)
+        entries[key] = JaggedTensor._trusted(v.to(dev, non_blocking=True), o.to(dev, non_blocking=True))
     return KJT(len(rows), entries)
 
 

@@ -254,7 +254,36 @@ def make_transforms():
     np.savez_compressed(OUT / "transforms.npz", **store)
 
 
+def make_wire():
+    """Canonical wire format (tensors.py:463-515) of KJTs and IKJTs built by the
+    real reference: serialize_kjt / serialize_ikjt bytes + slice byte counts."""
+    rng = np.random.default_rng(13)
+    store = {}
+    cases = []
+    for ci, (b, keys, dup) in enumerate([(1, ["a"], 0.0), (7, ["user_hist", "x"], 0.7),
+                                         (300, ["k0", "k1", "k_\u00e9"], 0.85), (64, ["e"], 0.5)]):
+        rows = session_rows(rng, b, keys, dup, 12, 1 << 40)
+        if ci == 3:  # rows with only empty lists
+            rows = [{"e": []} for _ in range(b)]
+        kjt = T.build_kjt(rows, keys)
+        ik = T.build_ikjt(rows, keys)
+        name = f"w{ci}"
+        store[f"{name}/kjt_bytes"] = np.frombuffer(T.serialize_kjt(kjt), np.uint8)
+        store[f"{name}/ikjt_bytes"] = np.frombuffer(T.serialize_ikjt(ik), np.uint8)
+        store[f"{name}/keys"] = np.array(keys)
+        store[f"{name}/slice_bytes"] = np.array([T.slice_stream_bytes(ik.per_feature[k]) for k in keys], np.int64)
+        store[f"{name}/values_bytes"] = np.array([T.values_stream_bytes(ik.per_feature[k]) for k in keys],
+                                                 np.int64)
+        for k in keys:
+            store[f"{name}/in_{k}_values"] = kjt.entries[k].values
+            store[f"{name}/in_{k}_offsets"] = kjt.entries[k].offsets
+        cases.append(name)
+    store["names"] = np.array(cases)
+    np.savez_compressed(OUT / "wire.npz", **store)
+
+
 if __name__ == "__main__":
+    make_wire()
     make_transforms()
     make_dedup()
     make_datagen()

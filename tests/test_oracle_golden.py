@@ -99,3 +99,20 @@ def test_transforms_oracle_matches_reference_golden():
         op, param = str(d[f"c{i}/op"][0]), int(d[f"c{i}/param"][0])
         got = oracle.apply_transform(v, op, param or None)
         np.testing.assert_array_equal(got, d[f"c{i}/out"])
+
+
+def test_wire_oracle_matches_reference_golden():
+    """tensors.serialize_kjt / serialize_ikjt (tensors.py:463-515) restated in oracle/wire.py."""
+    d = golden("wire")
+    for name in d["names"]:
+        name = str(name)
+        keys = [str(k) for k in d[f"{name}/keys"]]
+        feats = [(d[f"{name}/in_{k}_values"], d[f"{name}/in_{k}_offsets"]) for k in keys]
+        B = feats[0][1].size
+        kjt = oracle.wire.serialize(keys, B, None, [o for _, o in feats], [v for v, _ in feats])
+        assert kjt == d[f"{name}/kjt_bytes"].tobytes()
+        inv, outs = oracle.build_ikjt_arrays(feats)
+        ik = oracle.wire.serialize(keys, B, inv, [o for _, o in outs], [v for v, _ in outs])
+        assert ik == d[f"{name}/ikjt_bytes"].tobytes()
+        assert [oracle.wire.slice_stream_bytes(o, v) for v, o in outs] == list(d[f"{name}/slice_bytes"])
+        assert [oracle.wire.values_stream_bytes(v) for v, _ in outs] == list(d[f"{name}/values_bytes"])
