@@ -6,9 +6,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
-    "l2keep": ["RECD_SCATTER_L2=2"],
-    "full": ["RECD_BWD_FULLOK=1"],
-    "l2full": ["RECD_SCATTER_L2=2", "RECD_BWD_FULLOK=1"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
