@@ -34,6 +34,8 @@ struct CountParams {
   const int64_t* uoffsets[RECD_MAX_FEAT];
   const int64_t* counts;                // [2F] device
   int64_t* rowcnt[RECD_MAX_FEAT];       // [S][B] IDs per (shard, unique row)
+  int64_t* rowoff1[RECD_MAX_FEAT];      // S == 1: row offsets written directly
+  int64_t* totals1;                     // S == 1: [F] IDs per feature
 };
 
 // Scatter of the unique IDs into per-(table, shard) pair lists.  Pair p =
@@ -144,6 +146,38 @@ __global__ void __launch_bounds__(256) k_shard_scatter(const __grid_constant__ D
   }
 }
 
+
+// S == 1 (whole tables per owner, the cfg5 placement): every ID of a feature
+// goes to one pair and keeps its position, so the per-row counts are the row
+// lengths, the row offsets are the unique offsets and the dispatch is a flat,
+// coalesced copy -- no per-row warp work.
+__global__ void __launch_bounds__(256) k_shard_count1(const __grid_constant__ CountParams p) {
+  const int f = blockIdx.y;
+  const int64_t U = p.counts[f], N = p.counts[p.F + f];
+  const int64_t* uo = p.uoffsets[f];
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < U;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = uo[u];
+    p.rowoff1[f][u] = a;
+    if (p.rowcnt[f]) p.rowcnt[f][u] = ((u + 1 < U) ? uo[u + 1] : N) - a;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.totals1[f] = N;
+}
+
+__global__ void __launch_bounds__(256) k_shard_scatter1(const __grid_constant__ DispatchParams p) {
+  const int f = blockIdx.y;
+  const int64_t U = p.counts[f], N = p.counts[p.F + f];
+  const int64_t base = p.id_base ? p.id_base[f] : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t* src = p.uvalues[f];
+  int64_t* dst = p.dst_ids[f] + base;
+  for (int64_t j = t0; j < N; j += stride) dst[j] = __ldg(src + j);
+  if (p.dst_ro[f]) {
+    int64_t* ro = p.dst_ro[f] + (p.row_base ? p.row_base[f] : 0);
+    for (int64_t u = t0; u < U; u += stride) ro[u] = base + p.rowoff[f][u];
+  }
+}
 
 struct CombineParams {
   int F;
@@ -256,6 +290,19 @@ static int shard_count(int F, int S, int64_t batch_size, const int64_t* const* u
                     batch_size, counts + f, totals_out + (int64_t)f * S + o});
   }
   int64_t* part = a.take<int64_t>(scan_part_words(sd.data(), (int)sd.size()));
+  if (S == 1) {
+    for (int f = 0; f < F; ++f) {
+      if (!rowcnt_out) p.rowcnt[f] = nullptr;
+      p.rowoff1[f] = rowoff_out[f];
+    }
+    p.totals1 = totals_out;
+    const unsigned gx =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(batch_size, 256), 512));
+    k_shard_count1<<<dim3(gx, F), 256, 0, stream>>>(p);
+    note_launch();
+    RECD_LAUNCH_CHECK();
+    return RECD_OK;
+  }
   k_shard_count<<<shard_grid(batch_size, F), 256, 0, stream>>>(p);
   note_launch();
   rc = seg_exclusive_scan(sd.data(), (int)sd.size(), part, stream);
@@ -304,7 +351,14 @@ extern "C" int recd_shard_dispatch(int32_t num_features, int32_t num_shards, int
     p.dst_ids[i] = dst_ids[i];
     p.dst_ro[i] = dst_rowoffs ? dst_rowoffs[i] : nullptr;
   }
-  k_shard_scatter<<<shard_grid(batch_size, F), 256, 0, stream>>>(p);
+  if (S == 1) {
+    int64_t vmax = batch_size;
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(vmax * 8, 256),
+                                                                        (int64_t)num_sms() * 4));
+    k_shard_scatter1<<<dim3(gx, F), 256, 0, stream>>>(p);
+  } else {
+    k_shard_scatter<<<shard_grid(batch_size, F), 256, 0, stream>>>(p);
+  }
   note_launch();
   RECD_LAUNCH_CHECK();
   return RECD_OK;
