@@ -176,9 +176,22 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
         }
       }
       int64_t pv[RS_IT];
+      const int64_t pq0 = q0 - (int64_t)s_len[max(jk[0], 0)];
+      if (a16 && jk[0] >= 0 && jk[0] == jk[RS_IT - 1] && pq0 >= 0 && (pq0 & 1) == 0) {
+        // all 8 values in one row of even length: the predecessor's 8 values
+        // are contiguous and 16-byte aligned -> 4 vector loads instead of 8
+        const longlong2* src = reinterpret_cast<const longlong2*>(val + pq0);
 #pragma unroll
-      for (int k = 0; k < RS_IT; ++k)
-        pv[k] = (jk[k] >= 0) ? __ldg(val + max(q0 + k - (int64_t)s_len[jk[k]], (int64_t)0)) : 0;
+        for (int k = 0; k < RS_IT / 2; ++k) {
+          const longlong2 t = __ldg(src + k);
+          pv[2 * k] = t.x;
+          pv[2 * k + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < RS_IT; ++k)
+          pv[k] = (jk[k] >= 0) ? __ldg(val + max(q0 + k - (int64_t)s_len[jk[k]], (int64_t)0)) : 0;
+      }
 #pragma unroll
       for (int k = 0; k < RS_IT; ++k)
         if (jk[k] >= 0 && pv[k] != v[k]) s_mism[jk[k]] = 1u;

@@ -346,10 +346,14 @@ class PeerShardedStep:
                    "recd_peer_copy_rows")
         self._exchange(s, False)
         self._mark("return_partials")
-        rc = L.recd_shard_combine(F, S, B, D, self.mode_id, self.a_blocks, self.a_uoffsets,
-                                  self.counts.data_ptr(), self.a_pooled, s)
-        _lib.check(rc, "recd_shard_combine")
-        rc = L.recd_expand(F, B, D, self.a_inverse, self.a_pooled, self.a_out, s)
+        if S == 1 and self.mode_id == _lib.POOL_MODES["sum"]:
+            # one shard per table: the owner's partial row IS the pooled row
+            rc = L.recd_expand(F, B, D, self.a_inverse, self.a_blocks, self.a_out, s)
+        else:
+            rc = L.recd_shard_combine(F, S, B, D, self.mode_id, self.a_blocks, self.a_uoffsets,
+                                      self.counts.data_ptr(), self.a_pooled, s)
+            _lib.check(rc, "recd_shard_combine")
+            rc = L.recd_expand(F, B, D, self.a_inverse, self.a_pooled, self.a_out, s)
         _lib.check(rc, "recd_expand")
         self._mark("combine_expand")
 
