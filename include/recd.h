@@ -234,6 +234,16 @@ int recd_attention_pool(int32_t num_features, int64_t batch_size, int32_t dim,
 int recd_gemm_bf16_tn(int32_t n, int32_t k, const void* a, const void* b, void* c,
                       const int64_t* m_count, recd_stream_t stream);
 
+/* Segmented stable LSD radix sort (one-sweep, 8-bit digits) of (uint32 key,
+ * uint32 value) pairs by the low `bits` bits of the key: segment s occupies
+ * [bases[s], bases[s] + caps[s]), *device_counts[s] elements valid.  The sorted
+ * pairs end in keys/vals (*in_alt_out = 0) or keys_alt/vals_alt (1). */
+size_t recd_sort_pairs_scratch_bytes(int32_t num_segments, const int64_t* bases, const int64_t* caps);
+int recd_sort_pairs(int32_t num_segments, const int64_t* bases, const int64_t* caps,
+                    const int64_t* const* device_counts, int32_t bits, uint32_t* keys, uint32_t* vals,
+                    uint32_t* keys_alt, uint32_t* vals_alt, int32_t* in_alt_out, void* scratch,
+                    size_t scratch_bytes, recd_stream_t stream);
+
 /* Source half: grad_u_out[f] ([U x dim]) = grad_u of recd_pool_bwd (avg scaled). */
 size_t recd_grad_unique_scratch_bytes(int32_t num_features, int64_t batch_size);
 int recd_grad_unique(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,

@@ -55,6 +55,8 @@ _SIGS = {
     "recd_wire_bound": (_i64, [_i32, C.POINTER(C.c_char_p), _i64, _i32, _p64, _p64]),
     "recd_wire_serialize": (_i32, [_i32, C.POINTER(C.c_char_p), _i64, _vp, _pp, _pp, _pp, _pp, _p64,
                                    _p64, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "recd_sort_pairs_scratch_bytes": (_sz, [_i32, _p64, _p64]),
+    "recd_sort_pairs": (_i32, [_i32, _p64, _p64, _pp, _i32, _vp, _vp, _vp, _vp, _p32, _vp, _sz, _vp]),
     "recd_transform": (_i32, [_i32, _pp, _pp, _p64, _pp, _p32, _p64, _vp]),
     "recd_attention_pool_scratch_bytes": (_sz, [_i32, _i32, _p64]),
     "recd_attention_pool": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _vp, _vp, _vp,

@@ -440,3 +440,34 @@ int seg_exclusive_scan(const ScanDesc* segs, int S, int64_t* part, cudaStream_t 
 }
 
 }  // namespace recd
+
+using namespace recd;
+
+// Segmented stable radix sort of (uint32 key, uint32 value) pairs by the low
+// `bits` bits of the key (the primitive under the backward's inverse CSR and
+// occurrence sort; exported for tests and reuse).  Segment s occupies
+// [bases[s], bases[s] + caps[s]) of keys/vals, *device_counts[s] elements
+// valid; the result is left in keys/vals (*in_alt_out = 0) or keys_alt/vals_alt
+// (*in_alt_out = 1).
+extern "C" size_t recd_sort_pairs_scratch_bytes(int32_t num_segments, const int64_t* bases,
+                                                const int64_t* caps) {
+  std::vector<SegDesc> segs;
+  for (int s = 0; s < num_segments; ++s) segs.push_back({bases[s], caps[s], nullptr});
+  return (size_t)std::max<int64_t>(sort_hist_words(segs.data(), num_segments), 256) * sizeof(uint32_t);
+}
+
+extern "C" int recd_sort_pairs(int32_t num_segments, const int64_t* bases, const int64_t* caps,
+                               const int64_t* const* device_counts, int32_t bits, uint32_t* keys,
+                               uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
+                               int32_t* in_alt_out, void* scratch, size_t scratch_bytes,
+                               recd_stream_t stream) {
+  if (num_segments <= 0 || bits < 0 || bits > 32 || !device_counts || !in_alt_out) return RECD_ERR_ARG;
+  if (recd_sort_pairs_scratch_bytes(num_segments, bases, caps) > scratch_bytes) return RECD_ERR_SCRATCH;
+  std::vector<SegDesc> segs;
+  for (int s = 0; s < num_segments; ++s) segs.push_back({bases[s], caps[s], device_counts[s]});
+  bool alt = false;
+  const int rc = seg_sort_pairs(segs.data(), num_segments, bits, keys, vals, keys_alt, vals_alt,
+                                reinterpret_cast<uint32_t*>(scratch), &alt, (cudaStream_t)stream);
+  *in_alt_out = alt ? 1 : 0;
+  return rc;
+}

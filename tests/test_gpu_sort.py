@@ -1,0 +1,54 @@
+"""The segmented stable radix sort under the backward (recd_sort_pairs)
+against numpy's stable argsort: many equal keys (stability), several
+segments with device counts below their capacity, 8..32 key bits."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2211_05239_b200 import _lib  # noqa: E402
+
+
+@pytest.mark.parametrize("bits,nseg,maxn", [(24, 26, 300_000), (16, 3, 70_000), (8, 1, 5000),
+                                            (32, 4, 40_000), (24, 64, 9000), (20, 2, 1)])
+def test_sort_pairs_stable(bits, nseg, maxn):
+    rng = np.random.default_rng(bits * 100 + nseg)
+    caps = rng.integers(1, maxn + 1, size=nseg)
+    counts = [int(rng.integers(0, c + 1)) for c in caps]
+    bases = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.int64)
+    total = int(caps.sum())
+    hi = (1 << bits) if bits < 32 else (1 << 32)
+    nkeys = max(2, min(hi, 1 + total // 5))          # heavy duplication
+    keys = rng.integers(0, nkeys, size=total, dtype=np.uint64) % hi
+    if bits < 32:  # bits above `bits` must not affect the order
+        keys |= rng.integers(0, 1 << (32 - bits), size=total, dtype=np.uint64) << np.uint64(bits)
+    keys = (keys & 0xffffffff).astype(np.uint32)
+    vals = np.arange(total, dtype=np.uint32)
+    dev = torch.device("cuda")
+    k = torch.as_tensor(keys.view(np.int32), device=dev)
+    v = torch.as_tensor(vals.view(np.int32), device=dev)
+    ka, va = torch.empty_like(k), torch.empty_like(v)
+    cnt = [torch.tensor([c], dtype=torch.int64, device=dev) for c in counts]
+    lib = _lib.load()
+    nb = lib.recd_sort_pairs_scratch_bytes(nseg, _lib.i64s(bases.tolist()), _lib.i64s(caps.tolist()))
+    scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
+    alt = C.c_int32(-1)
+    rc = lib.recd_sort_pairs(nseg, _lib.i64s(bases.tolist()), _lib.i64s(caps.tolist()), _lib.ptrs(cnt),
+                             bits, k.data_ptr(), v.data_ptr(), ka.data_ptr(), va.data_ptr(),
+                             C.byref(alt), scratch.data_ptr(), nb, _lib.stream_ptr(dev))
+    assert rc == 0
+    torch.cuda.synchronize()
+    rk, rv = (ka, va) if alt.value else (k, v)
+    rk = rk.cpu().numpy().view(np.uint32)
+    rv = rv.cpu().numpy().view(np.uint32)
+    mask = np.uint32((1 << bits) - 1) if bits < 32 else np.uint32(0xffffffff)
+    for s in range(nseg):
+        a, n = int(bases[s]), counts[s]
+        seg_k = keys[a:a + n]
+        order = np.argsort(seg_k & mask, kind="stable")
+        np.testing.assert_array_equal(rv[a:a + n], vals[a:a + n][order])
+        np.testing.assert_array_equal(rk[a:a + n], seg_k[order])
