@@ -15,7 +15,8 @@
 //                 CTAs, W resident in shared memory (128-B swizzle, K-major),
 //                 X tiles of 128 tokens double-buffered with cp.async, BF16 x
 //                 BF16 -> F32 accumulators in TMEM (M = 128, N = 3d), epilogue
-//                 tcgen05.ld -> BF16 -> global
+//                 by 8 warps (two per TMEM lane quarter, alternate 32-column
+//                 chunks): tcgen05.ld -> BF16 -> global
 //   k_enc_attn    CTA per unique row: scores on the tensor cores (mma.sync
 //                 m16n8k16, 64 x 64 blocks), pass 1 row max / sum, pass 2
 //                 column sums of P, then (w v) / n and @ W_o in fp32
@@ -101,8 +102,9 @@ __device__ __forceinline__ void cp16_zfill(uint32_t saddr, const void* g, bool v
                "r"(valid ? 16 : 0));
 }
 
+constexpr int GM_NT = 256;  // 8 warps: warps w and w + 4 share TMEM lanes 32 (w % 4) .. + 32
 template <int N, int K>
-__global__ void __launch_bounds__(128, 1) k_gemm_tn(const __grid_constant__ GemmParams p) {
+__global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ GemmParams p) {
   static_assert(K % 64 == 0 && N % 16 == 0 && N <= 512, "tile shape");
   constexpr int KB = K / 64;               // 128-byte K blocks
   constexpr uint32_t A_STAGE = KB * 128 * 128;
@@ -125,13 +127,13 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tn(const __grid_constant__ Gemm
   const uint32_t sB_addr = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_addr = (uint32_t)__cvta_generic_to_shared(sA);
   // B once: (row n, K block kb, 16-B chunk c)
-  for (int idx = tid; idx < N * KB * 8; idx += 128) {
+  for (int idx = tid; idx < N * KB * 8; idx += GM_NT) {
     const int n = idx / (KB * 8), r = idx - n * (KB * 8), kb = r >> 3, c = r & 7;
     cp16_zfill(sB_addr + kb * N * 128 + umma::sw128_offset(n, c), p.B + (int64_t)n * K + kb * 64 + c * 8,
                true);
   }
   auto load_a = [&](int64_t t, int stage) {
-    for (int idx = tid; idx < 128 * KB * 8; idx += 128) {
+    for (int idx = tid; idx < 128 * KB * 8; idx += GM_NT) {
       const int r = idx / (KB * 8), q = idx - r * (KB * 8), kb = q >> 3, c = q & 7;
       const int64_t m = t * 128 + r;
       const bool ok = m < M;
@@ -173,12 +175,14 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tn(const __grid_constant__ Gemm
     umma::mbar_wait(&mbar, phase);
     phase ^= 1;
     umma::fence_after_sync();
-    const int64_t m = t * 128 + warp * 32 + lane;
+    const int lq = warp & 3;  // TMEM lane quarter of this warp
+    const int64_t m = t * 128 + lq * 32 + lane;
     __nv_bfloat16* crow = p.C + m * N;
+    // the two warps of a lane quarter take alternate 32-column chunks
 #pragma unroll 1
-    for (int c0 = 0; c0 < N; c0 += 32) {
+    for (int c0 = (warp >> 2) * 32; c0 < N; c0 += 64) {
       float v[32];
-      umma::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      umma::tmem_ld32(tmem + ((uint32_t)(lq * 32) << 16) + c0, v);
       if (m < M) {
         uint32_t w[16];
 #pragma unroll
@@ -398,7 +402,7 @@ template <int N, int K>
 static int launch_gemm(const GemmParams& g, cudaStream_t stream) {
   constexpr int smem = (K / 64) * N * 128 + 2 * (K / 64) * 128 * 128 + 1024;
   RECD_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_gemm_tn<N, K><<<num_sms(), 128, smem, stream>>>(g);
+  k_gemm_tn<N, K><<<num_sms(), GM_NT, smem, stream>>>(g);
   return RECD_OK;
 }
 
