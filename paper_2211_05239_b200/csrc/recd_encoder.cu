@@ -15,8 +15,9 @@
 //                 CTAs, W resident in shared memory (128-B swizzle, K-major),
 //                 X tiles of 128 tokens double-buffered with cp.async, BF16 x
 //                 BF16 -> F32 accumulators in TMEM (M = 128, N = 3d), epilogue
-//                 by 8 warps (two per TMEM lane quarter, alternate 32-column
-//                 chunks): tcgen05.ld -> BF16 -> global
+//                 by 8 warps (two per TMEM lane quarter, 64-column halves):
+//                 tcgen05.ld -> BF16 -> shared staging -> one 128-byte bulk
+//                 (TMA-engine) store per thread and chunk
 //   k_enc_attn    CTA per unique row: scores on the tensor cores (mma.sync
 //                 m16n8k16, 64 x 64 blocks), pass 1 row max / sum, pass 2
 //                 column sums of P, then (w v) / n and @ W_o in fp32
@@ -102,7 +103,8 @@ __device__ __forceinline__ void cp16_zfill(uint32_t saddr, const void* g, bool v
                "r"(valid ? 16 : 0));
 }
 
-constexpr int GM_NT = 256;  // 8 warps: warps w and w + 4 share TMEM lanes 32 (w % 4) .. + 32
+constexpr int GM_NT = 256;
+constexpr int GM_CPITCH = 272;  // staging row pitch (256 B + 16: conflict-free 16-B stores)  // 8 warps: warps w and w + 4 share TMEM lanes 32 (w % 4) .. + 32
 template <int N, int K>
 __global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ GemmParams p) {
   static_assert(K % 64 == 0 && N % 16 == 0 && N <= 512, "tile shape");
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ Ge
   uint8_t* smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;
   uint8_t* sA = smem + B_BYTES;
+  uint8_t* sC = sA + 2 * A_STAGE;  // epilogue staging: 128 rows x 256 B, padded pitch
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -176,29 +179,45 @@ __global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ Ge
     phase ^= 1;
     umma::fence_after_sync();
     const int lq = warp & 3;  // TMEM lane quarter of this warp
-    const int64_t m = t * 128 + lq * 32 + lane;
-    __nv_bfloat16* crow = p.C + m * N;
-    // the two warps of a lane quarter take alternate 32-column chunks
+    const int r = lq * 32 + lane;  // tile row of this thread
+    const int64_t m = t * 128 + r;
+    const int h = warp >> 2;  // the two warps of a lane quarter take the two 64-column halves
+    uint8_t* srow = sC + r * GM_CPITCH + h * 128;
 #pragma unroll 1
-    for (int c0 = (warp >> 2) * 32; c0 < N; c0 += 64) {
-      float v[32];
-      umma::tmem_ld32(tmem + ((uint32_t)(lq * 32) << 16) + c0, v);
-      if (m < M) {
-        uint32_t w[16];
+    for (int c0 = 0; c0 < N; c0 += 128) {
+      const int cb = c0 + h * 64;  // 64 columns of this thread
+      if (cb < N) {
+        // staging row segment free again (this thread's previous bulk store read it)
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-          w[i] = *reinterpret_cast<uint32_t*>(&h);
+        for (int q = 0; q < 2; ++q) {
+          float v[32];
+          umma::tmem_ld32(tmem + ((uint32_t)(lq * 32) << 16) + cb + 32 * q, v);
+          uint32_t w[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t*>(&hh);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(srow + q * 64);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
-        uint4* dst = reinterpret_cast<uint4*>(crow + c0);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        // 128 contiguous bytes of row m: one bulk (TMA-engine) store per thread
+        umma::fence_proxy_async();
+        if (m < M) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(p.C + m * N + cb),
+                       "r"((uint32_t)__cvta_generic_to_shared(srow))
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
     }
     umma::fence_before_sync();
     __syncthreads();  // TMEM drained and the A stage free before the next tile's MMAs / loads
   }
   cp_async_wait<0>();
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (warp == 0) {
     umma::fence_after_sync();
     umma::tmem_free<512>(tmem);
@@ -400,7 +419,7 @@ static size_t carve_enc(void* base, size_t cap, int64_t tok_cap, int D, EncScrat
 
 template <int N, int K>
 static int launch_gemm(const GemmParams& g, cudaStream_t stream) {
-  constexpr int smem = (K / 64) * N * 128 + 2 * (K / 64) * 128 * 128 + 1024;
+  constexpr int smem = (K / 64) * N * 128 + 2 * (K / 64) * 128 * 128 + 128 * GM_CPITCH + 1024;
   RECD_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tn<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_gemm_tn<N, K><<<num_sms(), GM_NT, smem, stream>>>(g);
   return RECD_OK;
