@@ -309,19 +309,24 @@ __global__ void __launch_bounds__(AT_NT) k_enc_attn(const __grid_constant__ EncP
         }
         // pass 1 over ALL keys: running row max / sum (exact softmax statistics)
         float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows g, g + 8 of this warp
+        // one 64 x 64 block (n <= 64, the common history length): pass 2 reuses
+        // pass 1's scaled scores instead of reloading K and recomputing them
+        const bool single = n <= AT_KB;
+        float s[8][4];
         for (int pass = 0; pass < 2; ++pass) {
           const int64_t kbeg = pass == 0 ? 0 : kc0, kend = pass == 0 ? n : kc0 + kcn;
           for (int64_t k0 = kbeg; k0 < kend; k0 += AT_KB) {
-            __syncthreads();
-            for (int idx = tid; idx < AT_KB * (D / 8); idx += AT_NT) {
-              const int r = idx / (D / 8), c = idx - r * (D / 8);
-              uint4 v = make_uint4(0, 0, 0, 0);
-              if (k0 + r < kend) v = *reinterpret_cast<const uint4*>(Kg + (k0 + r) * (3 * D) + c * 8);
-              *reinterpret_cast<uint4*>(sK + r * PITCH + c * 8) = v;
+            if (!(single && pass == 1)) {
+              __syncthreads();
+              for (int idx = tid; idx < AT_KB * (D / 8); idx += AT_NT) {
+                const int r = idx / (D / 8), c = idx - r * (D / 8);
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (k0 + r < kend) v = *reinterpret_cast<const uint4*>(Kg + (k0 + r) * (3 * D) + c * 8);
+                *reinterpret_cast<uint4*>(sK + r * PITCH + c * 8) = v;
+              }
+              __syncthreads();
+              scores16x64<D>(sQ, sK, PITCH, warp, lane, s);
             }
-            __syncthreads();
-            float s[8][4];
-            scores16x64<D>(sQ, sK, PITCH, warp, lane, s);
             // C fragment: s[nt][0..1] row g cols nt*8 + 2tq + {0,1}; s[nt][2..3] row g + 8
             if (pass == 0) {
               float bm0 = -INFINITY, bm1 = -INFINITY;
@@ -368,9 +373,10 @@ __global__ void __launch_bounds__(AT_NT) k_enc_attn(const __grid_constant__ EncP
                 for (int i = 0; i < 2; ++i) {
                   const int64_t j = k0 + nt * 8 + 2 * tq + i;
                   float c = 0.f;
-                  if (j < kend) {
-                    c = (r0 ? __expf(s[nt][i] * scale - m0) * i0 : 0.f) +
-                        (r1 ? __expf(s[nt][2 + i] * scale - m1) * i1 : 0.f);
+                  if (j < kend) {  // single: s already scaled (same fp32 value)
+                    const float s0 = single ? s[nt][i] : s[nt][i] * scale;
+                    const float s1 = single ? s[nt][2 + i] : s[nt][2 + i] * scale;
+                    c = (r0 ? __expf(s0 - m0) * i0 : 0.f) + (r1 ? __expf(s1 - m1) * i1 : 0.f);
                   }
                   // sum over the 8 row groups (lanes with equal tq)
 #pragma unroll
