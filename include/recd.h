@@ -123,6 +123,17 @@ int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t
                   float* const* pooled_out, float* const* out, int64_t* err,
                   recd_stream_t stream);
 
+/* Owner-side pooled lookup whose output rows go straight to the sources'
+ * receive buffers (the all-to-all of partial rows fused into the pooling):
+ * feature f's row u is stored at seg_dst[f * num_segs + s] + (u - seg_row0[f][s]) * dim
+ * for the segment s with seg_row0[f][s] <= u < seg_row0[f][s + 1] (seg_row0:
+ * device, ascending; num_segs <= 8; seg_dst may be peer / NVLink memory). */
+int recd_pool_fwd_scatter(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                          const float* const* tables, const int64_t* table_rows,
+                          const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                          const int64_t* counts, int32_t num_segs, const int64_t* const* seg_row0,
+                          float* const* seg_dst, int64_t* err, recd_stream_t stream);
+
 /* Expansion only: out[f][i] = pooled[f][inverse[f][i]] (inverse[f] NULL =
  * identity).  recd_pool_fwd with out = NULL followed by recd_expand equals one
  * recd_pool_fwd with out set (the split lets callers time the two kernels). */
@@ -251,6 +262,17 @@ int recd_grad_unique(int32_t num_features, int64_t batch_size, int32_t dim, int3
                      const int64_t* const* inverse, const float* const* grad_out,
                      float* const* grad_u_out, void* scratch, size_t scratch_bytes,
                      recd_stream_t stream);
+
+/* recd_grad_unique whose rows go straight to the owners' receive buffers (the
+ * push of unique-row gradients fused into the segment reduce): feature f's row
+ * u is stored at seg_dst[f * num_segs + j] + (*seg_row0[f * num_segs + j] + u) * dim
+ * for every j < num_segs (<= 8; seg_row0 on the device; seg_dst may be peer memory). */
+int recd_grad_unique_scatter(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                             const int64_t* const* uoffsets, const int64_t* counts,
+                             const int64_t* const* inverse, const float* const* grad_out,
+                             int32_t num_segs, const int64_t* const* seg_row0,
+                             float* const* seg_dst, void* scratch, size_t scratch_bytes,
+                             recd_stream_t stream);
 
 /* Owner half: grad_rows[f] holds one gradient row per unique row of feature f
  * (max_rows >= its row count, < 2^24); occurrences are reduced per ID in

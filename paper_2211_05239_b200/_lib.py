@@ -42,6 +42,8 @@ _SIGS = {
     "recd_dedup": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _pp, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_pool_fwd": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _pp, _pp, _pp,
                              _vp, _vp]),
+    "recd_pool_fwd_scatter": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _i32, _pp, _pp,
+                                     _vp, _vp]),
     "recd_expand": (_i32, [_i32, _i64, _i32, _pp, _pp, _pp, _vp]),
     "recd_embedding_lookup": (_i32, [_vp, _i64, _i32, _vp, _i64, _vp, _vp, _vp]),
     "recd_pool_dense": (_i32, [_vp, _i64, _i32, _vp, _i64, _i32, _vp, _vp]),
@@ -64,6 +66,8 @@ _SIGS = {
     "recd_gemm_bf16_tn": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "recd_grad_unique_scratch_bytes": (_sz, [_i32, _i64]),
     "recd_grad_unique": (_i32, [_i32, _i64, _i32, _i32, _pp, _vp, _pp, _pp, _pp, _vp, _sz, _vp]),
+    "recd_grad_unique_scatter": (_i32, [_i32, _i64, _i32, _i32, _pp, _vp, _pp, _pp, _i32, _pp, _pp, _vp,
+                                        _sz, _vp]),
     "recd_sparse_sgd_scratch_bytes": (_sz, [_i32, _p64]),
     "recd_sparse_sgd": (_i32, [_i32, _i64, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _f32, _i32,
                                _pp, _pp, _vp, _vp, _sz, _vp]),

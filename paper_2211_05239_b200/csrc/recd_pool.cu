@@ -10,6 +10,9 @@
 #include "recd_slice.cuh"
 
 // Tuning knobs of the forward gather (overridable with -D at build time).
+#ifndef RECD_PEER_MAXSEG
+#define RECD_PEER_MAXSEG 8  // ranks a fused pooled-row scatter can address
+#endif
 #ifndef RECD_POOL_VW
 #define RECD_POOL_VW 4
 #endif
@@ -46,7 +49,22 @@ struct PoolParams {
   int64_t Ftot;
   int64_t* err;
   int f0;                 // global index of feature 0 of this chunk (error packing)
+  // optional scatter of the pooled rows to peers (fused owner -> source return):
+  // rows [row0[f][s], row0[f][s + 1]) of feature f go to dst[f][s] (NVLink
+  // memory of source s), row0 read from the device (exchange plan)
+  int nseg;
+  const int64_t* seg_row0[RECD_MAX_FEAT];   // device: nseg bases, ascending
+  float* seg_dst[RECD_MAX_FEAT][RECD_PEER_MAXSEG];
 };
+
+// destination row of pooled row u of feature f (peer segment or local buffer)
+__device__ __forceinline__ float* pooled_row(const PoolParams& p, int f, int64_t u) {
+  if (p.nseg == 0) return p.pooled[f] + u * p.D;
+  int s = 0;
+  const int64_t* r0 = p.seg_row0[f];
+  while (s + 1 < p.nseg && __ldg(r0 + s + 1) <= u) ++s;
+  return p.seg_dst[f][s] + (u - __ldg(r0 + s)) * p.D;
+}
 
 template <class C>
 __global__ void __launch_bounds__(256, RECD_POOL_MINB) k_pool_fwd(const __grid_constant__ PoolParams p) {
@@ -78,7 +96,7 @@ __global__ void __launch_bounds__(256, RECD_POOL_MINB) k_pool_fwd(const __grid_c
     row.window(a);
     float acc[C::VW];
     pool_row<C>(row, a, e - a, p.mode, cw.ok, acc);
-    C::st(p.pooled[f] + u * p.D + cw.lo, cw.ok, acc);
+    C::st(pooled_row(p, f, u) + cw.lo, cw.ok, acc);
   }
 }
 
@@ -429,7 +447,7 @@ __global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_
         for (int k = 0; k < 4; ++k) acc[k] = __fdiv_rn(acc[k], fl);
       }
     }
-    C::st(p.pooled[f] + u * p.D + cw.lo, cw.ok, acc);
+    C::st(pooled_row(p, f, u) + cw.lo, cw.ok, acc);
   }
   cp_async_wait<0>();
 }
@@ -518,6 +536,55 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
     if (rc != RECD_OK) return rc;
     RECD_LAUNCH_CHECK();
   }
+  return RECD_OK;
+}
+
+// Owner-side pooling whose rows go straight to the sources' receive buffers
+// over NVLink (the all-to-all of partial rows fused into the pooling kernel):
+// feature f's row u lands at seg_dst[f * num_segs + s] + (u - row0[f][s]) * dim
+// for the segment s with row0[f][s] <= u < row0[f][s + 1] (row0 on the device,
+// num_segs <= 8).  Sum / avg, no expansion.
+extern "C" int recd_pool_fwd_scatter(int32_t num_features, int64_t batch_size, int32_t dim,
+                                     int32_t mode, const float* const* tables,
+                                     const int64_t* table_rows, const int64_t* const* uvalues,
+                                     const int64_t* const* uoffsets, const int64_t* counts,
+                                     int32_t num_segs, const int64_t* const* seg_row0,
+                                     float* const* seg_dst, int64_t* err, recd_stream_t stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (num_features <= 0 || num_features > RECD_MAX_FEAT || batch_size < 0 || dim <= 0 ||
+      mode < 0 || mode > 2 || !counts || !err || num_segs <= 0 || num_segs > RECD_PEER_MAXSEG ||
+      !seg_row0 || !seg_dst)
+    return RECD_ERR_ARG;
+  RECD_CUDA_CHECK(cudaMemsetAsync(err, 0x7f, sizeof(int64_t), stream));
+  PoolParams p;
+  memset(&p, 0, sizeof(p));
+  p.F = num_features;
+  p.D = dim;
+  p.mode = mode;
+  p.B = batch_size;
+  p.counts = counts;
+  p.Ftot = num_features;
+  p.err = err;
+  p.nseg = num_segs;
+  for (int f = 0; f < p.F; ++f) {
+    p.tables[f] = tables[f];
+    p.table_rows[f] = table_rows[f];
+    p.uvalues[f] = uvalues[f];
+    p.uoffsets[f] = uoffsets[f];
+    p.seg_row0[f] = seg_row0[f];
+    for (int s = 0; s < num_segs; ++s) {
+      p.seg_dst[f][s] = seg_dst[(int64_t)f * num_segs + s];
+      if (!p.seg_dst[f][s] || (dim % 2 == 0 && (uintptr_t)p.seg_dst[f][s] % 8)) return RECD_ERR_ARG;
+    }
+    if (!p.tables[f] || !p.uoffsets[f] || !p.seg_row0[f]) return RECD_ERR_ARG;
+  }
+  int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, 1, {
+    const int lrc = launch_pool_fwd<C>(p, mode, grid_for(batch_size * p.F * col_blocks<C>(dim)), stream);
+    if (lrc != RECD_OK) return lrc;
+    note_launch();
+  });
+  if (rc != RECD_OK) return rc;
+  RECD_LAUNCH_CHECK();
   return RECD_OK;
 }
 
