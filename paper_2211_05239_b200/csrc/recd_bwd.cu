@@ -84,6 +84,11 @@ struct BwdParams {
   uint32_t* occ_keys;     // sorted occurrence IDs
   uint32_t* occ_vals;     // tag = (f << 24) | u
   int64_t* run_part;      // [total_rc_chunks] exclusive run counts (grad-output mode)
+  // optional scatter of grad_u rows to peers (fused source -> owner push): row u
+  // of feature f goes to gseg_dst[f][j] + (*gseg_row0[f][j] + u) * D, j < gsegs
+  int gsegs;
+  float* gseg_dst[RECD_MAX_FEAT][8];
+  const int64_t* gseg_row0[RECD_MAX_FEAT][8];
 };
 
 __global__ void k_bwd_setup(const __grid_constant__ BwdParams p) {
@@ -174,7 +179,12 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
         for (int k = 0; k < V; ++k) acc[k] = __fdiv_rn(acc[k], fl);
       }
     }
-    C::st(p.gout[f] + u * p.D + cw.lo, cw.ok, acc);
+    if (p.gsegs == 0) {
+      C::st(p.gout[f] + u * p.D + cw.lo, cw.ok, acc);
+    } else {
+      for (int j = 0; j < p.gsegs; ++j)
+        C::st(p.gseg_dst[f][j] + (__ldg(p.gseg_row0[f][j]) + u) * p.D + cw.lo, cw.ok, acc);
+    }
   }
 }
 
@@ -534,7 +544,9 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
             const int64_t* const* inverse, const float* const* grad_out, float* const* gout_ext,
             const float* const* grow_ext, float lr, int apply_sgd, int64_t* const* grad_ids_out,
             float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
-            size_t scratch_bytes, cudaStream_t stream, int phase = PH_ALL) {
+            size_t scratch_bytes, cudaStream_t stream, int phase = PH_ALL,
+            int gsegs = 0, float* const* gseg_dst = nullptr,
+            const int64_t* const* gseg_row0 = nullptr) {
   if (F <= 0 || F > RECD_MAX_FEAT || B <= 0 || dim <= 0 || !counts) return RECD_ERR_ARG;
   if (mode != RECD_POOL_SUM && mode != RECD_POOL_AVG) return RECD_ERR_UNSUPPORTED;
   if (B >= (1ll << 24)) return RECD_ERR_UNSUPPORTED;  // occurrence tags hold u in 24 bits
@@ -618,6 +630,14 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     }
   }
   p.total_rc_chunks = pl.rc_chunks;
+  if (gsegs < 0 || gsegs > 8 || (gsegs && (!gseg_dst || !gseg_row0))) return RECD_ERR_ARG;
+  p.gsegs = gsegs;
+  for (int f = 0; f < F && gsegs; ++f)
+    for (int j = 0; j < gsegs; ++j) {
+      p.gseg_dst[f][j] = gseg_dst[f * gsegs + j];
+      p.gseg_row0[f][j] = gseg_row0[f * gsegs + j];
+      if (!p.gseg_dst[f][j] || !p.gseg_row0[f][j]) return RECD_ERR_ARG;
+    }
   p.feat_base = sc.feat_base;
   p.seg_count = sc.seg_count;
   p.is_count = sc.is_count;
@@ -794,6 +814,26 @@ extern "C" int recd_grad_unique(int32_t num_features, int64_t batch_size, int32_
   return run_bwd(BwdMode::GradOnly, num_features, batch_size, dim, mode, nullptr, nullptr, nullptr,
                  uoffsets, nullptr, counts, inverse, grad_out, grad_u_out, nullptr, 0.f, 1,
                  nullptr, nullptr, nullptr, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+// recd_grad_unique whose rows go straight to the owners' receive buffers (the
+// push of unique-row gradients fused into the segment reduce): feature f's row
+// u is stored at seg_dst[f * num_segs + j] + (*seg_row0[f * num_segs + j] + u) * dim
+// for every j < num_segs (<= 8; seg_row0 on the device, seg_dst may be peer memory).
+extern "C" int recd_grad_unique_scatter(int32_t num_features, int64_t batch_size, int32_t dim,
+                                        int32_t mode, const int64_t* const* uoffsets,
+                                        const int64_t* counts, const int64_t* const* inverse,
+                                        const float* const* grad_out, int32_t num_segs,
+                                        const int64_t* const* seg_row0, float* const* seg_dst,
+                                        void* scratch, size_t scratch_bytes, recd_stream_t stream) {
+  if (num_segs <= 0 || num_segs > 8 || !seg_dst || num_features <= 0 || num_features > RECD_MAX_FEAT)
+    return RECD_ERR_ARG;
+  std::vector<float*> first(num_features);
+  for (int f = 0; f < num_features; ++f) first[f] = seg_dst[(int64_t)f * num_segs];
+  return run_bwd(BwdMode::GradOnly, num_features, batch_size, dim, mode, nullptr, nullptr, nullptr,
+                 uoffsets, nullptr, counts, inverse, grad_out, first.data(), nullptr, 0.f, 1,
+                 nullptr, nullptr, nullptr, scratch, scratch_bytes, (cudaStream_t)stream, PH_ALL,
+                 num_segs, seg_dst, seg_row0);
 }
 
 extern "C" size_t recd_sparse_sgd_scratch_bytes(int32_t num_features, const int64_t* value_caps) {

@@ -11,11 +11,12 @@ other rank's exchange buffers (CUDA IPC over NVLink / NVSwitch) and
   recd_peer_exchange   all-gather of the per-pair counts + barrier + plan (device)
   recd_shard_dispatch  stores the IDs and row offsets straight into the owners'
                        lists at the planned offsets (NVLink stores)
-  recd_pool_fwd        owner: partial pooling of every source's rows
-  recd_peer_copy_rows  owner -> sources: partial rows, sizes read on the device
+  recd_pool_fwd_scatter owner: partial pooling of every source's rows, each
+                       row stored straight into its source's receive buffer
+                       over NVLink (pooling fused with the return all-to-all)
   recd_shard_combine   source: shard-order sum + avg, then recd_expand
-  recd_grad_unique     source: gradient of every unique row
-  recd_peer_copy_rows  source -> owners: unique-row gradients
+  recd_grad_unique_scatter source: gradient of every unique row, stored
+                       straight into the owners' receive buffers over NVLink
   recd_sparse_sgd      owner: deterministic sorted scatter-add + SGD (its
                        _prepare half -- the occurrence sort -- runs on a side
                        stream from the end of the dispatch, overlapping the rest)
@@ -232,6 +233,11 @@ class PeerShardedStep:
                 segs.append((self.part_out[q].data_ptr(), self._peer(s, "part") + p * B * row,
                              _CTL_META + s * W + P + p, self.i_own_base + q * R + s, -1))
         self.part_segs = self._segs(segs)
+        # fused return: owned pair q's rows of source s start at own_base[q][s]
+        # (device, exchange plan) and go to source s's receive buffer of pair p
+        self.a_seg_row0 = Pp([self.ctl_ptr + 8 * (self.i_own_base + q * R) for q in range(Q)] or [0])
+        self.a_seg_dst = Pp([self._peer(s2, "part") + p * B * row for p in self.mine for s2 in range(R)]
+                            or [0])
         # source -> owners: all U rows of feature f(p) at src_row_base[p]
         segs = []
         for p in range(P):
@@ -240,6 +246,11 @@ class PeerShardedStep:
                          self._peer(o, "grad", self.owned_by[o].index(p)),
                          _CTL_META + rank * W + P + p, -1, self.i_plan + P + p))
         self.grad_segs = self._segs(segs)
+        # fused push: feature f's rows go to the owner of each pair (f, j) at that
+        # owner's row base for this rank (device, exchange plan)
+        self.a_gseg_dst = Pp([self._peer(self.place[p], "grad", self.owned_by[self.place[p]].index(p))
+                              for p in range(P)])
+        self.a_gseg_row0 = Pp([self.ctl_ptr + 8 * (self.i_plan + P + p) for p in range(P)])
 
     def _segs(self, segs) -> tuple[torch.Tensor, int]:
         arr = (_RowSeg * max(len(segs), 1))()
@@ -336,14 +347,14 @@ class PeerShardedStep:
                        "recd_sparse_sgd_prepare")
             self._ev_join.record(self._side)
         if Q:
-            rc = L.recd_pool_fwd(Q, R * B, D, _lib.POOL_MODES["sum"], self.a_tables, self.a_rows,
-                                 self.a_own_ids, self.a_own_ro, self.own_counts_ptr, None,
-                                 self.a_part_out, None, self.err.data_ptr(), s)
-            _lib.check(rc, "recd_pool_fwd(owner)")
+            # owner pooling fused with the return all-to-all: every partial row
+            # is stored straight into its source's receive buffer over NVLink
+            rc = L.recd_pool_fwd_scatter(Q, R * B, D, _lib.POOL_MODES["sum"], self.a_tables,
+                                         self.a_rows, self.a_own_ids, self.a_own_ro,
+                                         self.own_counts_ptr, R, self.a_seg_row0, self.a_seg_dst,
+                                         self.err.data_ptr(), s)
+            _lib.check(rc, "recd_pool_fwd_scatter(owner)")
         self._mark("owner_pool")
-        segs, n = self.part_segs
-        _lib.check(L.recd_peer_copy_rows(n if Q else 0, segs.data_ptr(), self.ctl_ptr, 4 * D, B, s),
-                   "recd_peer_copy_rows")
         self._exchange(s, False)
         self._mark("return_partials")
         if S == 1 and self.mode_id == _lib.POOL_MODES["sum"]:
@@ -360,14 +371,24 @@ class PeerShardedStep:
     def backward(self):
         L, s = self.lib, _lib.stream_ptr(self.dev)
         R, B, D, F, Q = self.R, self.B, self.D, self.F, self.Q
-        rc = L.recd_grad_unique(F, B, D, self.mode_id, self.a_uoffsets, self.counts.data_ptr(),
-                                self.a_inverse, self.a_grad_out, self.a_gradG,
-                                self.s_grad.data_ptr(), self.s_grad.numel(), s)
-        _lib.check(rc, "recd_grad_unique")
-        self._mark("grad_unique")
-        segs, n = self.grad_segs
-        _lib.check(L.recd_peer_copy_rows(n, segs.data_ptr(), self.ctl_ptr, 4 * D, B, s),
-                   "recd_peer_copy_rows")
+        if self.S <= 8:
+            # segment reduce fused with the push: every unique-row gradient is
+            # stored straight into its owners' receive buffers over NVLink
+            rc = L.recd_grad_unique_scatter(F, B, D, self.mode_id, self.a_uoffsets,
+                                            self.counts.data_ptr(), self.a_inverse, self.a_grad_out,
+                                            self.S, self.a_gseg_row0, self.a_gseg_dst,
+                                            self.s_grad.data_ptr(), self.s_grad.numel(), s)
+            _lib.check(rc, "recd_grad_unique_scatter")
+            self._mark("grad_unique")
+        else:
+            rc = L.recd_grad_unique(F, B, D, self.mode_id, self.a_uoffsets, self.counts.data_ptr(),
+                                    self.a_inverse, self.a_grad_out, self.a_gradG,
+                                    self.s_grad.data_ptr(), self.s_grad.numel(), s)
+            _lib.check(rc, "recd_grad_unique")
+            self._mark("grad_unique")
+            segs, n = self.grad_segs
+            _lib.check(L.recd_peer_copy_rows(n, segs.data_ptr(), self.ctl_ptr, 4 * D, B, s),
+                       "recd_peer_copy_rows")
         self._exchange(s, False)
         self._mark("push_grads")
         if Q and self.overlap:
