@@ -150,6 +150,24 @@ int recd_embedding_lookup(const float* table, int64_t table_rows, int32_t dim,
 int recd_pool_dense(const float* acts, int64_t n_values, int32_t dim, const int64_t* offsets,
                     int64_t n_rows, int32_t mode, float* out, recd_stream_t stream);
 
+/* recd_dedup in two halves (same arguments, same scratch): _number computes
+ * inverse_out, uoffsets_out and counts_out; _copy gathers the unique values into
+ * uvalues_out and, for features with remote_values[f] != NULL, also into
+ * remote_values[f] + *remote_base[f] (device base; e.g. the owner's list in
+ * peer memory -- the row-sharded step's ID dispatch fused into the gather). */
+int recd_dedup_number(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+                      const int64_t* const* values, const int64_t* const* offsets,
+                      const int64_t* num_values, int64_t* const* inverse_out,
+                      int64_t* const* uoffsets_out, int64_t* const* uvalues_out,
+                      int64_t* counts_out, void* scratch, size_t scratch_bytes,
+                      recd_stream_t stream);
+int recd_dedup_copy(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+                    const int64_t* const* values, const int64_t* const* offsets,
+                    const int64_t* num_values, int64_t* const* inverse_out,
+                    int64_t* const* uoffsets_out, int64_t* const* uvalues_out, int64_t* counts_out,
+                    int64_t* const* remote_values, const int64_t* const* remote_base,
+                    void* scratch, size_t scratch_bytes, recd_stream_t stream);
+
 /* ------------------------------------------------------------- pool bwd --
  * grad_u[u] = sum_{i: inverse[i]=u} grad_out[i]  (ascending i; /len for avg),
  * then for every distinct ID v of the feature, in ascending v:

@@ -40,6 +40,9 @@ _SIGS = {
     "recd_debug_kernel_events": (None, [C.c_char_p, _vp, _vp]),
     "recd_dedup_scratch_bytes": (_sz, [_i32, _i32, _i64]),
     "recd_dedup": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _pp, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_dedup_number": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _pp, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_dedup_copy": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _pp, _pp, _pp, _vp, _pp, _pp, _vp, _sz,
+                               _vp]),
     "recd_pool_fwd": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _pp, _pp, _pp,
                              _vp, _vp]),
     "recd_pool_fwd_scatter": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _i32, _pp, _pp,

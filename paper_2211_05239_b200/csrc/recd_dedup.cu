@@ -59,7 +59,11 @@ struct DedupParams {
   uint32_t* treps;            // [G][C]
   int32_t* collide;           // [G]
   int rs_group[RECD_MAX_FEAT];
-  int64_t cp_blk0[RECD_MAX_FEAT + 1];  // k_copy: first block of each feature  // k_rowscan: groups in launch order (most values first)
+  int64_t cp_blk0[RECD_MAX_FEAT + 1];  // k_copy: first block of each feature
+  // k_copy second destination (fused shard dispatch): values also go to
+  // rdst[f][*rbase[f] + j] (peer memory of the feature's owner), or null
+  int64_t* rdst[RECD_MAX_FEAT];
+  const int64_t* rbase[RECD_MAX_FEAT];  // k_rowscan: groups in launch order (most values first)
 };
 
 __device__ __forceinline__ int64_t row_begin(const int64_t* off, int64_t i) { return off[i]; }
@@ -547,6 +551,7 @@ __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupPar
   const int64_t* off = p.offsets[f];
   const int64_t* src = p.values[f];
   int64_t* dst = p.uvalues[f];
+  int64_t* rdst = p.rdst[f] ? p.rdst[f] + *p.rbase[f] : nullptr;
   const int32_t* frows = p.first_rows + (int64_t)p.feat_group[f] * p.B;
   __shared__ int64_t s_u0;
   __shared__ int64_t s_uo[CP_MAXR + 1];
@@ -577,7 +582,9 @@ __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupPar
         if (s_uo[mid] <= q) lo = mid; else hi = mid - 1;
       }
       r = lo;
-      dst[q] = __ldg(src + s_so[r] + (q - s_uo[r]));
+      const int64_t v = __ldg(src + s_so[r] + (q - s_uo[r]));
+      dst[q] = v;
+      if (rdst) rdst[q] = v;
     }
     if (covered >= j1) break;
     __syncthreads();
@@ -631,13 +638,14 @@ extern "C" size_t recd_dedup_scratch_bytes(int32_t num_groups, int32_t num_featu
                      table_slots(batch_size), &s);
 }
 
-extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
-                          const int64_t* const* values, const int64_t* const* offsets,
-                          const int64_t* num_values, int64_t* const* inverse_out,
-                          int64_t* const* uoffsets_out, int64_t* const* uvalues_out,
-                          int64_t* counts_out, void* scratch, size_t scratch_bytes,
-                          recd_stream_t stream_) {
-  cudaStream_t stream = (cudaStream_t)stream_;
+enum { DD_NUMBER = 1, DD_COPY = 2, DD_ALL = 3 };
+
+static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+                     const int64_t* const* values, const int64_t* const* offsets,
+                     const int64_t* num_values, int64_t* const* inverse_out,
+                     int64_t* const* uoffsets_out, int64_t* const* uvalues_out, int64_t* counts_out,
+                     void* scratch, size_t scratch_bytes, cudaStream_t stream, int phase,
+                     int64_t* const* remote_values, const int64_t* const* remote_base) {
   if (num_groups <= 0 || batch_size <= 0 || batch_size >= (1ll << 31) || !group_sizes)
     return RECD_ERR_ARG;
   int F = 0;
@@ -648,7 +656,8 @@ extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_
   const int64_t B = batch_size, C = table_slots(B);
   DedupScratch s;
   if (carve_dedup(scratch, scratch_bytes, num_groups, F, B, C, &s) > scratch_bytes) return RECD_ERR_SCRATCH;
-  RECD_CUDA_CHECK(cudaMemsetAsync(s.collide, 0, sizeof(int32_t) * num_groups, stream));
+  if (phase & DD_NUMBER)
+    RECD_CUDA_CHECK(cudaMemsetAsync(s.collide, 0, sizeof(int32_t) * num_groups, stream));
 
   int g0 = 0, f0 = 0;
   while (g0 < num_groups) {
@@ -673,6 +682,9 @@ extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_
         p.nvalues[f] = num_values[f0 + f];
         p.uoffsets[f] = uoffsets_out[f0 + f];
         p.uvalues[f] = uvalues_out[f0 + f];
+        p.rdst[f] = remote_values ? remote_values[f0 + f] : nullptr;
+        p.rbase[f] = remote_base ? remote_base[f0 + f] : nullptr;
+        if (p.rdst[f] && !p.rbase[f]) return RECD_ERR_ARG;
         if (!p.offsets[f] || !p.inverse[g] || !p.uoffsets[f] || (!p.values[f] && p.nvalues[f] > 0))
           return RECD_ERR_ARG;
       }
@@ -708,28 +720,69 @@ extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_
       std::stable_sort(order.begin(), order.end());
       for (int k = 0; k < p.G; ++k) p.rs_group[k] = order[k].second;
     }
-    k_rowscan<<<dim3((unsigned)ceil_div(B, RS_RPB), p.G), RS_NT, 0, stream>>>(p);
-    k_insert<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
-    k_resolve<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
-    k_fallback<<<p.G, FB_NT, 0, stream>>>(p);
-    {
+    if (phase & DD_NUMBER) {
+      k_rowscan<<<dim3((unsigned)ceil_div(B, RS_RPB), p.G), RS_NT, 0, stream>>>(p);
+      k_insert<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
+      k_resolve<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
+      k_fallback<<<p.G, FB_NT, 0, stream>>>(p);
       const dim3 ng((unsigned)ceil_div(B, NB_CH), p.G);
       k_num_reduce<<<ng, NB_NT, 0, stream>>>(p);
       k_num_scan<<<p.G, NB_NT, 0, stream>>>(p);
       k_num_down<<<ng, NB_NT, 0, stream>>>(p);
       k_num_inv<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
+      note_launch(8);
     }
-    int64_t cblk = 0;
-    for (int ff = 0; ff < p.F; ++ff) {
-      p.cp_blk0[ff] = cblk;
-      cblk += std::max<int64_t>(1, ceil_div(p.nvalues[ff], CP_CH));
+    if (phase & DD_COPY) {
+      int64_t cblk = 0;
+      for (int ff = 0; ff < p.F; ++ff) {
+        p.cp_blk0[ff] = cblk;
+        cblk += std::max<int64_t>(1, ceil_div(p.nvalues[ff], CP_CH));
+      }
+      p.cp_blk0[p.F] = cblk;
+      k_copy<<<(unsigned)cblk, CP_NT, 0, stream>>>(p);
+      note_launch(1);
     }
-    p.cp_blk0[p.F] = cblk;
-    k_copy<<<(unsigned)cblk, CP_NT, 0, stream>>>(p);
-    note_launch(9);
     RECD_LAUNCH_CHECK();
     g0 = g1;
     f0 += nf;
   }
   return RECD_OK;
+}
+
+extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+                          const int64_t* const* values, const int64_t* const* offsets,
+                          const int64_t* num_values, int64_t* const* inverse_out,
+                          int64_t* const* uoffsets_out, int64_t* const* uvalues_out,
+                          int64_t* counts_out, void* scratch, size_t scratch_bytes,
+                          recd_stream_t stream) {
+  return run_dedup(num_groups, group_sizes, batch_size, values, offsets, num_values, inverse_out,
+                   uoffsets_out, uvalues_out, counts_out, scratch, scratch_bytes,
+                   (cudaStream_t)stream, DD_ALL, nullptr, nullptr);
+}
+
+// recd_dedup in two halves (same arguments, same scratch): _number computes the
+// inverse, unique offsets and counts; _copy gathers the unique values and can
+// also store them into a second (peer) buffer at a device-side base -- the
+// row-sharded step's ID dispatch fused into the gather.
+extern "C" int recd_dedup_number(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+                                 const int64_t* const* values, const int64_t* const* offsets,
+                                 const int64_t* num_values, int64_t* const* inverse_out,
+                                 int64_t* const* uoffsets_out, int64_t* const* uvalues_out,
+                                 int64_t* counts_out, void* scratch, size_t scratch_bytes,
+                                 recd_stream_t stream) {
+  return run_dedup(num_groups, group_sizes, batch_size, values, offsets, num_values, inverse_out,
+                   uoffsets_out, uvalues_out, counts_out, scratch, scratch_bytes,
+                   (cudaStream_t)stream, DD_NUMBER, nullptr, nullptr);
+}
+
+extern "C" int recd_dedup_copy(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+                               const int64_t* const* values, const int64_t* const* offsets,
+                               const int64_t* num_values, int64_t* const* inverse_out,
+                               int64_t* const* uoffsets_out, int64_t* const* uvalues_out,
+                               int64_t* counts_out, int64_t* const* remote_values,
+                               const int64_t* const* remote_base, void* scratch,
+                               size_t scratch_bytes, recd_stream_t stream) {
+  return run_dedup(num_groups, group_sizes, batch_size, values, offsets, num_values, inverse_out,
+                   uoffsets_out, uvalues_out, counts_out, scratch, scratch_bytes,
+                   (cudaStream_t)stream, DD_COPY, remote_values, remote_base);
 }

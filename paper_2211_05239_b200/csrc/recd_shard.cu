@@ -171,8 +171,10 @@ __global__ void __launch_bounds__(256) k_shard_scatter1(const __grid_constant__ 
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t* src = p.uvalues[f];
-  int64_t* dst = p.dst_ids[f] + base;
-  for (int64_t j = t0; j < N; j += stride) dst[j] = __ldg(src + j);
+  if (p.dst_ids[f]) {
+    int64_t* dst = p.dst_ids[f] + base;
+    for (int64_t j = t0; j < N; j += stride) dst[j] = __ldg(src + j);
+  }
   if (p.dst_ro[f]) {
     int64_t* ro = p.dst_ro[f] + (p.row_base ? p.row_base[f] : 0);
     for (int64_t u = t0; u < U; u += stride) ro[u] = base + p.rowoff[f][u];
@@ -347,7 +349,7 @@ extern "C" int recd_shard_dispatch(int32_t num_features, int32_t num_shards, int
     p.rowoff[f] = rowoff[f];
   }
   for (int i = 0; i < F * S; ++i) {
-    if (!dst_ids[i]) return RECD_ERR_ARG;
+    if (!dst_ids[i] && S != 1) return RECD_ERR_ARG;  // S == 1: null = IDs already placed
     p.dst_ids[i] = dst_ids[i];
     p.dst_ro[i] = dst_rowoffs ? dst_rowoffs[i] : nullptr;
   }

@@ -10,7 +10,9 @@ other rank's exchange buffers (CUDA IPC over NVLink / NVSwitch) and
   recd_shard_count     per-(shard, unique row) counts of the local unique IDs
   recd_peer_exchange   all-gather of the per-pair counts + barrier + plan (device)
   recd_shard_dispatch  stores the IDs and row offsets straight into the owners'
-                       lists at the planned offsets (NVLink stores)
+                       lists at the planned offsets (NVLink stores); with one
+                       shard per table the IDs are stored by the dedup's own
+                       gather instead (recd_dedup_number / recd_dedup_copy)
   recd_pool_fwd_scatter owner: partial pooling of every source's rows, each
                        row stored straight into its source's receive buffer
                        over NVLink (pooling fused with the return all-to-all)
@@ -212,6 +214,8 @@ class PeerShardedStep:
             dst_ids.append(self._peer(o, "ids", qo))
             dst_ro.append(self._peer(o, "ro", qo))
         self.a_dst_ids, self.a_dst_ro = Pp(dst_ids), Pp(dst_ro)
+        self.a_no_ids = Pp([0] * P)                                 # dispatch: row offsets only
+        self.a_id_base = Pp([self.ctl_ptr + 8 * (self.i_plan + p) for p in range(P)])
         self.plan_ptr = self.ctl_ptr + 8 * self.i_plan
         self.own_counts_ptr = self.ctl_ptr + 8 * self.i_own_counts
         self.a_tables = Pp([self.tables[p].weights for p in self.mine])
@@ -319,10 +323,15 @@ class PeerShardedStep:
         R, S, B, D, F, Q = self.R, self.S, self.B, self.D, self.F, self.Q
         self.marks = []
         self._mark("start")
-        rc = L.recd_dedup(F, self.a_gsizes, B, self.a_in_values, self.a_in_offsets, self.a_nvalues,
-                          self.a_inverse, self.a_uoffsets, self.a_uvalues, self.counts.data_ptr(),
-                          self.s_dedup.data_ptr(), self.s_dedup.numel(), s)
-        _lib.check(rc, "recd_dedup")
+        dd = (F, self.a_gsizes, B, self.a_in_values, self.a_in_offsets, self.a_nvalues,
+              self.a_inverse, self.a_uoffsets, self.a_uvalues, self.counts.data_ptr())
+        fused = S == 1  # the gather of the unique values doubles as the ID dispatch
+        if fused:
+            rc = L.recd_dedup_number(*dd, self.s_dedup.data_ptr(), self.s_dedup.numel(), s)
+            _lib.check(rc, "recd_dedup_number")
+        else:
+            rc = L.recd_dedup(*dd, self.s_dedup.data_ptr(), self.s_dedup.numel(), s)
+            _lib.check(rc, "recd_dedup")
         self._mark("dedup")
         rc = L.recd_shard_count(F, S, B, self.a_uvalues, self.a_uoffsets, self.counts.data_ptr(),
                                 self.a_rowoff, self.totals.data_ptr(), self.s_count.data_ptr(),
@@ -331,9 +340,15 @@ class PeerShardedStep:
         self._mark("shard_count")
         self._exchange(s, True)
         self._mark("exchange_counts")
+        if fused:
+            # unique values gathered straight into the owners' ID lists (plan bases)
+            rc = L.recd_dedup_copy(*dd, self.a_dst_ids, self.a_id_base, self.s_dedup.data_ptr(),
+                                   self.s_dedup.numel(), s)
+            _lib.check(rc, "recd_dedup_copy")
         rc = L.recd_shard_dispatch(F, S, B, self.a_uvalues, self.a_uoffsets, self.counts.data_ptr(),
                                    self.a_rowoff, self.totals.data_ptr(), self.plan_ptr,
-                                   self.plan_ptr + 8 * self.P, self.a_dst_ids, self.a_dst_ro, s)
+                                   self.plan_ptr + 8 * self.P,
+                                   self.a_no_ids if fused else self.a_dst_ids, self.a_dst_ro, s)
         _lib.check(rc, "recd_shard_dispatch")
         self._exchange(s, False)
         self._mark("dispatch_ids")
