@@ -84,6 +84,7 @@ struct BwdParams {
   uint32_t* occ_keys;     // sorted occurrence IDs
   uint32_t* occ_vals;     // tag = (f << 24) | u
   int64_t* run_part;      // [total_rc_chunks] exclusive run counts (grad-output mode)
+  int64_t occ_blk0[RECD_MAX_FEAT + 1];  // k_occ: first block of each feature (capacity)
   // optional scatter of grad_u rows to peers (fused source -> owner push): row u
   // of feature f goes to gseg_dst[f][j] + (*gseg_row0[f][j] + u) * D, j < gsegs
   int gsegs;
@@ -188,36 +189,62 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
   }
 }
 
-// occurrence pairs: warp per unique row writes (ID, f*B+u) for its values
+// occurrence pairs (ID, (f << 24) | u) of every unique value, value-parallel:
+// block per 4096 unique values of a feature; the block finds its first unique
+// row with a 32-ary warp search, stages the unique offsets of the rows it
+// spans in shared memory, and consecutive threads handle consecutive values
+// (coalesced loads of the unique values, coalesced pair stores).
+constexpr int OC_CH = 4096;
+constexpr int OC_MAXR = 512;
 __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p, uint32_t* keys,
                                              uint32_t* vals) {
-  __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int f = 0; f < p.F; ++f) {
-      s_pref[f] = acc;
-      acc += p.counts[f];
-    }
-    s_pref[p.F] = acc;
+  int f = 0;
+  while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
+  const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * OC_CH;
+  const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
+  if (j0 >= NV) return;
+  const int64_t j1 = min(NV, j0 + (int64_t)OC_CH);
+  const int tid = threadIdx.x;
+  const int64_t* uo = p.uoffsets[f];
+  const int64_t* src = p.uvalues[f];
+  const int64_t dst = p.ts_base[p.feat_ts[f]] + p.feat_base[f];
+  __shared__ int64_t s_u0;
+  __shared__ int64_t s_uo[OC_MAXR + 1];
+  if (tid < 32) {
+    const int64_t u = warp_last_le(uo, U, j0, tid);
+    if (tid == 0) s_u0 = u;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t total = s_pref[p.F];
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
-       w += nwarps) {
-    const int f = find_seg(s_pref, p.F, w);
-    const int64_t u = w - s_pref[f];
-    const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
-    const int64_t* uo = p.uoffsets[f];
-    const int64_t a = uo[u], e = (u + 1 < U) ? uo[u + 1] : NV;
-    const int64_t dst = p.ts_base[p.feat_ts[f]] + p.feat_base[f];
-    const uint32_t tag = ((uint32_t)f << 24) | (uint32_t)u;
-    const int64_t* vals_f = p.uvalues[f];
-    for (int64_t j = a + lane; j < e; j += 32) {
-      keys[dst + j] = (uint32_t)vals_f[j];
-      vals[dst + j] = tag;
+  int64_t u0 = s_u0;
+  while (true) {
+    const int nr = (int)min((int64_t)OC_MAXR, U - u0);
+    for (int t = tid; t <= nr; t += 256) {
+      const int64_t u = u0 + t;
+      s_uo[t] = (u < U) ? uo[u] : NV;
     }
+    __syncthreads();
+    const int64_t covered = s_uo[nr];
+    const int64_t qa = max(j0, s_uo[0]), qb = min(j1, covered);
+    int r = 0;
+    for (int64_t q = qa + tid; q < qb; q += 256) {
+      // row of q: short forward walk from the previous value's row (q moved
+      // by one block stride), binary search only past 8 rows
+      if (s_uo[min(r + 8, nr)] <= q) {
+        int lo = r + 8, hi = nr - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_uo[mid] <= q) lo = mid; else hi = mid - 1;
+        }
+        r = lo;
+      } else {
+        while (s_uo[r + 1] <= q) ++r;
+      }
+      keys[dst + q] = (uint32_t)__ldg(src + q);
+      vals[dst + q] = ((uint32_t)f << 24) | (uint32_t)(u0 + r);
+    }
+    if (covered >= j1) break;
+    __syncthreads();
+    u0 += nr;
   }
 }
 
@@ -258,6 +285,10 @@ __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t
 #define RECD_SC_RS 8
 #endif
 constexpr int SC_RS = RECD_SC_RS;  // table rows prefetched ahead per warp (shared-memory ring)
+#ifndef RECD_SC_BATCH
+#define RECD_SC_BATCH 8
+#endif
+constexpr int SC_BATCH = RECD_SC_BATCH;  // unique-row gradient gathers in flight per warp
 
 // One warp per (chunk of RC sorted positions, column block).  Runs of equal
 // IDs that start in the chunk are reduced in position order (== ascending
@@ -347,16 +378,16 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
     int32_t bnd = (nruns > 1) ? (int32_t)starts[1] : pe;  // end of run r
     float acc[V];
     C::zero(acc);
-    float x[8][V];
-    for (int32_t k0 = starts[0]; k0 < pe; k0 += 8) {
-      if (k0 + 8 > wbase + 32) {
+    float x[SC_BATCH][V];
+    for (int32_t k0 = starts[0]; k0 < pe; k0 += SC_BATCH) {
+      if (k0 + SC_BATCH > wbase + 32) {
         __syncwarp();
         wbase = k0;
         win[lane] = (k0 + lane < pe) ? __ldg(Vl + k0 + lane) : 0u;
         __syncwarp();
       }
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+      for (int t = 0; t < SC_BATCH; ++t) {
         const uint32_t vv = win[k0 + t - wbase];
         const float* gp = SINGLE ? gs + (uint64_t)(vv & 0xffffffu) * D32
                                  : p.grow[vv >> 24] + lo_f + (uint64_t)(vv & 0xffffffu) * D32;
@@ -374,7 +405,7 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
         }
       }
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+      for (int t = 0; t < SC_BATCH; ++t) {
         if (k0 + t < pe) {
 #pragma unroll
           for (int e = 0; e < V; ++e) acc[e] = __fadd_rn(acc[e], x[t][e]);
@@ -675,7 +706,13 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     }
     // 3-4. occurrences, sorted by ID per table segment
     if (do_scatter) {
-      k_occ<<<num_sms() * 4, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
+      int64_t ob = 0;
+      for (int f = 0; f < F; ++f) {
+        p.occ_blk0[f] = ob;
+        ob += std::max<int64_t>(1, ceil_div(do_scatter ? value_caps[f] : 1, OC_CH));
+      }
+      p.occ_blk0[F] = ob;
+      k_occ<<<(unsigned)ob, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
       note_launch();
       std::vector<SegDesc> segs;
       for (int s = 0; s < pl.nts; ++s) segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});

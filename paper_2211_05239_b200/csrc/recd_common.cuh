@@ -190,6 +190,23 @@ __device__ __forceinline__ int64_t block_inclusive_max(int64_t v, int64_t* smem,
   return r;
 }
 
+// Last index k in [0, n) with a[k] <= x for a non-decreasing a with a[0] <= x,
+// found by the whole warp with 32-ary probing (every lane returns it).
+__device__ __forceinline__ int64_t warp_last_le(const int64_t* a, int64_t n, int64_t x, int lane) {
+  // last index k in [0, n) with a[k] <= x (a non-decreasing, a[0] <= x)
+  int64_t lo = 0, hi = n;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t k = lo + (int64_t)lane * step;
+    const bool le = k < hi && a[k] <= x;
+    const unsigned b = __ballot_sync(0xffffffffu, le);
+    const int last = 31 - __clz(b);  // lane 0 always qualifies
+    lo = lo + (int64_t)last * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
 // Scratch arena carving helper (256-byte aligned sub-buffers).
 struct Arena {
   char* base;

@@ -524,20 +524,6 @@ constexpr int CP_IT = 16;
 constexpr int CP_CH = CP_NT * CP_IT;  // unique values per block
 constexpr int CP_MAXR = 512;          // rows staged per pass
 
-__device__ __forceinline__ int64_t warp_last_le(const int64_t* a, int64_t n, int64_t x, int lane) {
-  // last index k in [0, n) with a[k] <= x (a non-decreasing, a[0] <= x)
-  int64_t lo = 0, hi = n;  // answer in [lo, hi)
-  while (hi - lo > 1) {
-    const int64_t step = (hi - lo + 31) / 32;
-    const int64_t k = lo + (int64_t)lane * step;
-    const bool le = k < hi && a[k] <= x;
-    const unsigned b = __ballot_sync(0xffffffffu, le);
-    const int last = 31 - __clz(b);  // lane 0 always qualifies
-    lo = lo + (int64_t)last * step;
-    hi = min(hi, lo + step);
-  }
-  return lo;
-}
 
 __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupParams p) {
   int f = 0;
@@ -576,12 +562,18 @@ __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupPar
     // value by a search over the staged rows, starting from the previous one
     int r = 0;
     for (int64_t q = qa + tid; q < qb; q += CP_NT) {
-      int lo = r, hi = nr - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_uo[mid] <= q) lo = mid; else hi = mid - 1;
+      // row of q: short forward walk from the previous value's row (q moved
+      // by one block stride), binary search only past 8 rows
+      if (s_uo[min(r + 8, nr)] <= q) {
+        int lo = r + 8, hi = nr - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_uo[mid] <= q) lo = mid; else hi = mid - 1;
+        }
+        r = lo;
+      } else {
+        while (s_uo[r + 1] <= q) ++r;
       }
-      r = lo;
       const int64_t v = __ldg(src + s_so[r] + (q - s_uo[r]));
       dst[q] = v;
       if (rdst) rdst[q] = v;
