@@ -592,6 +592,16 @@ def run_sharded(args, world, rank, local, dev):
     sent += 4 * D * int(recv_rows.sum())  # partial pooled rows returned
     sent += 4 * D * int(send_rows.sum())  # unique-row gradients (one copy per shard)
     N_kjt = int(sum(caps.values()))
+    # the reference's all-to-all accounting (trainer_sim.sdd,
+    # tensors.slice_stream_bytes) for this rank's batch -- canonical wire bytes of
+    # every (offsets, values) slice sent, dedup vs KJT, and the pooled rows back
+    a2a_fwd_dedup = sum(16 + 8 * (U[f] + N_u[f]) for f in range(len(keys)))
+    a2a_fwd_kjt = sum(16 + 8 * (args.batch + int(caps[k])) for k in keys)
+    a2a = {"fwd_bytes_dedup": a2a_fwd_dedup, "fwd_bytes_kjt": a2a_fwd_kjt,
+           "fwd_reduction": a2a_fwd_kjt / max(a2a_fwd_dedup, 1),
+           "back_bytes_dedup": 4 * D * int(sum(U)), "back_bytes_kjt": 4 * D * args.batch * len(keys),
+           "definition": "trainer_sim.sdd / a2a_bytes_back (trainer_sim.py:281-305, 557, 573) on rank 0's "
+                         "batch; the inverse never travels"}
 
     e2e = None
     if not args.no_e2e and not args.profile:
@@ -613,7 +623,7 @@ def run_sharded(args, world, rank, local, dev):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 (ids int64)", "data": "synthetic (restated reference session generator)",
             "config": cfg, "phases_ms": ph,
-            "comm_bytes_sent_per_rank": sent,
+            "comm_bytes_sent_per_rank": sent, "a2a_accounting_rank0": a2a,
             "stats_rank0": {"N_kjt": N_kjt, "N_u": int(sum(N_u)), "U_tot": int(sum(U))},
             "roofline": None, "cpu_baseline": None, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
