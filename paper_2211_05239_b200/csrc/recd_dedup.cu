@@ -95,9 +95,15 @@ __device__ __forceinline__ uint64_t finalize_hash(uint64_t h, uint64_t mask) {
 // same position of the previous row (q - len; an L1 hit for rows shorter
 // than a tile).  Only run heads need a content hash, and they are ~20% of the
 // rows of a session-clustered batch, so hashing is deferred to k_insert.
+#ifndef RECD_RS_RPB
+#define RECD_RS_RPB 256
+#endif
+#ifndef RECD_RS_IT
+#define RECD_RS_IT 8
+#endif
 constexpr int RS_NT = 256;
-constexpr int RS_RPB = 256;
-constexpr int RS_IT = 8;  // consecutive values per thread
+constexpr int RS_RPB = RECD_RS_RPB;  // rows per block
+constexpr int RS_IT = RECD_RS_IT;    // consecutive values per thread
 
 __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ DedupParams p) {
   const int g = p.rs_group[blockIdx.y];
