@@ -11,15 +11,18 @@ shrinks by the dedupe factor and commutes with the expansion
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import time
+from dataclasses import dataclass, field, replace
 from typing import Mapping, Sequence
 
+import numpy as np
 import torch
 
 from . import _lib
-from .tensors import IKJT, KJT, JaggedTensor
+from .tensors import IKJT, KJT, JaggedTensor, build_kjt, kjt_to_ikjts
 
-__all__ = ["Transform", "apply_transform", "process"]
+__all__ = ["Transform", "apply_transform", "DataloaderSpec", "ReaderBatch", "StageTimings",
+           "convert", "process", "process_tensors"]
 
 _OPS = {"identity": 0, "mod_hash": 1, "clamp": 2}
 
@@ -67,8 +70,8 @@ def apply_transform(values: torch.Tensor | JaggedTensor, t: Transform):
     return _run([(values, t)])[0]
 
 
-def process(kjts: Mapping[str, JaggedTensor], ikjts: Sequence[IKJT],
-            transforms: Sequence[Transform]) -> tuple[dict[str, JaggedTensor], list[IKJT]]:
+def process_tensors(kjts: Mapping[str, JaggedTensor], ikjts: Sequence[IKJT],
+                    transforms: Sequence[Transform]) -> tuple[dict[str, JaggedTensor], list[IKJT]]:
     """The transform stage of reader.process (reader.py:178-217): transforms of
     a key run in order; IKJT features are transformed on their unique values
     and the inverse is kept.  Raises like the reference for unknown keys."""
@@ -94,3 +97,101 @@ def process(kjts: Mapping[str, JaggedTensor], ikjts: Sequence[IKJT],
                       {k: cur[("i", i, k)] for k in ik.per_feature}, validate=False)
                  for i, ik in enumerate(ikjts)]
     return new_kjts, new_ikjts
+
+
+@dataclass(frozen=True)
+class DataloaderSpec:
+    """reader.DataloaderSpec (reader.py:86-121): keys, dedup groups, transforms."""
+
+    keys: tuple[str, ...]
+    dedup_sparse_features: tuple[tuple[str, ...], ...]
+    transforms: tuple[Transform, ...] = ()
+    batch_size: int = 4096
+
+    def __post_init__(self) -> None:
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+        seen: set[str] = set()
+        for group in self.dedup_sparse_features:
+            if not group:
+                raise ValueError("empty dedup group")
+            for key in group:
+                if key in seen:
+                    raise ValueError(f"feature {key!r} in more than one dedup group")
+                if key not in self.keys:
+                    raise ValueError(f"grouped feature {key!r} not in keys")
+                seen.add(key)
+        for t in self.transforms:
+            if t.key not in self.keys:
+                raise ValueError(f"transform targets unknown key {t.key!r}")
+
+    @property
+    def plain_keys(self) -> tuple[str, ...]:
+        grouped = {k for g in self.dedup_sparse_features for k in g}
+        return tuple(k for k in self.keys if k not in grouped)
+
+    def without_dedup(self) -> "DataloaderSpec":
+        """The baseline spec: same keys and transforms, no dedup groups."""
+        return replace(self, dedup_sparse_features=())
+
+
+@dataclass
+class StageTimings:
+    fill_s: float = 0.0
+    convert_s: float = 0.0
+    process_s: float = 0.0
+
+    @property
+    def total_s(self) -> float:
+        return self.fill_s + self.convert_s + self.process_s
+
+
+@dataclass
+class ReaderBatch:
+    """reader.ReaderBatch (reader.py:136-150) on device tensors."""
+
+    batch_size: int
+    kjts: dict[str, JaggedTensor]
+    ikjts: list[IKJT]
+    labels: np.ndarray
+    stage_timings: StageTimings = field(default_factory=StageTimings)
+    bytes_in: int = 0
+    bytes_out: int = 0
+
+    def all_keys(self) -> tuple[str, ...]:
+        keys = list(self.kjts)
+        for ikjt in self.ikjts:
+            keys.extend(ikjt.group_keys)
+        return tuple(keys)
+
+
+def convert(rows, spec: DataloaderSpec) -> ReaderBatch:
+    """reader.convert (reader.py:160-175): one IKJT per dedup group, one plain
+    jagged tensor per remaining key.  The records are packed once in native
+    code (all keys), copied to the GPU, and every group is deduplicated in one
+    batched recd_dedup."""
+    if not rows:
+        raise ValueError("convert needs a non-empty row batch")
+    t0 = time.perf_counter()
+    keys = list(spec.keys)
+    kjt = build_kjt(rows, keys)
+    groups = [list(g) for g in spec.dedup_sparse_features]
+    ikjts = kjt_to_ikjts(kjt, groups) if groups else []
+    kjts = {k: kjt.entries[k] for k in spec.plain_keys}
+    labels = np.fromiter((r.label for r in rows), dtype=np.int64, count=len(rows))
+    batch = ReaderBatch(batch_size=len(rows), kjts=kjts, ikjts=ikjts, labels=labels)
+    torch.cuda.synchronize()
+    batch.stage_timings.convert_s = time.perf_counter() - t0
+    return batch
+
+
+def process(batch: ReaderBatch, transforms: Sequence[Transform]) -> ReaderBatch:
+    """reader.process (reader.py:178-217): element-wise transforms; IKJT features
+    are transformed on their deduplicated values only and stay IKJTs."""
+    t0 = time.perf_counter()
+    kjts, ikjts = process_tensors(batch.kjts, batch.ikjts, transforms)
+    out = ReaderBatch(batch_size=batch.batch_size, kjts=kjts, ikjts=ikjts, labels=batch.labels,
+                      stage_timings=batch.stage_timings, bytes_in=batch.bytes_in,
+                      bytes_out=batch.bytes_out)
+    out.stage_timings.process_s += time.perf_counter() - t0
+    return out

@@ -12,7 +12,8 @@ from conftest import golden
 pytestmark = pytest.mark.gpu
 
 import paper_2211_05239_b200 as R  # noqa: E402
-from paper_2211_05239_b200.reader import Transform, apply_transform, process  # noqa: E402
+from paper_2211_05239_b200.reader import (DataloaderSpec, Transform, apply_transform, convert,  # noqa: E402
+                                          process, process_tensors)
 
 
 def test_transforms_match_reference_golden():
@@ -31,7 +32,7 @@ def test_transform_errors_like_reference():
         Transform("mod_hash", "k", 0)
     kjt = R.KJT(2, {"a": R.JaggedTensor(np.array([1, 2], np.int64), np.array([0, 1], np.int64))})
     with pytest.raises(ValueError, match="transform targets missing key 'zz'"):
-        process(kjt.entries, [], [Transform("clamp", "zz", 3)])
+        process_tensors(kjt.entries, [], [Transform("clamp", "zz", 3)])
 
 
 def test_transform_commutes_with_expansion():
@@ -49,10 +50,40 @@ def test_transform_commutes_with_expansion():
     ik = R.kjt_to_ikjt(kjt, ["h"])
     ts = [Transform("mod_hash", "h", 1_000_003), Transform("clamp", "h", 500_000),
           Transform("mod_hash", "p", 97)]
-    plain, [ik2] = process({"p": kjt.entries["p"]}, [ik], ts)
+    plain, [ik2] = process_tensors({"p": kjt.entries["p"]}, [ik], ts)
     expanded = R.ikjt_to_kjt(ik2).entries["h"]
-    ref_h, _ = process({"h": kjt.entries["h"]}, [], ts[:2])
+    ref_h, _ = process_tensors({"h": kjt.entries["h"]}, [], ts[:2])
     assert R.jt_equal(expanded, ref_h["h"])
     assert torch.equal(ik2.inverse_lookup, ik.inverse_lookup)
     ref_p = apply_transform(kjt.entries["p"], ts[2])
     assert R.jt_equal(plain["p"], ref_p)
+
+
+def test_reader_convert_process_like_reference():
+    """reader.convert + reader.process (reader.py:160-217) on records with
+    labels: groups become IKJTs equal to build_ikjt, plain keys stay jagged,
+    transforms hit unique values only."""
+    import oracle
+    from types import SimpleNamespace
+    rng = np.random.default_rng(9)
+    rows, state = [], None
+    for i in range(700):
+        if state is None or rng.random() > 0.8:
+            state = {k: rng.integers(0, 1000, size=int(rng.integers(0, 9))).tolist() for k in ("a", "b", "c")}
+        rows.append(SimpleNamespace(features=dict(state), label=i % 2))
+    spec = DataloaderSpec(keys=("a", "b", "c"), dedup_sparse_features=(("a", "b"),),
+                          transforms=(Transform("mod_hash", "a", 97),))
+    batch = convert(rows, spec)
+    assert batch.all_keys() == ("c", "a", "b")
+    np.testing.assert_array_equal(batch.labels, np.arange(700) % 2)
+    feats = [(np.array(sum([r.features["a"] for r in rows], []), np.int64),
+              np.cumsum([0] + [len(r.features["a"]) for r in rows[:-1]]).astype(np.int64)),
+             (np.array(sum([r.features["b"] for r in rows], []), np.int64),
+              np.cumsum([0] + [len(r.features["b"]) for r in rows[:-1]]).astype(np.int64))]
+    inv, outs = oracle.build_ikjt_arrays(feats)
+    np.testing.assert_array_equal(batch.ikjts[0].inverse_lookup.cpu().numpy(), inv)
+    out = process(batch, spec.transforms)
+    v, _ = out.ikjts[0].per_feature["a"].numpy()
+    np.testing.assert_array_equal(v, oracle.apply_transform(outs[0][0], "mod_hash", 97))
+    with pytest.raises(ValueError, match="feature 'a' in more than one dedup group"):
+        DataloaderSpec(keys=("a", "b"), dedup_sparse_features=(("a",), ("a", "b")))
