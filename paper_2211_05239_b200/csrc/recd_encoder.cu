@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ Ge
   uint8_t* sB = smem;
   uint8_t* sA = smem + B_BYTES;
   uint8_t* sC = sA + 2 * A_STAGE;  // epilogue staging: 128 rows x 256 B, padded pitch
-  __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t mbar2[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int64_t M = 0;
@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ Ge
   if ((int64_t)blockIdx.x >= ntiles) return;
 
   if (warp == 0) umma::tmem_alloc<512>(&tmem_base);
-  if (tid == 0) umma::mbar_init(&mbar, 1);
+  if (tid == 0) {
+    umma::mbar_init(&mbar2[0], 1);
+    umma::mbar_init(&mbar2[1], 1);
+  }
   const uint32_t sB_addr = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_addr = (uint32_t)__cvta_generic_to_shared(sA);
   // B once: (row n, K block kb, 16-B chunk c)
@@ -158,25 +161,29 @@ __global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ Ge
     cp_async_wait<1>();  // B and this tile's A (this thread's copies)
     umma::fence_proxy_async();
     __syncthreads();
+    // two MMA groups, each committed to its own mbarrier: columns [0, 128)
+    // first, so the epilogue of that chunk overlaps the MMAs of the rest
+    constexpr int NH = N < 128 ? N : 128;
     if (tid == 0) {
       umma::fence_after_sync();
 #pragma unroll
-      for (int kb = 0; kb < KB; ++kb)
+      for (int grp = 0; grp < 2; ++grp) {
+        const int cbeg = grp == 0 ? 0 : NH, cend = grp == 0 ? NH : N;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // UMMA_K = 16 bf16 = 32 B along the swizzled row
-          const uint64_t ad = umma::smem_desc_sw128_kmajor(sA_addr + stage * A_STAGE + kb * 16384 + k * 32);
+        for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
-          for (int n0 = 0; n0 < N; n0 += 256) {
-            constexpr int NC0 = N < 256 ? N : 256;
-            const int nc = (N - n0) < NC0 ? (N - n0) : NC0;
-            const uint64_t bd = umma::smem_desc_sw128_kmajor(sB_addr + kb * N * 128 + n0 * 128 + k * 32);
-            umma::mma_bf16(tmem + n0, ad, bd, umma::idesc_bf16_f32(128, nc), (kb | k) != 0);
+          for (int k = 0; k < 4; ++k) {  // UMMA_K = 16 bf16 = 32 B along the swizzled row
+            const uint64_t ad = umma::smem_desc_sw128_kmajor(sA_addr + stage * A_STAGE + kb * 16384 + k * 32);
+            for (int n0 = cbeg; n0 < cend; n0 += 256) {
+              const int nc = (cend - n0) < 256 ? (cend - n0) : 256;
+              const uint64_t bd = umma::smem_desc_sw128_kmajor(sB_addr + kb * N * 128 + n0 * 128 + k * 32);
+              umma::mma_bf16(tmem + n0, ad, bd, umma::idesc_bf16_f32(128, nc), (kb | k) != 0);
+            }
           }
-        }
-      umma::commit(&mbar);
+        if (grp == 0 || NH < N) umma::commit(&mbar2[grp]);
+      }
     }
-    umma::mbar_wait(&mbar, phase);
-    phase ^= 1;
+    umma::mbar_wait(&mbar2[0], phase);
     umma::fence_after_sync();
     const int lq = warp & 3;  // TMEM lane quarter of this warp
     const int r = lq * 32 + lane;  // tile row of this thread
@@ -185,6 +192,10 @@ __global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ Ge
     uint8_t* srow = sC + r * GM_CPITCH + h * 128;
 #pragma unroll 1
     for (int c0 = 0; c0 < N; c0 += 128) {
+      if (c0 == NH && NH < N) {  // the remaining columns' MMAs
+        umma::mbar_wait(&mbar2[1], phase);
+        umma::fence_after_sync();
+      }
       const int cb = c0 + h * 64;  // 64 columns of this thread
       if (cb < N) {
         // staging row segment free again (this thread's previous bulk store read it)
@@ -213,6 +224,7 @@ __global__ void __launch_bounds__(GM_NT, 1) k_gemm_tn(const __grid_constant__ Ge
         }
       }
     }
+    phase ^= 1;
     umma::fence_before_sync();
     __syncthreads();  // TMEM drained and the A stage free before the next tile's MMAs / loads
   }
