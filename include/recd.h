@@ -27,6 +27,7 @@
  *   recd_jagged_index_select_* <- tensors.jagged_index_select   (tensors.py:363-390)
  *                                 and ikjt_to_kjt (tensors.py:393-399)
  *   recd_slice_renumber        <- trainer_sim.slice_ikjt_rows   (trainer_sim.py:394-413)
+ *   recd_partial_ikjt          <- tensors.build_partial_ikjt    (tensors.py:311-360)
  *
  * Conventions
  *   - Jagged features use the reference layout: int64 values[N] and one int64
@@ -456,6 +457,20 @@ size_t recd_slice_scratch_bytes(int64_t num_unique, int64_t num_rows);
 int recd_slice_renumber(const int64_t* inverse, int64_t start, int64_t stop, int64_t num_unique,
                         int64_t* new_inverse_out, int64_t* order_out, int64_t* count_out,
                         void* scratch, size_t scratch_bytes, recd_stream_t stream);
+
+/* ------------------------------------------------------- partial IKJT ---
+ * build_partial_ikjt (tensors.py:311-360) of one key, from recd_dedup's
+ * unique rows (uvalues / uoffsets = row starts, num_uvalues values) and its
+ * inverse lookup: values_out[0 .. *num_values_out) is the shared value buffer
+ * (capacity num_uvalues), windows_out[2 i], [2 i + 1] = (offset, length) of
+ * batch row i, bit-exact with the reference's greedy batch-order encoder.
+ * Synchronises `stream` once per speculation round (*rounds_out, nullable).
+ */
+size_t recd_partial_ikjt_scratch_bytes(int64_t num_unique, int64_t num_uvalues);
+int recd_partial_ikjt(int64_t batch_size, int64_t num_unique, const int64_t* uvalues,
+                      const int64_t* uoffsets, int64_t num_uvalues, const int64_t* inverse,
+                      int64_t* values_out, int64_t* windows_out, int64_t* num_values_out,
+                      int64_t* rounds_out, void* scratch, size_t scratch_bytes, recd_stream_t stream);
 
 #ifdef __cplusplus
 }

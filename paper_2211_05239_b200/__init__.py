@@ -11,6 +11,9 @@ from .tensors import (  # noqa: F401
     IKJT,
     KJT,
     JaggedTensor,
+    PartialIKJT,
+    build_partial_ikjt,
+    kjt_to_partial_ikjt,
     build_ikjt,
     build_kjt,
     ikjt_to_kjt,

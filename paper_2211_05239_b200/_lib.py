@@ -105,6 +105,8 @@ _SIGS = {
                                              _vp]),
     "recd_slice_scratch_bytes": (_sz, [_i64, _i64]),
     "recd_slice_renumber": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "recd_partial_ikjt_scratch_bytes": (_sz, [_i64, _i64]),
+    "recd_partial_ikjt": (_i32, [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _p64, _p64, _vp, _sz, _vp]),
 }
 
 EXPORTS = tuple(_SIGS)

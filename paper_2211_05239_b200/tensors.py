@@ -12,11 +12,14 @@ conversion runs in librecd's sm_100a kernels:
   ikjt_to_kjt(ikjt)            tensors.py:393-399  -> recd_jagged_index_select_*
   jagged_index_select(jt, idx) tensors.py:363-390  -> recd_jagged_index_select_*
   slice_ikjt_rows / split_ikjt trainer_sim.py:394-446 -> recd_slice_renumber
+  build_partial_ikjt(rows, key) tensors.py:311-360  -> recd_dedup + recd_partial_ikjt
 """
 
 from __future__ import annotations
 
 from typing import Iterable, Mapping, Sequence
+
+import ctypes
 
 import numpy as np
 import torch
@@ -35,6 +38,9 @@ __all__ = [
     "jagged_index_select",
     "slice_ikjt_rows",
     "split_ikjt",
+    "PartialIKJT",
+    "build_partial_ikjt",
+    "kjt_to_partial_ikjt",
     "jt_equal",
     "kjt_equal",
     "default_device",
@@ -377,3 +383,67 @@ def split_ikjt(ikjt: IKJT, num_ranks: int) -> list[IKJT]:
         out.append(slice_ikjt_rows(ikjt, start, stop))
         start = stop
     return out
+
+
+# --------------------------------------------------------- partial IKJT
+class PartialIKJT:
+    """Single-feature shift-aware encoding (tensors.py:194-225): rows are
+    (offset, length) windows into one shared value buffer."""
+
+    def __init__(self, feature_key: str, values, windows, *, validate: bool = True):
+        dev = values.device if isinstance(values, torch.Tensor) and values.is_cuda else default_device()
+        self.feature_key = feature_key
+        self.values = _as_ids(values, dev)
+        w = windows if isinstance(windows, torch.Tensor) else torch.as_tensor(
+            np.asarray(windows, dtype=np.int64))
+        self.windows = w.to(device=dev, dtype=torch.int64).contiguous()
+        if not validate:
+            return
+        if self.windows.dim() != 2 or self.windows.shape[1] != 2:
+            raise ValueError("windows must be a (B, 2) array")
+        if self.windows.numel():
+            if bool((self.windows[:, 0] + self.windows[:, 1] > self.values.numel()).any()):
+                raise ValueError("window exceeds value buffer")
+            if bool((self.windows < 0).any()):
+                raise ValueError("negative window bound")
+
+    @property
+    def row_count(self) -> int:
+        return int(self.windows.shape[0])
+
+    def row(self, i: int) -> torch.Tensor:
+        off, length = (int(x) for x in self.windows[i].tolist())
+        return self.values[off:off + length]
+
+
+def kjt_to_partial_ikjt(kjt: KJT, key: str, ikjt: IKJT | None = None) -> PartialIKJT:
+    """build_partial_ikjt on a KJT already on the GPU (recd_dedup of the key,
+    then recd_partial_ikjt over its unique rows).  `ikjt` may pass an existing
+    exact dedup of the key to skip the first step."""
+    if ikjt is None:
+        ikjt = kjt_to_ikjt(kjt, [key])
+    lib = _lib.load()
+    jt = ikjt.per_feature[key]
+    dev = jt.device
+    B, U, nval = ikjt.batch_size, jt.row_count, int(jt.values.numel())
+    values = torch.empty(max(nval, 1), dtype=torch.int64, device=dev)
+    windows = torch.empty((B, 2), dtype=torch.int64, device=dev)
+    scratch = _lib.Workspace.get(lib.recd_partial_ikjt_scratch_bytes(U, nval), dev, "partial")
+    n_out, rounds = ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = lib.recd_partial_ikjt(B, U, jt.values.data_ptr(), jt.offsets.data_ptr(), nval,
+                               ikjt.inverse_lookup.data_ptr(), values.data_ptr(), windows.data_ptr(),
+                               ctypes.byref(n_out), ctypes.byref(rounds), scratch.data_ptr(),
+                               scratch.numel(), _lib.stream_ptr(dev))
+    _lib.check(rc, "recd_partial_ikjt")
+    out = PartialIKJT(key, values[: n_out.value], windows, validate=False)
+    out.rounds = int(rounds.value)
+    return out
+
+
+def build_partial_ikjt(rows: Sequence, key: str, device=None) -> PartialIKJT:
+    """tensors.py:311-338: greedy batch-order shift-aware encoding of one
+    feature -- reuse the leftmost window equal to the row, else append the
+    row minus its longest prefix matching the buffer's suffix."""
+    if len(rows) == 0:
+        raise ValueError("empty batch")
+    return kjt_to_partial_ikjt(build_kjt(rows, [key], device), key)

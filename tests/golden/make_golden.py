@@ -4,7 +4,7 @@ Run in the build container (where `/root/reference` exists):
 
     python tests/golden/make_golden.py
 
-Writes `tests/golden/{dedup,pool,jagged,slice,datagen,errors}.npz`.  These
+Writes `tests/golden/{dedup,pool,jagged,slice,datagen,errors,transforms,wire,partial}.npz`.  These
 fixtures pin the oracle restatement (`oracle/`) and the CUDA path; the GPU box
 never needs `/root/reference`.
 """
@@ -282,7 +282,58 @@ def make_wire():
     np.savez_compressed(OUT / "wire.npz", **store)
 
 
+def shifted_sessions(rng, b, vocab, max_len, p_shift=(0.5, 0.35, 0.15), mean_session=8.0):
+    """Session-structured rows of one key: each session draws a length and a
+    value pool; consecutive rows shift the window by 0, 1 or 2 (the reference
+    datagen's shift model, datagen.py:149-183, with 2-shifts added)."""
+    rows = []
+    while len(rows) < b:
+        n = int(rng.integers(0, max_len + 1))
+        count = 1 + int(rng.poisson(mean_session - 1))
+        shifts = np.concatenate([[0], np.cumsum(rng.choice(3, size=count - 1, p=p_shift))]).astype(np.int64)
+        pool = rng.integers(-vocab // 4, vocab, size=n + int(shifts[-1]))
+        for s in shifts[: b - len(rows)]:
+            rows.append({"f": pool[s:s + n].tolist()})
+    return rows
+
+
+def make_partial():
+    """Partial IKJT (tensors.py:311-360) of the real reference: values + windows."""
+    rng = np.random.default_rng(17)
+    cases = {
+        "p0": [[3, 4, 5], [4, 5, 6], [3, 4, 5]],
+        "p1": [[3, 4, 5], [4, 5, 6], [1], []],
+        "p2": [[9, 9], [9, 9]],
+        "p4": [[1, 2, 3, 4, 5], [2, 3], [3, 4, 5], [5], [4, 5, 6], [1, 2], [6, 7], [], [7], [5, 6, 7, 8]],
+        "p5": [[1], [2], [1, 2, 3], [3], [2, 3, 4, 5], [9], [3, 4, 5, 9, 1], [4, 5, 9, 1, 7], [1, 7]],
+        "p6": [[]] * 5,
+        "p9": [[-(2 ** 63), 2 ** 63 - 1], [2 ** 63 - 1, 0], [0, -(2 ** 63)], [-(2 ** 63), 2 ** 63 - 1, 0]],
+    }
+    pool = rng.integers(0, 10_000, size=400, dtype=np.int64)
+    rows, start = [], 0
+    for _ in range(40):
+        start += int(rng.integers(0, 3))
+        rows.append(pool[start:start + 20].tolist())
+    cases["p3"] = rows
+    cases["p7"] = [rng.integers(-1, 3, size=int(rng.integers(0, 7))).tolist() for _ in range(300)]
+    cases["p8"] = [r["f"] for r in shifted_sessions(rng, 400, 50, 12)]
+    cases["p10"] = [r["f"] for r in shifted_sessions(rng, 2000, 1 << 40, 64)]
+    cases["p11"] = [r["f"] for r in shifted_sessions(rng, 1500, 6, 9, p_shift=(0.2, 0.5, 0.3), mean_session=4.0)]
+    store = {}
+    for name, lists in cases.items():
+        recs = [{"f": x} for x in lists]
+        kjt = T.build_kjt(recs, ["f"])
+        pk = T.build_partial_ikjt(recs, "f")
+        store[f"{name}/in_values"] = np.array(kjt.entries["f"].values)
+        store[f"{name}/in_offsets"] = np.array(kjt.entries["f"].offsets)
+        store[f"{name}/values"] = np.array(pk.values)
+        store[f"{name}/windows"] = np.array(pk.windows)
+    store["names"] = np.array(list(cases))
+    np.savez_compressed(OUT / "partial.npz", **store)
+
+
 if __name__ == "__main__":
+    make_partial()
     make_wire()
     make_transforms()
     make_dedup()

@@ -116,3 +116,22 @@ def test_wire_oracle_matches_reference_golden():
         assert ik == d[f"{name}/ikjt_bytes"].tobytes()
         assert [oracle.wire.slice_stream_bytes(o, v) for v, o in outs] == list(d[f"{name}/slice_bytes"])
         assert [oracle.wire.values_stream_bytes(v) for v, _ in outs] == list(d[f"{name}/values_bytes"])
+
+
+def test_partial_oracle_matches_reference_golden():
+    """oracle/partial.py vs the real build_partial_ikjt (tests/golden/partial.npz):
+    worked examples, found substrings, overlaps deeper than the previous row,
+    int64 extremes, adversarial small vocabularies, session batches."""
+    from oracle.partial import build_partial_jagged
+    d = golden("partial")
+    for name in d["names"]:
+        name = str(name)
+        v, w = build_partial_jagged(d[f"{name}/in_values"], d[f"{name}/in_offsets"])
+        np.testing.assert_array_equal(v, d[f"{name}/values"], err_msg=name)
+        np.testing.assert_array_equal(w, d[f"{name}/windows"], err_msg=name)
+
+
+def test_partial_oracle_empty_batch():
+    from oracle.partial import build_partial
+    with pytest.raises(ValueError, match="empty batch"):
+        build_partial([])
