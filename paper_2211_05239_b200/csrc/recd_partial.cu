@@ -19,8 +19,8 @@
 //     appended lengths, and one parallel copy build the whole buffer.
 // A verification pass then checks each speculated row against the buffer
 // prefix it would have seen, E_u elements long: (i) no aligned occurrence in
-// buffer[0, E_u) (candidates from a radix-sorted (hash(value), position)
-// index of the buffer), (ii) no longer overlap k > |a| reaching past the
+// buffer[0, E_u) (candidates: the buffer positions in hash(T[0])'s bucket of a
+// CSR index built by counting atomics + a scan), (ii) no longer overlap k > |a| reaching past the
 // previous row.  The first failing row u* has a correct prefix in front of
 // it, so its true decision (found at p / overlap k) is pinned and the next
 // round re-speculates the rows after it.  Session-structured batches verify
@@ -30,7 +30,9 @@
 // Layout: uvalues/uoffsets are recd_dedup's unique rows of the key (offsets
 // are row starts), `inverse` its inverse lookup.  Output: the buffer in
 // values_out (capacity num_uvalues >= final length), windows_out[B][2],
-// *num_values_out (host).  The call synchronises the stream once per round.
+// *num_values_out (host).  The call synchronises the stream once per round
+// (one 16-byte read: buffer length + first failing row); the windows kernel
+// is left enqueued.
 #include <algorithm>
 
 #include "recd_common.cuh"
@@ -52,14 +54,15 @@ struct PartialParams {
   int64_t* prevn;      // length of the previous appended row (0: none)
   int64_t* ustart;     // window start per unique row
   int64_t* buf;        // the value buffer (values_out)
-  uint32_t* hkey;      // index of the buffer: hash(value), position
-  uint32_t* hpos;
-  const uint32_t* skey;  // sorted index (hkey/hpos or their alt buffers)
-  const uint32_t* spos;
+  // index of the buffer: positions bucketed by hash(value) (CSR)
+  int64_t nb;            // buckets (power of two)
+  int64_t* bstart;       // counts, then (exclusive scan) bucket starts
+  int32_t* bcur;         // fill cursor per bucket
+  uint32_t* bidx;        // positions, grouped by bucket
   const int64_t* total;  // device: buffer length
   int32_t* res_kind;
   int64_t* res_val;
-  unsigned long long* fail;  // first failing unique row
+  unsigned long long* fail;  // first failing unique row (ctl[1]; ctl[0] = total)
 };
 
 __device__ __forceinline__ int64_t pt_len(const PartialParams& p, int64_t u) {
@@ -142,9 +145,15 @@ __global__ void __launch_bounds__(PT_NT) k_pt_fill(const __grid_constant__ Parti
     const int64_t q = e + j - o;
     const int64_t v = T[j];
     p.buf[q] = v;
-    p.hkey[q] = pt_hash(v);
-    p.hpos[q] = (uint32_t)q;
+    atomicAdd(reinterpret_cast<unsigned long long*>(p.bstart + (pt_hash(v) & (p.nb - 1))), 1ull);
   }
+}
+
+__global__ void __launch_bounds__(PT_NT) k_pt_bucket(const __grid_constant__ PartialParams p) {
+  const int64_t q = (int64_t)blockIdx.x * PT_NT + threadIdx.x;
+  if (q >= *p.total) return;
+  const int64_t b = pt_hash(p.buf[q]) & (p.nb - 1);
+  p.bidx[p.bstart[b] + atomicAdd(p.bcur + b, 1)] = (uint32_t)q;
 }
 
 __global__ void __launch_bounds__(PT_NT) k_pt_verify(const __grid_constant__ PartialParams p) {
@@ -158,38 +167,27 @@ __global__ void __launch_bounds__(PT_NT) k_pt_verify(const __grid_constant__ Par
   int kind = PK_NONE;
   int64_t val = 0;
   if (n <= e) {
-    // (i) leftmost aligned occurrence in buf[0, e): candidates share hash(T[0]),
-    // positions ascending within a key (stable sort of ascending positions)
-    const uint32_t key = pt_hash(T[0]);
-    const int64_t tot = *p.total;
-    int64_t lo = 0, hi = tot;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (p.skey[mid] < key) lo = mid + 1;
-      else hi = mid;
-    }
+    // (i) leftmost aligned occurrence in buf[0, e): every position of T[0]'s
+    // bucket is a candidate (unordered: the minimum matching one wins)
+    const int64_t b = pt_hash(T[0]) & (p.nb - 1);
+    const int64_t lo = p.bstart[b], hi = b + 1 < p.nb ? p.bstart[b + 1] : *p.total;
     const int64_t t0 = T[0];
-    for (int64_t i0 = lo; i0 < tot; i0 += 32) {
+    int64_t best = INT64_MAX;
+    for (int64_t i0 = lo; i0 < hi; i0 += 32) {
       const int64_t i = i0 + lane;
-      const bool inkey = i < tot && p.skey[i] == key;
-      const int64_t pos = inkey ? (int64_t)p.spos[i] : INT64_MAX;
-      const bool cand = inkey && pos + n <= e && p.buf[pos] == t0;
+      const int64_t pos = i < hi ? (int64_t)p.bidx[i] : INT64_MAX;
+      const bool cand = i < hi && pos + n <= e && p.buf[pos] == t0;
       unsigned m = __ballot_sync(0xffffffffu, cand);
-      bool done = false;
       while (m) {
         const int l = __ffs(m) - 1;
         m &= m - 1;
         const int64_t pp = __shfl_sync(0xffffffffu, pos, l);
-        if (warp_equal(p.buf + pp, T, n, lane)) {
-          kind = PK_FOUND;
-          val = pp;
-          done = true;
-          break;
-        }
+        if (pp < best && warp_equal(p.buf + pp, T, n, lane)) best = pp;
       }
-      // stop at the first found, past the key's range, or past e - n
-      const bool past = !inkey || pos + n > e;
-      if (done || __any_sync(0xffffffffu, past)) break;
+    }
+    if (best != INT64_MAX) {
+      kind = PK_FOUND;
+      val = best;
     }
   }
   if (kind == PK_NONE) {
@@ -235,8 +233,7 @@ struct PtLayout {
 };
 
 static size_t pt_carve(PartialParams* p, int64_t U, int64_t nval, void* scratch, size_t cap_bytes,
-                       uint32_t** alt_k, uint32_t** alt_v, uint32_t** hist, int64_t** part,
-                       int64_t** total) {
+                       int64_t** part, int64_t** total) {
   Arena a(scratch, cap_bytes);
   const int64_t cap = std::max<int64_t>(nval, 1), uu = std::max<int64_t>(U, 1);
   p->pin_kind = a.take<int32_t>(uu);
@@ -248,16 +245,14 @@ static size_t pt_carve(PartialParams* p, int64_t U, int64_t nval, void* scratch,
   p->prevn = a.take<int64_t>(uu);
   p->ustart = a.take<int64_t>(uu);
   p->res_val = a.take<int64_t>(uu);
-  p->hkey = a.take<uint32_t>(cap);
-  p->hpos = a.take<uint32_t>(cap);
-  *alt_k = a.take<uint32_t>(cap);
-  *alt_v = a.take<uint32_t>(cap);
-  SegDesc sg{0, cap, nullptr};
-  *hist = a.take<uint32_t>(std::max<int64_t>(sort_hist_words(&sg, 1), 256));
-  ScanDesc sd{nullptr, nullptr, uu, nullptr, nullptr};
-  *part = a.take<int64_t>(scan_part_words(&sd, 1));
-  *total = a.take<int64_t>(1);
-  p->fail = a.take<unsigned long long>(1);
+  p->nb = std::max<int64_t>((int64_t)next_pow2((uint64_t)cap) / 2, 1);  // ~1 position per bucket
+  p->bstart = a.take<int64_t>(p->nb);
+  p->bcur = a.take<int32_t>(p->nb);
+  p->bidx = a.take<uint32_t>(cap);
+  ScanDesc sd{nullptr, nullptr, uu, nullptr, nullptr}, sb{nullptr, nullptr, p->nb, nullptr, nullptr};
+  *part = a.take<int64_t>(std::max(scan_part_words(&sd, 1), scan_part_words(&sb, 1)));
+  *total = a.take<int64_t>(2);  // [total, fail]: one D2H read per round
+  p->fail = reinterpret_cast<unsigned long long*>(*total + 1);
   return a.used;
 }
 
@@ -267,9 +262,8 @@ using namespace recd;
 
 extern "C" size_t recd_partial_ikjt_scratch_bytes(int64_t num_unique, int64_t num_uvalues) {
   PartialParams p;
-  uint32_t *ak, *av, *h;
   int64_t *part, *total;
-  return pt_carve(&p, num_unique, num_uvalues, nullptr, 0, &ak, &av, &h, &part, &total);
+  return pt_carve(&p, num_unique, num_uvalues, nullptr, 0, &part, &total);
 }
 
 extern "C" int recd_partial_ikjt(int64_t batch_size, int64_t num_unique, const int64_t* uvalues,
@@ -284,9 +278,8 @@ extern "C" int recd_partial_ikjt(int64_t batch_size, int64_t num_unique, const i
   if (num_uvalues > (int64_t)0x3fffffff) return RECD_ERR_UNSUPPORTED;  // 32-bit positions in the index
   if (recd_partial_ikjt_scratch_bytes(num_unique, num_uvalues) > scratch_bytes) return RECD_ERR_SCRATCH;
   PartialParams p;
-  uint32_t *alt_k, *alt_v, *hist;
   int64_t *part, *total;
-  pt_carve(&p, num_unique, num_uvalues, scratch, scratch_bytes, &alt_k, &alt_v, &hist, &part, &total);
+  pt_carve(&p, num_unique, num_uvalues, scratch, scratch_bytes, &part, &total);
   p.U = num_unique;
   p.nval = num_uvalues;
   p.uval = uvalues;
@@ -296,39 +289,36 @@ extern "C" int recd_partial_ikjt(int64_t batch_size, int64_t num_unique, const i
   RECD_CUDA_CHECK(cudaMemsetAsync(p.pin_kind, 0, sizeof(int32_t) * num_unique, stream));
   const unsigned g = (unsigned)ceil_div(num_unique, PT_WPB);
   ScanDesc sd{p.app, p.E, num_unique, nullptr, total};
-  SegDesc sg{0, std::max<int64_t>(num_uvalues, 1), total};
-  int64_t rounds = 0;
+  ScanDesc sb{p.bstart, p.bstart, p.nb, nullptr, nullptr};
+  int64_t rounds = 0, ctl[2] = {0, -1};
   for (;;) {
     ++rounds;
     k_pt_spec<<<g, PT_NT, 0, stream>>>(p);
     note_launch();
     int rc = seg_exclusive_scan(&sd, 1, part, stream);
     if (rc != RECD_OK) return rc;
+    RECD_CUDA_CHECK(cudaMemsetAsync(p.bstart, 0, sizeof(int64_t) * p.nb, stream));
+    RECD_CUDA_CHECK(cudaMemsetAsync(p.bcur, 0, sizeof(int32_t) * p.nb, stream));
     k_pt_fill<<<g, PT_NT, 0, stream>>>(p);
     note_launch();
-    if (num_uvalues == 0) break;
-    bool in_alt = false;
-    rc = seg_sort_pairs(&sg, 1, 32, p.hkey, p.hpos, alt_k, alt_v, hist, &in_alt, stream);
+    if (num_uvalues == 0) break;  // every row empty: nothing to verify
+    rc = seg_exclusive_scan(&sb, 1, part, stream);
     if (rc != RECD_OK) return rc;
-    p.skey = in_alt ? alt_k : p.hkey;
-    p.spos = in_alt ? alt_v : p.hpos;
+    k_pt_bucket<<<(unsigned)ceil_div(num_uvalues, PT_NT), PT_NT, 0, stream>>>(p);
+    note_launch();
     RECD_CUDA_CHECK(cudaMemsetAsync(p.fail, 0xff, sizeof(unsigned long long), stream));
     k_pt_verify<<<g, PT_NT, 0, stream>>>(p);
     k_pt_pin<<<1, 1, 0, stream>>>(p);
     note_launch(2);
-    unsigned long long f = 0;
-    RECD_CUDA_CHECK(cudaMemcpyAsync(&f, p.fail, sizeof(f), cudaMemcpyDeviceToHost, stream));
+    RECD_CUDA_CHECK(cudaMemcpyAsync(ctl, total, sizeof(ctl), cudaMemcpyDeviceToHost, stream));
     RECD_CUDA_CHECK(cudaStreamSynchronize(stream));
-    if (f >= (unsigned long long)num_unique) break;  // every speculated row verified
+    if ((unsigned long long)ctl[1] >= (unsigned long long)num_unique) break;  // all verified
   }
   k_pt_windows<<<(unsigned)ceil_div(batch_size, PT_NT), PT_NT, 0, stream>>>(p, inverse, batch_size,
                                                                             windows_out);
   note_launch();
   RECD_LAUNCH_CHECK();
-  int64_t n = 0;
-  RECD_CUDA_CHECK(cudaMemcpyAsync(&n, total, sizeof(n), cudaMemcpyDeviceToHost, stream));
-  RECD_CUDA_CHECK(cudaStreamSynchronize(stream));
-  *num_values_out = n;
+  *num_values_out = ctl[0];
   if (rounds_out) *rounds_out = rounds;
   return RECD_OK;
 }
