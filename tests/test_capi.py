@@ -44,6 +44,10 @@ def test_host_only_entry_points_without_gpu():
     # argument validation happens before any device work
     rc = lib.recd_dedup(0, None, 1, None, None, None, None, None, None, None, None, 0, None)
     assert rc == 1
+    # partial IKJT: scratch grows with the unique values; bad sizes rejected up front
+    assert lib.recd_partial_ikjt_scratch_bytes(65536, 1 << 20) > lib.recd_partial_ikjt_scratch_bytes(65536, 1)
+    rc = lib.recd_partial_ikjt(4, 5, None, None, 0, None, None, None, None, None, None, 0, None)
+    assert rc == 1
 
 
 def test_no_cpu_fallback():
