@@ -24,7 +24,10 @@
 namespace recd {
 
 constexpr int OS_NT = 256;                     // threads == digits
-constexpr int OS_ITEMS = 16;
+#ifndef RECD_OS_ITEMS
+#define RECD_OS_ITEMS 16
+#endif
+constexpr int OS_ITEMS = RECD_OS_ITEMS;
 constexpr int OS_TILE = OS_NT * OS_ITEMS;      // 4096 elements per tile
 constexpr int OS_WARPS = OS_NT / 32;
 constexpr int OS_HCHUNK = OS_TILE * 4;         // elements per histogram block

@@ -13,9 +13,14 @@ pytestmark = pytest.mark.gpu
 from paper_2211_05239_b200 import _lib  # noqa: E402
 
 
-@pytest.mark.parametrize("bits,nseg,maxn", [(24, 26, 300_000), (16, 3, 70_000), (8, 1, 5000),
-                                            (32, 4, 40_000), (24, 64, 9000), (20, 2, 1)])
-def test_sort_pairs_stable(bits, nseg, maxn):
+@pytest.mark.parametrize("bits,nseg,maxn,dist", [
+    (24, 26, 300_000, "dup"), (16, 3, 70_000, "dup"), (8, 1, 5000, "dup"), (32, 4, 40_000, "dup"),
+    (24, 64, 9000, "dup"), (20, 2, 1, "dup"),
+    # MSD split (top digit + per-bucket local passes): uniform keys, one huge
+    # bucket, 3 local passes, and a top digit too narrow for the split
+    (24, 26, 1_200_000, "uniform"), (24, 3, 400_000, "onebucket"), (30, 5, 200_000, "uniform"),
+    (32, 2, 300_000, "uniform"), (28, 2, 100_000, "uniform"), (22, 70, 20_000, "uniform")])
+def test_sort_pairs_stable(bits, nseg, maxn, dist):
     rng = np.random.default_rng(bits * 100 + nseg)
     caps = rng.integers(1, maxn + 1, size=nseg)
     counts = [int(rng.integers(0, c + 1)) for c in caps]
@@ -23,7 +28,11 @@ def test_sort_pairs_stable(bits, nseg, maxn):
     total = int(caps.sum())
     hi = (1 << bits) if bits < 32 else (1 << 32)
     nkeys = max(2, min(hi, 1 + total // 5))          # heavy duplication
+    if dist == "uniform":
+        nkeys = hi
     keys = rng.integers(0, nkeys, size=total, dtype=np.uint64) % hi
+    if dist == "onebucket":  # every key in the same top digit, low bits duplicated
+        keys = (np.uint64(5) << np.uint64(bits - 8)) | rng.integers(0, 3000, size=total, dtype=np.uint64)
     if bits < 32:  # bits above `bits` must not affect the order
         keys |= rng.integers(0, 1 << (32 - bits), size=total, dtype=np.uint64) << np.uint64(bits)
     keys = (keys & 0xffffffff).astype(np.uint32)
