@@ -16,8 +16,8 @@ from paper_2211_05239_b200 import _lib  # noqa: E402
 @pytest.mark.parametrize("bits,nseg,maxn,dist", [
     (24, 26, 300_000, "dup"), (16, 3, 70_000, "dup"), (8, 1, 5000, "dup"), (32, 4, 40_000, "dup"),
     (24, 64, 9000, "dup"), (20, 2, 1, "dup"),
-    # MSD split (top digit + per-bucket local passes): uniform keys, one huge
-    # bucket, 3 local passes, and a top digit too narrow for the split
+    # uniform keys over the full digit range, every key in one top digit,
+    # 30/32-bit keys (4 passes), many small segments
     (24, 26, 1_200_000, "uniform"), (24, 3, 400_000, "onebucket"), (30, 5, 200_000, "uniform"),
     (32, 2, 300_000, "uniform"), (28, 2, 100_000, "uniform"), (22, 70, 20_000, "uniform")])
 def test_sort_pairs_stable(bits, nseg, maxn, dist):
