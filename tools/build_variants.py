@@ -6,10 +6,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
-    "m4": ["RECD_OS_MINB=4"],
-    "m2": ["RECD_OS_MINB=2"],
-    "i12m4": ["RECD_OS_ITEMS=12", "RECD_OS_MINB=4"],
-    "i8m5": ["RECD_OS_ITEMS=8", "RECD_OS_MINB=5"],
+    "nopref": ["RECD_RING_PREF=0"],
+    "pref2": ["RECD_RING_PREF=2"],
+    "k3": ["RECD_RING_PREF=0", "RECD_RING_K=3", "RECD_RING_MINB=2"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
