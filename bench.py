@@ -38,7 +38,7 @@ METRIC = "samples/sec for IKJT dedup + embedding fwd/bwd; achieved HBM GB/s vs p
 
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of the
 # cfg2 bench (profiles/r1_ncu_summary.txt); refreshed when the kernels change.
-TRAFFIC: dict = {"k_scatter": 9.876e9, "k_pool_fwd": 4.855e9}
+TRAFFIC: dict = {"k_scatter": 9.818e9, "k_pool_fwd": 4.852e9}  # profiles/r1_ncu_final.txt
 LENS = ([8, 16, 32, 64, 128, 256] * 5)[:26]
 
 
