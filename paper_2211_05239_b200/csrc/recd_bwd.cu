@@ -31,7 +31,7 @@
 #define RECD_BWD_FULLOK 1
 #endif
 #ifndef RECD_SCATTER_MINB
-#define RECD_SCATTER_MINB 3
+#define RECD_SCATTER_MINB 4
 #endif
 // L2 policy of the scatter: 1 = table rows (read + write) evict_first, 2 = also
 // unique-row gradient gathers evict_last, 0 = no hints
@@ -282,11 +282,11 @@ __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t
 }
 
 #ifndef RECD_SC_RS
-#define RECD_SC_RS 8
+#define RECD_SC_RS 6
 #endif
 constexpr int SC_RS = RECD_SC_RS;  // table rows prefetched ahead per warp (shared-memory ring)
 #ifndef RECD_SC_BATCH
-#define RECD_SC_BATCH 8
+#define RECD_SC_BATCH 6
 #endif
 constexpr int SC_BATCH = RECD_SC_BATCH;  // unique-row gradient gathers in flight per warp
 
