@@ -125,6 +125,12 @@ __global__ void k_csr_bounds(const __grid_constant__ BwdParams p) {
   if (j == p.B - 1) start[u + 1] = (int32_t)p.B;
 }
 
+// 1: features with an inverse reduce through k_grad_u_flat (position-parallel
+// over the inverse CSR); k_grad_u keeps the identity (KJT) features
+#ifndef RECD_GU_FLAT
+#define RECD_GU_FLAT 1
+#endif
+
 template <class C>
 __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdParams p) {
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
     int64_t acc = 0;
     for (int f = 0; f < p.F; ++f) {
       s_pref[f] = acc;
-      acc += p.counts[f] * ncb;
+      if (!RECD_GU_FLAT || p.feat_is[f] < 0) acc += p.counts[f] * ncb;
     }
     s_pref[p.F] = acc;
   }
@@ -185,6 +191,105 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
     } else {
       for (int j = 0; j < p.gsegs; ++j)
         C::st(p.gseg_dst[f][j] + (__ldg(p.gseg_row0[f][j]) + u) * p.D + cw.lo, cw.ok, acc);
+    }
+  }
+}
+
+// grad_u of the features with an inverse, position-parallel: warp per
+// (feature, GU_CH consecutive positions of the inverse CSR, column block).  The
+// warp reduces every unique row whose CSR run starts in its chunk (to the run's
+// end), gathering grad_out rows 8 positions at a time across run boundaries, so
+// no per-row dependent chain (CSR start -> row ids -> gradient rows) stalls it.
+// Same order as k_grad_u (ascending batch row within each unique row).
+constexpr int GU_CH = 256;
+__device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t n, uint32_t id,
+                                           int lane);
+#ifndef RECD_GUF_MINB
+#define RECD_GUF_MINB 3
+#endif
+template <class C>
+__global__ void __launch_bounds__(256, RECD_GUF_MINB) k_grad_u_flat(const __grid_constant__ BwdParams p) {
+  __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
+  const int ncb = col_blocks<C>(p.D);
+  const int64_t nch = (p.B + GU_CH - 1) / GU_CH;
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int f = 0; f < p.F; ++f) {
+      s_pref[f] = acc;
+      if (p.feat_is[f] >= 0) acc += nch * ncb;
+    }
+    s_pref[p.F] = acc;
+  }
+  __syncthreads();
+  const int64_t total = s_pref[p.F];
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  constexpr int V = C::VW;
+  const int64_t B = p.B;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
+       w += nwarps) {
+    const int f = find_seg(s_pref, p.F, w);
+    const ColWork cw = col_work<C>(w - s_pref[f], p.D, lane);  // cw.row = chunk
+    const int is = p.feat_is[f];
+    const uint32_t* K = p.inv_keys + (int64_t)is * B;
+    const uint32_t* R = p.inv_rows + (int64_t)is * B;
+    const int64_t lo = cw.row * GU_CH, hi = min(B, lo + (int64_t)GU_CH);
+    // first run start at or after lo
+    int64_t j = lo;
+    if (lo > 0) j = run_end(K, lo, B, __ldg(K + lo - 1), lane);
+    if (j >= hi) continue;
+    const float* G = p.grad_out[f] + cw.lo;
+    const uint32_t D32 = (uint32_t)p.D;
+    // window of 32 positions [wb, wb + 32): keys and rows, one per lane
+    int64_t wb = j;
+    uint32_t kw = wb + lane < B ? __ldg(K + wb + lane) : 0xffffffffu;
+    uint32_t rw = wb + lane < B ? __ldg(R + wb + lane) : 0u;
+    float acc[V];
+    C::zero(acc);
+    float x[8][V];
+    bool done = false;
+    for (int64_t k0 = j; !done; k0 += 8) {
+      if (k0 + 9 > wb + 32) {
+        wb = k0;
+        kw = wb + lane < B ? __ldg(K + wb + lane) : 0xffffffffu;
+        rw = wb + lane < B ? __ldg(R + wb + lane) : 0u;
+      }
+      const int sh = (int)(k0 - wb);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t row = __shfl_sync(0xffffffffu, rw, sh + t);
+        if (k0 + t < B) C::ld(G + (uint64_t)row * D32, cw.ok, x[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t u = __shfl_sync(0xffffffffu, kw, sh + t);
+        const uint32_t un = __shfl_sync(0xffffffffu, kw, sh + t + 1);
+        if (!done && k0 + t < B) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[e] = __fadd_rn(acc[e], x[t][e]);
+          if (k0 + t + 1 == B || un != u) {  // run of u complete (warp-uniform)
+            if (p.mode == RECD_POOL_AVG) {
+              const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
+              const int64_t* uo = p.uoffsets[f];
+              const int64_t len = ((u + 1 < U) ? uo[u + 1] : NV) - uo[u];
+              if (len > 0) {
+                const float fl = (float)len;
+#pragma unroll
+                for (int e = 0; e < V; ++e) acc[e] = __fdiv_rn(acc[e], fl);
+              }
+            }
+            if (p.gsegs == 0) {
+              C::st(p.gout[f] + (int64_t)u * p.D + cw.lo, cw.ok, acc);
+            } else {
+              for (int g = 0; g < p.gsegs; ++g)
+                C::st(p.gseg_dst[f][g] + (__ldg(p.gseg_row0[f][g]) + u) * p.D + cw.lo, cw.ok, acc);
+            }
+            C::zero(acc);
+            if (k0 + t + 1 >= hi) done = true;  // the next run belongs to the next chunk
+          }
+        }
+      }
+      if (k0 + 8 >= B) done = true;
     }
   }
 }
@@ -735,8 +840,18 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     if (do_grad) {
       const unsigned grid =
           (unsigned)std::min<int64_t>(ceil_div(B * F * ncb, 8), (int64_t)num_sms() * 16);
-      k_grad_u<C><<<grid, 256, 0, stream>>>(p);
-      note_launch();
+      bool any_id = !RECD_GU_FLAT, any_inv = false;
+      for (int f = 0; f < F; ++f) (p.feat_is[f] < 0 ? any_id : any_inv) = true;
+      if (any_id) {
+        k_grad_u<C><<<grid, 256, 0, stream>>>(p);
+        note_launch();
+      }
+      if (RECD_GU_FLAT && any_inv) {
+        const unsigned gf = (unsigned)std::min<int64_t>(
+            ceil_div(ceil_div(B, GU_CH) * F * ncb, 8), (int64_t)num_sms() * 16);
+        k_grad_u_flat<C><<<std::max(gf, 1u), 256, 0, stream>>>(p);
+        note_launch();
+      }
     }
     // 5. sorted scatter-add (+ fused SGD)
     if (do_scatter) {
