@@ -100,6 +100,9 @@ __global__ void __launch_bounds__(256, RECD_POOL_MINB) k_pool_fwd(const __grid_c
   }
 }
 
+#ifndef RECD_EXPAND_CS
+#define RECD_EXPAND_CS 1
+#endif
 // out[f][i] = pooled[f][inverse[f][i]]  (trainer_sim.py:558-561)
 // Warp per (32-row block, column block): one coalesced load of the 32 inverse
 // entries, then the rows' slices are gathered 8 at a time (8 loads in flight
@@ -140,7 +143,15 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ PoolPara
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t)
-        if (r0 + t < nr) C::st(dst + (int64_t)(r0 + t) * p.D, cw.ok, x[t]);
+        if (r0 + t < nr) {
+          if constexpr (RECD_EXPAND_CS && C::VW == 4) {  // streaming store: keep pooled rows in L2
+            if (C::FULL || cw.ok)
+              __stcs(reinterpret_cast<float4*>(dst + (int64_t)(r0 + t) * p.D),
+                     make_float4(x[t][0], x[t][1], x[t][2], x[t][3]));
+          } else {
+            C::st(dst + (int64_t)(r0 + t) * p.D, cw.ok, x[t]);
+          }
+        }
     }
   }
 }

@@ -8,6 +8,9 @@ from paper_2211_05239_b200.build import build  # noqa: E402
 V = {
     "noflat": ["RECD_GU_FLAT=0"],
     "fm4": ["RECD_GUF_MINB=4"],
+    "rs8": ["RECD_SC_RS=8"],
+    "rs4": ["RECD_SC_RS=4"],
+    "noxcs": ["RECD_EXPAND_CS=0"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
