@@ -204,6 +204,9 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
 constexpr int GU_CH = 256;
 __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t n, uint32_t id,
                                            int lane);
+#ifndef RECD_GUF_CS
+#define RECD_GUF_CS 0
+#endif
 #ifndef RECD_GUF_MINB
 #define RECD_GUF_MINB 3
 #endif
@@ -258,7 +261,18 @@ __global__ void __launch_bounds__(256, RECD_GUF_MINB) k_grad_u_flat(const __grid
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const uint32_t row = __shfl_sync(0xffffffffu, rw, sh + t);
-        if (k0 + t < B) C::ld(G + (uint64_t)row * D32, cw.ok, x[t]);
+        if (k0 + t < B) {
+          if constexpr (RECD_GUF_CS && V == 4) {  // grad_out is read once: evict first
+            if (C::FULL || cw.ok) {
+              const float4 q = __ldcs(reinterpret_cast<const float4*>(G + (uint64_t)row * D32));
+              x[t][0] = q.x; x[t][1] = q.y; x[t][2] = q.z; x[t][3] = q.w;
+            } else {
+              C::zero(x[t]);
+            }
+          } else {
+            C::ld(G + (uint64_t)row * D32, cw.ok, x[t]);
+          }
+        }
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t) {

@@ -11,6 +11,7 @@ V = {
     "rs8": ["RECD_SC_RS=8"],
     "rs4": ["RECD_SC_RS=4"],
     "noxcs": ["RECD_EXPAND_CS=0"],
+    "gcs": ["RECD_GUF_CS=1"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
