@@ -100,6 +100,10 @@ __global__ void __launch_bounds__(256, RECD_POOL_MINB) k_pool_fwd(const __grid_c
   }
 }
 
+#ifndef RECD_EXPAND_RF
+#define RECD_EXPAND_RF 8
+#endif
+constexpr int EXP_RF = RECD_EXPAND_RF;  // row copies in flight per lane
 #ifndef RECD_EXPAND_CS
 #define RECD_EXPAND_CS 1
 #endif
@@ -134,15 +138,15 @@ __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ PoolPara
     const int64_t my = (lane < nr) ? (p.inverse[f] ? __ldg(p.inverse[f] + i0 + lane) : i0 + lane) : 0;
     const float* src = p.pooled[f] + cw.lo;
     float* dst = p.out[f] + i0 * p.D + cw.lo;
-    for (int r0 = 0; r0 < nr; r0 += 8) {
-      float x[8][C::VW];
+    for (int r0 = 0; r0 < nr; r0 += EXP_RF) {
+      float x[EXP_RF][C::VW];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
+      for (int t = 0; t < EXP_RF; ++t) {
         const int64_t u = __shfl_sync(0xffffffffu, my, (r0 + t) & 31);
         if (r0 + t < nr) C::ld(src + u * p.D, cw.ok, x[t]);
       }
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
+      for (int t = 0; t < EXP_RF; ++t)
         if (r0 + t < nr) {
           if constexpr (RECD_EXPAND_CS && C::VW == 4) {  // streaming store: keep pooled rows in L2
             if (C::FULL || cw.ok)

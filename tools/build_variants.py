@@ -12,6 +12,8 @@ V = {
     "rs4": ["RECD_SC_RS=4"],
     "noxcs": ["RECD_EXPAND_CS=0"],
     "gcs": ["RECD_GUF_CS=1"],
+    "xrf16": ["RECD_EXPAND_RF=16"],
+    "xrf4": ["RECD_EXPAND_RF=4"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
