@@ -10,8 +10,9 @@
 //
 // Semantics kept: a row is a Mapping or an object with a `.features` mapping
 // (tensors.py:228-234); an absent key (or None) is an empty list (237-243); an
-// ID list must be one-dimensional (47-51); IDs are int64 (OverflowError like
-// numpy's conversion otherwise).
+// ID list must be one-dimensional (47-51); lists that are not plain Python
+// ints go through the optional `convert` callable (np.asarray + 1-D check), so
+// floats, numpy arrays and scalars convert or fail exactly as in the reference.
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
 
@@ -40,9 +41,43 @@ PyObject* row_features(PyObject* row) {
   return nullptr;
 }
 
-// append the IDs of `seq` to `out`; -1 with an exception on error
-int append_ids(PyObject* seq, std::vector<int64_t>& out) {
+// IDs of `seq` through the Python converter (the reference's _as_id_array,
+// np.asarray(seq, dtype=int64) + the 1-D check, tensors.py:47-51): used for
+// everything the fast path below does not take, so odd inputs (floats, numpy
+// arrays of any shape, scalars) behave exactly like the reference.
+int append_converted(PyObject* seq, std::vector<int64_t>& out, PyObject* conv) {
+  if (!conv) {  // no converter: keep the pending error, or the reference's 1-D text
+    if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "ID list must be one-dimensional");
+    return -1;
+  }
+  PyErr_Clear();
+  PyObject* arr = PyObject_CallFunctionObjArgs(conv, seq, nullptr);
+  if (!arr) return -1;
+  Py_buffer view;
+  if (PyObject_GetBuffer(arr, &view, PyBUF_C_CONTIGUOUS | PyBUF_FORMAT) != 0) {
+    Py_DECREF(arr);
+    return -1;
+  }
+  if (view.itemsize != (Py_ssize_t)sizeof(int64_t)) {
+    PyBuffer_Release(&view);
+    Py_DECREF(arr);
+    PyErr_SetString(PyExc_TypeError, "ID converter must return an int64 array");
+    return -1;
+  }
+  const size_t n = (size_t)(view.len / (Py_ssize_t)sizeof(int64_t)), base = out.size();
+  out.resize(base + n);
+  if (n) std::memcpy(out.data() + base, view.buf, n * sizeof(int64_t));
+  PyBuffer_Release(&view);
+  Py_DECREF(arr);
+  return 0;
+}
+
+// append the IDs of `seq` to `out`; -1 with an exception on error.  Fast path:
+// a list/tuple of Python ints (or index-like scalars); anything else goes
+// through `conv`.
+int append_ids(PyObject* seq, std::vector<int64_t>& out, PyObject* conv) {
   if (seq == Py_None) return 0;
+  if (conv && !PyList_Check(seq) && !PyTuple_Check(seq)) return append_converted(seq, out, conv);
   PyObject* fast = PySequence_Fast(seq, "ID list must be a sequence");
   if (!fast) return -1;
   const Py_ssize_t n = PySequence_Fast_GET_SIZE(fast);
@@ -51,26 +86,24 @@ int append_ids(PyObject* seq, std::vector<int64_t>& out) {
   out.resize(base + (size_t)n);
   for (Py_ssize_t i = 0; i < n; ++i) {
     PyObject* it = items[i];
-    if (PyList_Check(it) || PyTuple_Check(it)) {
-      Py_DECREF(fast);
-      PyErr_SetString(PyExc_ValueError, "ID list must be one-dimensional");
-      return -1;
-    }
-    long long v = PyLong_AsLongLong(it);
-    if (v == -1 && PyErr_Occurred()) {
-      // numpy integer scalars and other index-like objects
-      PyErr_Clear();
-      PyObject* idx = PyNumber_Index(it);
-      if (!idx) {
-        Py_DECREF(fast);
-        return -1;
-      }
-      v = PyLong_AsLongLong(idx);
-      Py_DECREF(idx);
+    long long v = -1;
+    bool ok = PyLong_Check(it) || PyIndex_Check(it);
+    if (ok) {
+      v = PyLong_AsLongLong(it);
       if (v == -1 && PyErr_Occurred()) {
-        Py_DECREF(fast);
-        return -1;
+        PyErr_Clear();
+        PyObject* idx = PyNumber_Index(it);
+        if (idx) {
+          v = PyLong_AsLongLong(idx);
+          Py_DECREF(idx);
+        }
+        ok = !(v == -1 && PyErr_Occurred());
       }
+    }
+    if (!ok) {  // float, nested list, overflow, ...: numpy's conversion decides
+      Py_DECREF(fast);
+      out.resize(base);
+      return append_converted(seq, out, conv);
     }
     out[base + (size_t)i] = (int64_t)v;
   }
@@ -79,8 +112,8 @@ int append_ids(PyObject* seq, std::vector<int64_t>& out) {
 }
 
 PyObject* pack_rows(PyObject*, PyObject* args) {
-  PyObject *rows, *keys;
-  if (!PyArg_ParseTuple(args, "OO", &rows, &keys)) return nullptr;
+  PyObject *rows, *keys, *conv = nullptr;
+  if (!PyArg_ParseTuple(args, "OO|O", &rows, &keys, &conv)) return nullptr;
   PyObject* rfast = PySequence_Fast(rows, "rows must be a sequence");
   if (!rfast) return nullptr;
   PyObject* kfast = PySequence_Fast(keys, "keys must be a sequence");
@@ -117,7 +150,7 @@ PyObject* pack_rows(PyObject*, PyObject* args) {
           goto done;
         }
       }
-      const int rc = append_ids(seq, vals[k]);
+      const int rc = append_ids(seq, vals[k], conv);
       Py_DECREF(seq);
       if (rc) {
         Py_DECREF(feats);
@@ -139,9 +172,14 @@ PyObject* pack_rows(PyObject*, PyObject* args) {
       Py_CLEAR(result);
       goto done;
     }
-    PyList_SET_ITEM(result, k, PyTuple_Pack(2, v, o));
+    PyObject* pair = PyTuple_Pack(2, v, o);
     Py_DECREF(v);
     Py_DECREF(o);
+    if (!pair) {
+      Py_CLEAR(result);
+      goto done;
+    }
+    PyList_SET_ITEM(result, k, pair);
   }
 done:
   Py_DECREF(rfast);
@@ -151,7 +189,7 @@ done:
 
 PyMethodDef methods[] = {
     {"pack_rows", pack_rows, METH_VARARGS,
-     "pack_rows(rows, keys) -> [(values bytes, offsets bytes)] per key (int64 little-endian)"},
+     "pack_rows(rows, keys[, convert]) -> [(values bytes, offsets bytes)] per key (int64 little-endian)"},
     {nullptr, nullptr, 0, nullptr}};
 
 PyModuleDef module = {PyModuleDef_HEAD_INIT, "_hostpack", "Native KJT host packing", -1, methods};

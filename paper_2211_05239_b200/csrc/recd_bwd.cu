@@ -65,6 +65,7 @@ struct BwdParams {
   float* table[RECD_MAX_FEAT];
   int64_t ts_base[RECD_MAX_FEAT];    // element base in the occurrence arrays
   int64_t ts_chunk0[RECD_MAX_FEAT];  // first scatter chunk
+  int64_t ts_rows[RECD_MAX_FEAT];    // table rows (IDs must lie in [0, rows))
   int64_t* grad_ids[RECD_MAX_FEAT];
   float* grad_rows[RECD_MAX_FEAT];
   int64_t* grad_count[RECD_MAX_FEAT];
@@ -84,6 +85,7 @@ struct BwdParams {
   uint32_t* occ_keys;     // sorted occurrence IDs
   uint32_t* occ_vals;     // tag = (f << 24) | u
   int64_t* run_part;      // [total_rc_chunks] exclusive run counts (grad-output mode)
+  int32_t* bad;           // set by k_occ when an ID is outside [0, rows): no table update
   int64_t occ_blk0[RECD_MAX_FEAT + 1];  // k_occ: first block of each feature (capacity)
   // optional scatter of grad_u rows to peers (fused source -> owner push): row u
   // of feature f goes to gseg_dst[f][j] + (*gseg_row0[f][j] + u) * D, j < gsegs
@@ -94,6 +96,7 @@ struct BwdParams {
 
 __global__ void k_bwd_setup(const __grid_constant__ BwdParams p) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  *p.bad = 0;
   for (int s = 0; s < p.nts; ++s) p.seg_count[s] = 0;
   for (int f = 0; f < p.F; ++f) {
     const int s = p.feat_ts[f];
@@ -327,6 +330,7 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
   const int64_t* uo = p.uoffsets[f];
   const int64_t* src = p.uvalues[f];
   const int64_t dst = p.ts_base[p.feat_ts[f]] + p.feat_base[f];
+  const uint64_t rows = (uint64_t)p.ts_rows[p.feat_ts[f]];
   __shared__ int64_t s_u0;
   __shared__ int64_t s_uo[OC_MAXR + 1];
   if (tid < 32) {
@@ -358,7 +362,12 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
       } else {
         while (s_uo[r + 1] <= q) ++r;
       }
-      keys[dst + q] = (uint32_t)__ldg(src + q);
+      const int64_t id = __ldg(src + q);
+      // an ID outside [0, rows) (the forward reports it, trainer_sim.py:312-320)
+      // must not address the table: flag it, and the scatter skips every update
+      const bool in = (uint64_t)id < rows;
+      if (!in) *p.bad = 1;
+      keys[dst + q] = in ? (uint32_t)id : 0u;
       vals[dst + q] = ((uint32_t)f << 24) | (uint32_t)(u0 + r);
     }
     if (covered >= j1) break;
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(RC) k_run_count(const __grid_constant__ BwdPar
   const int64_t n = p.seg_count[s];
   const int64_t j = (chunk - p.ts_chunk0[s]) * RC + threadIdx.x;
   const uint32_t* K = p.occ_keys + p.ts_base[s];
-  const int start = (j < n) && (j == 0 || K[j] != K[j - 1]);
+  const int start = (j < n) && (j == 0 || K[j] != K[j - 1]) && !*p.bad;
   const int cnt = __syncthreads_count(start);
   if (threadIdx.x == 0) p.run_part[chunk] = cnt;
 }
@@ -428,6 +437,7 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   const int ncb = col_blocks<C>(p.D);
   const int64_t total = p.total_rc_chunks * ncb;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  if (*(volatile const int32_t*)p.bad) return;  // out-of-range ID in the batch: no update
   uint16_t* starts = s_starts[warp];
   uint32_t* rids = s_ids[warp];
   float* ring = &s_ring[warp][0][lane * V];
@@ -631,6 +641,7 @@ Plan make_plan(int F, const int64_t* const* inverse, float* const* tables, const
 
 struct BwdScratch {
   int64_t *feat_base, *seg_count, *is_count, *run_part, *scan_part;
+  int32_t* bad;
   uint32_t *inv_k0, *inv_v0, *inv_k1, *inv_v1, *hist;
   int32_t* csr_start;
   float* grad_u;
@@ -645,6 +656,7 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   s->feat_base = a.take<int64_t>(RECD_MAX_FEAT);
   s->seg_count = a.take<int64_t>(RECD_MAX_FEAT);
   s->is_count = a.take<int64_t>(RECD_MAX_FEAT);
+  s->bad = a.take<int32_t>(1);
   s->run_part = a.take<int64_t>((need & NEED_OCC) ? pl.rc_chunks : 1);
   const size_t nib = (need & NEED_INV) ? (size_t)std::max(pl.nis, 1) * B : 1;
   s->inv_k0 = a.take<uint32_t>(nib);
@@ -772,6 +784,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     p.table[s] = pl.table[s];
     p.ts_base[s] = pl.ts_base[s];
     p.ts_chunk0[s] = pl.ts_chunk0[s];
+    p.ts_rows[s] = pl.table_rows[s];
     if (do_scatter && !apply_sgd) {
       const int f = first_feat_of_ts[s];
       p.grad_ids[s] = grad_ids_out[f];
@@ -793,6 +806,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   p.is_count = sc.is_count;
   p.csr_start = sc.csr_start;
   p.run_part = sc.run_part;
+  p.bad = sc.bad;
 
   const bool prep = (phase & PH_PREP) != 0, fin = (phase & PH_FINISH) != 0;
   // sorted buffers: a stable LSD sort of `bits` bits ends in the alternate

@@ -57,6 +57,18 @@ struct DispatchParams {
   int64_t* dst_ro[SH_MAXBLK];            // null: no row offsets
 };
 
+// Owner shard and local row of an ID.  A negative ID (out of range, reported by
+// the owner's lookup) goes to shard 0 as local row -1, which every owner-side
+// range check rejects; `id % S` would index in front of the per-shard arrays.
+__device__ __forceinline__ int shard_of(int64_t id, int S, int64_t* local) {
+  if (id < 0) {
+    *local = -1;
+    return 0;
+  }
+  *local = id / S;
+  return (int)(id % S);
+}
+
 __device__ __forceinline__ void feature_prefix(int64_t* s_pref, const int64_t* counts, int F) {
   if (threadIdx.x == 0) {
     int64_t acc = 0;
@@ -89,7 +101,8 @@ __global__ void __launch_bounds__(256) k_shard_count(const __grid_constant__ Cou
     for (int64_t j0 = a; j0 < e; j0 += 32) {
       const int64_t j = j0 + lane;
       const bool valid = j < e;
-      const int o = valid ? (int)(__ldg(p.uvalues[f] + j) % p.S) : SH_MAXR;
+      int64_t lr;
+      const int o = valid ? shard_of(__ldg(p.uvalues[f] + j), p.S, &lr) : SH_MAXR;
       const unsigned peers = __match_any_sync(0xffffffffu, o);
       if (valid && lane == __ffs(peers) - 1) cnt[o] += __popc(peers);
       __syncwarp();
@@ -133,14 +146,15 @@ __global__ void __launch_bounds__(256) k_shard_scatter(const __grid_constant__ D
       const int64_t j = j0 + lane;
       const bool valid = j < e;
       const int64_t id = valid ? __ldg(p.uvalues[f] + j) : 0;
-      const int o = valid ? (int)(id % p.S) : SH_MAXR;
+      int64_t lr = 0;
+      const int o = valid ? shard_of(id, p.S, &lr) : SH_MAXR;
       const unsigned peers = __match_any_sync(0xffffffffu, o);
       int64_t pos = 0;
       if (valid) pos = run[o] + __popc(peers & lt);
       __syncwarp();
       if (valid && lane == __ffs(peers) - 1) run[o] += __popc(peers);
       __syncwarp();
-      if (valid) p.dst_ids[f * p.S + o][pos] = id / p.S;
+      if (valid) p.dst_ids[f * p.S + o][pos] = lr;
     }
     __syncwarp();
   }

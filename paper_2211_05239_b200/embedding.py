@@ -218,30 +218,34 @@ def pooled_lookup_backward(features: Sequence[JaggedTensor], tables: Sequence[Em
 
 
 class _PooledFn(torch.autograd.Function):
+    """Autograd node of one pooled_lookup call; the tables, batch size and
+    counts the backward needs are kept on ctx (not on the module), so several
+    forwards may be in flight before their backwards run."""
+
     @staticmethod
-    def forward(ctx, anchor, module, features, inverses, counts, op, B):
-        outs = pooled_lookup(features, module._tables_for(features), op, inverses, B,
-                             counts=counts)
-        ctx.module, ctx.features, ctx.inverses, ctx.counts, ctx.op = (
-            module, features, inverses, counts, op)
+    def forward(ctx, anchor, lr, tables, features, inverses, counts, op, B, sink):
+        outs = pooled_lookup(features, tables, op, inverses, B, counts=counts)
+        ctx.lr, ctx.tables, ctx.features, ctx.inverses, ctx.counts, ctx.op, ctx.B, ctx.sink = (
+            lr, tables, features, inverses, counts, op, B, sink)
         return tuple(outs)
 
     @staticmethod
     def backward(ctx, *grads):
-        m = ctx.module
         feats = ctx.features
-        tables = m._tables_for(feats)
         dev = feats[0].device
-        grads = [g if g is not None else torch.zeros((m._B, m.dim), device=dev) for g in grads]
-        res = pooled_lookup_backward(feats, tables, ctx.op, grads, ctx.inverses, lr=m.lr,
+        D = ctx.tables[0].dim
+        grads = [g if g is not None else torch.zeros((ctx.B, D), device=dev) for g in grads]
+        res = pooled_lookup_backward(feats, ctx.tables, ctx.op, grads, ctx.inverses, lr=ctx.lr,
                                      counts=ctx.counts)
         if res is not None:
-            m.sparse_grads.extend(res)
-        return (None,) * 7
+            ctx.sink.extend(res)
+        return (None,) * 9
 
 
 class DedupEmbeddingBagCollection(torch.nn.Module):
-    """Pooled embedding bags over IKJT groups (sum / avg / max per key).
+    """Pooled embedding bags over IKJT groups (sum / avg / max per key; max is
+    forward-only -- its outputs carry no autograd graph, and lr with max is
+    rejected at construction).
 
     ``forward`` takes the step's IKJTs (and/or a KJT for plain keys) and
     returns {key: [B, D]} -- each unique row is looked up and pooled once, then
@@ -265,14 +269,13 @@ class DedupEmbeddingBagCollection(torch.nn.Module):
             if op not in ELEMENT_POOLING:
                 raise ValueError(f"unknown pooling op {op!r}")
         self.pooling = dict(pooling)
+        if lr is not None and "max" in self.pooling.values():
+            # the fused SGD runs in the backward, which max pooling does not have
+            raise ValueError("max pooling is forward-only: it cannot be trained with lr "
+                             "(use sum or avg)")
         self.lr = lr
         self.sparse_grads: list = []
         self._anchor = torch.nn.Parameter(torch.zeros(0))
-        self._key_of: dict[int, str] = {}
-        self._B = 0
-
-    def _tables_for(self, features):
-        return [self.tables[self._key_of[id(f)]] for f in features]
 
     def forward(self, ikjts: Sequence[IKJT] = (), kjt: KJT | None = None) -> dict[str, torch.Tensor]:
         if isinstance(ikjts, IKJT):
@@ -289,7 +292,6 @@ class DedupEmbeddingBagCollection(torch.nn.Module):
                 jobs.append((k, jt, None))
         if not jobs:
             return {}
-        self._B = B
         out: dict[str, torch.Tensor] = {}
         by_op: dict[str, list] = {}
         for job in jobs:
@@ -298,9 +300,14 @@ class DedupEmbeddingBagCollection(torch.nn.Module):
             by_op.setdefault(self.pooling.get(job[0], "sum"), []).append(job)
         for op, js in by_op.items():
             feats = [j[1] for j in js]
-            self._key_of.update({id(f): j[0] for f, j in zip(feats, js)})
+            tables = [self.tables[j[0]] for j in js]
             counts = _counts_tensor(feats, feats[0].device)
-            res = _PooledFn.apply(self._anchor, self, feats, [j[2] for j in js], counts, op, B)
+            invs = [j[2] for j in js]
+            if op == "max":   # forward-only (no backward exists for max): no autograd node
+                res = pooled_lookup(feats, tables, op, invs, B, counts=counts)
+            else:
+                res = _PooledFn.apply(self._anchor, self.lr, tables, feats, invs, counts, op, B,
+                                      self.sparse_grads)
             for j, r in zip(js, res):
                 out[j[0]] = r
         return out

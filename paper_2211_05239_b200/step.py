@@ -130,10 +130,12 @@ class TrainStep:
             self.a_inverse_f = L.ptrs(inv_f)
             self.a_pooled = L.ptrs(self.pooled)
             self.a_feat_vals, self.a_feat_offs = self.a_uvalues, self.a_uoffsets
+            self.a_feat_vals_t = self.uvalues
         else:
             self.a_inverse_f = L.ptrs([None] * self.F)
             self.a_pooled = L.ptrs(self.out)  # no expansion: pooled rows are the batch rows
             self.a_feat_vals, self.a_feat_offs = self.a_in_values, self.a_in_offsets
+            self.a_feat_vals_t = self.in_values
 
     # ---------------------------------------------------------------- step
     def dedup(self, stream: int) -> None:
@@ -217,6 +219,19 @@ class TrainStep:
             self.run()
         else:
             self.graph.replay()
+
+    def check(self) -> None:
+        """Raise the reference's ValueError (trainer_sim.py:312-320) if the last
+        step's lookup saw an ID outside [0, rows).  The step itself never
+        synchronises; the backward skips every table update of such a batch
+        (k_occ flags it, k_scatter does nothing), so the tables stay intact."""
+        e = int(self.err[0].item())
+        if e == _lib.RECD_NO_ERROR:
+            return
+        f, pos = e >> 40, e & ((1 << 40) - 1)
+        vals = self.a_feat_vals_t[f]
+        raise ValueError(f"feature {self.keys[f]!r}: ID {int(vals[pos])} at position {pos} "
+                         f"out of range [0, {self.tables[f].rows})")
 
     def host_counts(self) -> StepCounts:
         c = self.counts.cpu().tolist()

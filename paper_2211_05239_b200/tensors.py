@@ -229,6 +229,15 @@ def _pack_rows(arrs: Sequence[np.ndarray]) -> tuple[np.ndarray, np.ndarray]:
     return values, offsets
 
 
+def _as_id_array(seq) -> np.ndarray:
+    """tensors.py:47-51: the conversion the native packer falls back to for
+    ID lists that are not plain Python ints (floats, numpy arrays, scalars)."""
+    arr = np.asarray(seq, dtype=np.int64)
+    if arr.ndim != 1:
+        raise ValueError(f"ID list must be one-dimensional, got shape {arr.shape}")
+    return np.ascontiguousarray(arr)
+
+
 def build_kjt(rows: Sequence, keys: Sequence[str], device=None) -> KJT:
     """Records -> KJT on the GPU, preserving batch order (tensors.py:246-254).
     The records are walked once in native code (`_hostpack.pack_rows`,
@@ -237,7 +246,7 @@ def build_kjt(rows: Sequence, keys: Sequence[str], device=None) -> KJT:
         raise ValueError("empty batch")
     from . import _hostpack  # built by build.build_host(); no Python fallback
     dev = device or default_device()
-    packed = _hostpack.pack_rows(rows, list(keys))
+    packed = _hostpack.pack_rows(rows, list(keys), _as_id_array)
     entries = {}
     for key, (vb, ob) in zip(keys, packed):
         v = torch.frombuffer(bytearray(vb), dtype=torch.int64) if vb else torch.empty(0, dtype=torch.int64)

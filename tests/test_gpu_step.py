@@ -92,3 +92,43 @@ def test_long_sessions_many_consecutive_rows():
     _, w1s = _oracle_step(batch, w0s, grads, lr)
     for k in keys:
         np.testing.assert_array_equal(tables[k].weights.cpu().numpy(), w1s[k])
+
+
+@pytest.mark.parametrize("bad", ["rows", "negative", "huge"])
+@pytest.mark.parametrize("graph", [False, True])
+def test_out_of_range_id_reports_and_leaves_tables_intact(bad, graph):
+    """An ID outside [0, rows) (e.g. the reader's clamp transform with
+    param=rows) is the reference's ValueError (trainer_sim.py:312-320); the
+    fused SGD must not touch any table row for that batch (k_occ flags the ID,
+    k_scatter skips), and TrainStep.check() raises the reference's text."""
+    b, vocab, dim, lr = 512, 3000, 64, 0.5
+    batch = _batch(b, [8, 16], vocab, seed=5)
+    keys = list(batch.keys)
+    bad_id = {"rows": vocab, "negative": -3, "huge": (1 << 40) + 7}[bad]
+    vals = {k: batch.values[k].copy() for k in keys}
+    vals[keys[1]][37] = bad_id
+    rng = np.random.default_rng(2)
+    w0s = {k: rng.uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32) for k in keys}
+    tables = {k: R.EmbeddingTable(k, vocab, dim, torch.as_tensor(w0s[k], device="cuda").clone())
+              for k in keys}
+    caps = {k: int(batch.values[k].size) for k in keys}
+    step = TrainStep([[k] for k in keys], b, caps, tables, "sum", lr, "dedup")
+    step.load_batch(vals, batch.offsets)
+    step.fill_grad_out(3)
+    if graph:
+        step.capture()
+        step.replay()
+    else:
+        step.run()
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match=rf"feature '{keys[1]}': ID {bad_id} at position \d+ "
+                                         rf"out of range \[0, {vocab}\)"):
+        step.check()
+    for k in keys[1:]:
+        np.testing.assert_array_equal(tables[k].weights.cpu().numpy(), w0s[k])
+    # a clean batch afterwards trains normally (the flag is per step)
+    step.load_batch(batch.values, batch.offsets)
+    step.run()
+    torch.cuda.synchronize()
+    step.check()
+    assert not np.array_equal(tables[keys[1]].weights.cpu().numpy(), w0s[keys[1]])

@@ -46,3 +46,21 @@ def test_pack_errors(hostpack):
         hostpack.pack_rows([3], ["a"])
     with pytest.raises(OverflowError):
         hostpack.pack_rows([{"a": [2**64]}], ["a"])
+
+
+def test_pack_converter_matches_reference_semantics(hostpack):
+    """Inputs off the fast path go through the reference's conversion
+    (np.asarray(dtype=int64) + 1-D check, tensors.py:47-51)."""
+    from paper_2211_05239_b200.tensors import _as_id_array
+    rows = [{"a": [1.9, 2.2]}, {"a": np.array([[3], [4]]).ravel()}, {"a": (5, np.int32(6))},
+            {"a": np.arange(3, dtype=np.uint8)}]
+    got = _unpack(hostpack.pack_rows(rows, ["a"], _as_id_array))
+    ref = oracle.build_kjt_arrays(rows, ["a"])
+    np.testing.assert_array_equal(got[0][0], ref["a"][0])
+    np.testing.assert_array_equal(got[0][1], ref["a"][1])
+    with pytest.raises(ValueError, match=r"one-dimensional, got shape \(\)"):
+        hostpack.pack_rows([{"a": 7}], ["a"], _as_id_array)
+    with pytest.raises(ValueError, match=r"one-dimensional, got shape \(1, 2\)"):
+        hostpack.pack_rows([{"a": [[1, 2]]}], ["a"], _as_id_array)
+    with pytest.raises(ValueError, match=r"one-dimensional, got shape \(2, 1\)"):
+        hostpack.pack_rows([{"a": np.zeros((2, 1), np.int64)}], ["a"], _as_id_array)
