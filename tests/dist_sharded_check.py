@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
 import paper_2211_05239_b200 as R  # noqa: E402
-from paper_2211_05239_b200.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
+from tools.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
                                            generate_clustered_batch)
 from paper_2211_05239_b200.peer import PeerShardedStep  # noqa: E402
 from paper_2211_05239_b200.sharded import ShardedTrainStep  # noqa: E402

@@ -6,7 +6,7 @@ import hashlib
 import numpy as np
 
 from conftest import golden
-from paper_2211_05239_b200.datagen import (FeatureSpec, SampleCountDist, SessionConfig,
+from tools.datagen import (FeatureSpec, SampleCountDist, SessionConfig,
                                            cfg1_specs, generate_clustered_batch)
 
 

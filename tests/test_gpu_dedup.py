@@ -74,7 +74,7 @@ def test_batched_groups_one_call_equals_per_group():
 
 
 def test_cfg1_all_keys_bit_exact():
-    from paper_2211_05239_b200.datagen import (SampleCountDist, SessionConfig, cfg1_specs,
+    from tools.datagen import (SampleCountDist, SessionConfig, cfg1_specs,
                                                generate_clustered_batch)
     g = golden("datagen")
     batch = generate_clustered_batch(SessionConfig(600, SampleCountDist("geometric", 16.5), 0),

@@ -15,7 +15,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 import paper_2211_05239_b200 as R  # noqa: E402
-from paper_2211_05239_b200.datagen import SampleCountDist, SessionConfig, cfg2_specs, generate_clustered_batch  # noqa: E402,E501
+from tools.datagen import SampleCountDist, SessionConfig, cfg2_specs, generate_clustered_batch  # noqa: E402,E501
 from paper_2211_05239_b200.step import TrainStep  # noqa: E402
 
 B, VOCAB, D = 65536, 1_000_000, 128

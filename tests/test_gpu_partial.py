@@ -14,7 +14,7 @@ from conftest import golden
 pytestmark = pytest.mark.gpu
 
 import paper_2211_05239_b200 as R  # noqa: E402
-from paper_2211_05239_b200.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
+from tools.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
                                            generate_clustered_batch)
 
 

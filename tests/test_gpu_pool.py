@@ -76,7 +76,7 @@ def test_worked_group_sum():
 def test_cfg1_fused_dedup_path_equals_kjt_path(op):
     """The equivalence oracle of the reference (trainer_sim.py:494-496):
     dedup-mode outputs are bit-identical to baseline-mode outputs."""
-    from paper_2211_05239_b200.datagen import (SampleCountDist, SessionConfig, cfg1_specs,
+    from tools.datagen import (SampleCountDist, SessionConfig, cfg1_specs,
                                                generate_clustered_batch)
     batch = generate_clustered_batch(SessionConfig(600, SampleCountDist("geometric", 16.5), 0),
                                      cfg1_specs(), 4096)

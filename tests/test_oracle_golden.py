@@ -28,7 +28,7 @@ def test_oracle_dedup_matches_reference(case):
 
 
 def test_oracle_cfg1_dedup_matches_reference():
-    from paper_2211_05239_b200.datagen import (SampleCountDist, SessionConfig, cfg1_specs,
+    from tools.datagen import (SampleCountDist, SessionConfig, cfg1_specs,
                                                generate_clustered_batch)
     g = golden("datagen")
     cfg = SessionConfig(600, SampleCountDist("geometric", 16.5), 0)

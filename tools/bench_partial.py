@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import paper_2211_05239_b200 as R  # noqa: E402
-from paper_2211_05239_b200.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
+from tools.datagen import (FeatureSpec, SampleCountDist, SessionConfig,  # noqa: E402
                                            generate_clustered_batch)
 
 
