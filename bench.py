@@ -458,7 +458,7 @@ def run_single(args, dev):
                   for i, k in enumerate(keys)}
     caps = {k: batch.values[k].size for k in keys}
     step = TrainStep([[k] for k in keys], args.batch, caps, tables, "sum", args.lr, args.mode, dev,
-                     overlap=not args.no_overlap)
+                     overlap=not args.no_overlap, slots=1 if (args.no_e2e or args.profile) else 2)
     step.load_batch(batch.values, batch.offsets)
     step.fill_grad_out(1)
     torch.cuda.synchronize()
@@ -557,9 +557,10 @@ def run_single(args, dev):
     e2e = None
     if not args.no_e2e and not args.profile:
         e2e = e2e_pipelined(step, batch, keys, step.replay, dev, max(4, min(args.steps, 20)), 1)
-        e2e["how"] = ("public TrainStep API: pinned-host KJT -> H2D on a copy stream "
-                      "(double-buffered, overlaps the previous step) -> graph replay -> D2H of "
-                      "the step's dedup counts read by the host")
+        e2e["how"] = ("public TrainStep API: pinned-host KJT -> H2D on a copy stream straight "
+                      "into the step's other input slot (overlaps the previous step; one CUDA "
+                      "graph per slot, value counts read on the device, no device-to-device "
+                      "copy) -> graph replay -> D2H of the step's dedup counts read by the host")
 
     # ------------------------------------------------------ CPU baseline
     cpu = None
@@ -648,6 +649,7 @@ def e2e_pipelined(step, batch, keys, replay, dev, n_steps, world, dist=None):
     h2d = sum(pin_v[k].numel() * 8 + pin_o[k].numel() * 8 for k in keys)
     pipe = H2DPipeline(step, dev)
     res = [torch.empty(step.counts.numel(), dtype=torch.int64).pin_memory() for _ in range(2)]
+    direct = pipe.direct
     done = [torch.cuda.Event(), torch.cuda.Event()]
     torch.cuda.synchronize()
     if dist is not None:
@@ -657,8 +659,11 @@ def e2e_pipelined(step, batch, keys, replay, dev, n_steps, world, dist=None):
     for i in range(n_steps):
         if i + 1 < n_steps:
             pipe.prefetch((i + 1) % 2, pin_v, pin_o)
-        pipe.install(i % 2)
-        replay()
+        if direct:   # the step reads the staged slot itself (one graph per slot)
+            pipe.run(i % 2, replay)
+        else:
+            pipe.install(i % 2)
+            replay()
         res[i % 2].copy_(step.counts, non_blocking=True)
         done[i % 2].record()
         if i >= 1:

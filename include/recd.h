@@ -168,6 +168,19 @@ int recd_dedup_copy(int32_t num_groups, const int32_t* group_sizes, int64_t batc
                     int64_t* const* uoffsets_out, int64_t* const* uvalues_out, int64_t* counts_out,
                     int64_t* const* remote_values, const int64_t* const* remote_base,
                     void* scratch, size_t scratch_bytes, recd_stream_t stream);
+/* recd_dedup with the input value counts on the DEVICE (num_values_dev, int64[F],
+ * written with the batch) and host capacities (value_caps >= every batch's
+ * counts) for the launch geometry, so one captured CUDA graph serves every
+ * batch: the reference's convert takes any batch (reader.py:160-175).
+ *   phase  1 = number only (recd_dedup_number), 2 = copy only (recd_dedup_copy,
+ *          remote_values / remote_base optional), 3 = both (recd_dedup) */
+int recd_dedup_ex(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+                  const int64_t* const* values, const int64_t* const* offsets,
+                  const int64_t* value_caps, const int64_t* num_values_dev, int32_t phase,
+                  int64_t* const* inverse_out, int64_t* const* uoffsets_out,
+                  int64_t* const* uvalues_out, int64_t* counts_out,
+                  int64_t* const* remote_values, const int64_t* const* remote_base,
+                  void* scratch, size_t scratch_bytes, recd_stream_t stream);
 
 /* ------------------------------------------------------------- pool bwd --
  * grad_u[u] = sum_{i: inverse[i]=u} grad_out[i]  (ascending i; /len for avg),

@@ -43,6 +43,8 @@ _SIGS = {
     "recd_dedup_number": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _pp, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_dedup_copy": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _pp, _pp, _pp, _vp, _pp, _pp, _vp, _sz,
                                _vp]),
+    "recd_dedup_ex": (_i32, [_i32, _p32, _i64, _pp, _pp, _p64, _vp, _i32, _pp, _pp, _pp, _vp, _pp,
+                             _pp, _vp, _sz, _vp]),
     "recd_pool_fwd": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _pp, _pp, _pp,
                              _vp, _vp]),
     "recd_pool_fwd_scatter": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _i32, _pp, _pp,

@@ -39,7 +39,8 @@ struct DedupParams {
   int feat_group[RECD_MAX_FEAT];
   const int64_t* values[RECD_MAX_FEAT];
   const int64_t* offsets[RECD_MAX_FEAT];
-  int64_t nvalues[RECD_MAX_FEAT];
+  int64_t nvalues[RECD_MAX_FEAT];  // host: value counts, or capacities when nv_dev is set
+  const int64_t* nv_dev;            // device [F] value counts (one graph for any batch), or null
   int64_t* inverse[RECD_MAX_FEAT];
   int64_t* uoffsets[RECD_MAX_FEAT];
   int64_t* uvalues[RECD_MAX_FEAT];
@@ -66,6 +67,11 @@ struct DedupParams {
   const int64_t* rbase[RECD_MAX_FEAT];  // k_rowscan: groups in launch order (most values first)
 };
 
+// number of KJT values of feature f (the last row runs to it, tensors.py:65-66)
+__device__ __forceinline__ int64_t nval(const DedupParams& p, int f) {
+  return p.nv_dev ? __ldg(p.nv_dev + f) : p.nvalues[f];
+}
+
 __device__ __forceinline__ int64_t row_begin(const int64_t* off, int64_t i) { return off[i]; }
 __device__ __forceinline__ int64_t row_end(const int64_t* off, int64_t i, int64_t B, int64_t nv) {
   return (i + 1 < B) ? off[i + 1] : nv;
@@ -75,8 +81,8 @@ __device__ bool rows_equal(const DedupParams& p, int g, int64_t a, int64_t b) {
   for (int f = p.group_first[g]; f < p.group_first[g + 1]; ++f) {
     const int64_t* off = p.offsets[f];
     const int64_t* val = p.values[f];
-    int64_t sa = off[a], ea = row_end(off, a, p.B, p.nvalues[f]);
-    int64_t sb = off[b], eb = row_end(off, b, p.B, p.nvalues[f]);
+    int64_t sa = off[a], ea = row_end(off, a, p.B, nval(p, f));
+    int64_t sb = off[b], eb = row_end(off, b, p.B, nval(p, f));
     if (ea - sa != eb - sb) return false;
     for (int64_t k = 0; k < ea - sa; ++k)
       if (val[sa + k] != val[sb + k]) return false;
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
   for (int f = fbeg; f < fend; ++f) {
     const int64_t* off = p.offsets[f];
     const int64_t* val = p.values[f];
-    const int64_t nv = p.nvalues[f];
+    const int64_t nv = nval(p, f);
     for (int j = tid; j <= n; j += RS_NT) {
       const int64_t i = r0 + j;
       s_start[j] = (i < p.B) ? off[i] : nv;
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
       const int fi = f - fbeg;
       const int64_t* off = p.offsets[f];
       const int64_t st = (f == fend - 1) ? s_start[j] : off[row];
-      const int64_t len = (f == fend - 1) ? s_start[j + 1] - st : row_end(off, row, p.B, p.nvalues[f]) - st;
+      const int64_t len = (f == fend - 1) ? s_start[j + 1] - st : row_end(off, row, p.B, nval(p, f)) - st;
       const int64_t* val = p.values[f] + st;
       if (lane == 0) h += len_hash(len, fi);
       for (int64_t k0 = 0; k0 < len; k0 += 128) {
@@ -386,7 +392,7 @@ __global__ void __launch_bounds__(NB_NT) k_num_reduce(const __grid_constant__ De
     int64_t ls = 0;
 #pragma unroll
     for (int k = 0; k < NB_ITEMS; ++k)
-      if (first[k]) ls += row_end(off, i0 + k, B, p.nvalues[f]) - off[i0 + k];
+      if (first[k]) ls += row_end(off, i0 + k, B, nval(p, f)) - off[i0 + k];
     block_exclusive_scan<NB_NT>(ls, s_scan, &tot);
     if (tid == 0) p.nb_len[(int64_t)f * nch + c] = tot;
   }
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(NB_NT) k_num_down(const __grid_constant__ Dedu
     int64_t ls = 0;
 #pragma unroll
     for (int k = 0; k < NB_ITEMS; ++k) {
-      len[k] = first[k] ? row_end(off, i0 + k, B, p.nvalues[f]) - off[i0 + k] : 0;
+      len[k] = first[k] ? row_end(off, i0 + k, B, nval(p, f)) - off[i0 + k] : 0;
       ls += len[k];
     }
     int64_t o = p.nb_len[(int64_t)f * nch + c] + block_exclusive_scan<NB_NT>(ls, s_scan, &tot);
@@ -643,7 +649,8 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
                      const int64_t* num_values, int64_t* const* inverse_out,
                      int64_t* const* uoffsets_out, int64_t* const* uvalues_out, int64_t* counts_out,
                      void* scratch, size_t scratch_bytes, cudaStream_t stream, int phase,
-                     int64_t* const* remote_values, const int64_t* const* remote_base) {
+                     int64_t* const* remote_values, const int64_t* const* remote_base,
+                     const int64_t* num_values_dev = nullptr) {
   if (num_groups <= 0 || batch_size <= 0 || batch_size >= (1ll << 31) || !group_sizes)
     return RECD_ERR_ARG;
   int F = 0;
@@ -669,6 +676,7 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
     p.B = B;
     p.C = C;
     p.hash_mask = g_hash_mask;
+    p.nv_dev = num_values_dev ? num_values_dev + f0 : nullptr;
     int f = 0;
     for (int g = 0; g < p.G; ++g) {
       p.group_first[g] = f;
@@ -783,4 +791,24 @@ extern "C" int recd_dedup_copy(int32_t num_groups, const int32_t* group_sizes, i
   return run_dedup(num_groups, group_sizes, batch_size, values, offsets, num_values, inverse_out,
                    uoffsets_out, uvalues_out, counts_out, scratch, scratch_bytes,
                    (cudaStream_t)stream, DD_COPY, remote_values, remote_base);
+}
+
+// recd_dedup with the per-feature value counts on the device (num_values_dev,
+// int64[F]) and host capacities (value_caps) for the launch geometry: the
+// counts of a new batch are written to device memory together with its
+// values, so one captured graph serves every batch up to the capacities.
+// phase: 1 = number (inverse, unique offsets, counts), 2 = copy (unique values,
+// optionally also into remote_values at *remote_base), 3 = both.
+extern "C" int recd_dedup_ex(int32_t num_groups, const int32_t* group_sizes, int64_t batch_size,
+                             const int64_t* const* values, const int64_t* const* offsets,
+                             const int64_t* value_caps, const int64_t* num_values_dev,
+                             int32_t phase, int64_t* const* inverse_out,
+                             int64_t* const* uoffsets_out, int64_t* const* uvalues_out,
+                             int64_t* counts_out, int64_t* const* remote_values,
+                             const int64_t* const* remote_base, void* scratch,
+                             size_t scratch_bytes, recd_stream_t stream) {
+  if (!num_values_dev || !value_caps || phase < 1 || phase > 3) return RECD_ERR_ARG;
+  return run_dedup(num_groups, group_sizes, batch_size, values, offsets, value_caps, inverse_out,
+                   uoffsets_out, uvalues_out, counts_out, scratch, scratch_bytes,
+                   (cudaStream_t)stream, phase, remote_values, remote_base, num_values_dev);
 }

@@ -55,11 +55,17 @@ class EmbeddingTable:
         self.key, self.rows, self.dim = key, int(rows), int(dim)
         self.weights = weights.contiguous()
 
+    @staticmethod
+    def init_weights(key: str, rows: int, dim: int, seed: int) -> np.ndarray:
+        """The reference's seeded init (trainer_sim.py:62-66, 83-87): numpy
+        uniform(-0.1, 0.1) from SeedSequence((seed, blake2b(key))), host side."""
+        rng = _key_seed(seed, "table", key)
+        return rng.uniform(-0.1, 0.1, size=(rows, dim)).astype(np.float32)
+
     @classmethod
     def create(cls, key: str, rows: int, dim: int, seed: int, device=None) -> "EmbeddingTable":
         """Bit-identical to the reference's seeded init (numpy RNG on host)."""
-        rng = _key_seed(seed, "table", key)
-        w = rng.uniform(-0.1, 0.1, size=(rows, dim)).astype(np.float32)
+        w = cls.init_weights(key, rows, dim, seed)
         return cls(key, rows, dim, torch.from_numpy(w).to(device or default_device()))
 
     @classmethod

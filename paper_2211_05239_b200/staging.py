@@ -2,11 +2,18 @@
 
 The KJT of a cfg2 batch is ~1 GB of int64 per GPU, so end to end the step is
 bound by the PCIe copy, not by the kernels.  `H2DPipeline` copies batch i+1
-from pinned host memory into one of two device staging slots on a dedicated
-copy stream while step i runs, then installs it into the step's input
-buffers with one device-to-device copy (the CUDA graph stays bound to those
-buffers).  Works with TrainStep, ShardedTrainStep and PeerShardedStep (any
-object with `keys`, `in_values`, `in_offsets`, `nvalues`).
+from pinned host memory on a dedicated copy stream while step i runs.
+
+With a step that owns input slots (`TrainStep(slots=2)`: one CUDA graph per
+slot, value counts read on the device) the copy goes straight into the slot
+the next step reads -- values, offsets and the value counts -- and nothing is
+copied device-to-device: `run(slot, replay)` makes the step wait for the
+slot's copy, replays that slot's graph and releases the slot to the copy
+stream when the step is done with it.  Any batch up to the capacities works.
+
+Steps without slots (the sharded steps, whose graphs are bound to one set of
+input buffers and value counts) get the slot copied into their inputs by
+`install(slot)` (one device-to-device copy per step).
 """
 
 from __future__ import annotations
@@ -19,36 +26,67 @@ __all__ = ["H2DPipeline"]
 
 
 class H2DPipeline:
-    def __init__(self, step, device=None):
+    def __init__(self, step, device=None, nslots: int = 2):
         self.step = step
+        self.direct = getattr(step, "nslots", 1) >= nslots
         self.dev = device or step.in_values[0].device
         self.copy = torch.cuda.Stream(self.dev)
-        self.slots = [([torch.empty_like(v) for v in step.in_values],
-                       [torch.empty_like(o) for o in step.in_offsets]) for _ in range(2)]
-        self.counts = [None, None]
-        self.ready = [torch.cuda.Event() for _ in range(2)]
-        self.free = [torch.cuda.Event() for _ in range(2)]
-        self._freed = [False, False]
+        self.n = nslots
+        if self.direct:
+            self.slots = [(step.slot_values[s], step.slot_offsets[s]) for s in range(nslots)]
+        else:
+            self.slots = [([torch.empty_like(v) for v in step.in_values],
+                           [torch.empty_like(o) for o in step.in_offsets]) for _ in range(nslots)]
+        F = len(step.keys)
+        self._pin_counts = [torch.zeros(F, dtype=torch.int64).pin_memory() for _ in range(nslots)]
+        self._pc_done = [None] * nslots   # the last H2D copy out of _pin_counts[slot]
+        self.counts = [None] * nslots
+        self.ready = [torch.cuda.Event() for _ in range(nslots)]
+        self.free = [torch.cuda.Event() for _ in range(nslots)]
+        self._freed = [False] * nslots
 
     def prefetch(self, slot: int, values: dict, offsets: dict) -> None:
         """Queue the H2D copy of one batch (pinned host tensors) into `slot`."""
         vals, offs = self.slots[slot]
-        n = []
+        n = [values[k].numel() for k in self.step.keys]
+        for f, k in enumerate(self.step.keys):
+            if n[f] > vals[f].numel():
+                raise ValueError(f"feature {k!r}: batch exceeds the step's capacity")
         with torch.cuda.stream(self.copy):
             if self._freed[slot]:
-                self.copy.wait_event(self.free[slot])
+                self.copy.wait_event(self.free[slot])   # the step is done reading the slot
             for f, k in enumerate(self.step.keys):
-                v = values[k]
-                if v.numel() > vals[f].numel():
-                    raise ValueError(f"feature {k!r}: batch exceeds the step's capacity")
-                vals[f][: v.numel()].copy_(v, non_blocking=True)
+                vals[f][: n[f]].copy_(values[k], non_blocking=True)
                 offs[f].copy_(offsets[k], non_blocking=True)
-                n.append(v.numel())
+            if self.direct:
+                pc = self._pin_counts[slot]
+                if self._pc_done[slot] is not None:
+                    self._pc_done[slot].synchronize()   # host buffer free again
+                pc.copy_(torch.tensor(n, dtype=torch.int64))
+                F = len(n)
+                self.step.in_counts[slot, F:].copy_(pc, non_blocking=True)
+                self._pc_done[slot] = torch.cuda.Event()
+                self._pc_done[slot].record(self.copy)
             self.ready[slot].record(self.copy)
         self.counts[slot] = n
 
-    def install(self, slot: int) -> None:
-        """Make `slot` the step's input (on the current stream, after its copy)."""
+    def run(self, slot: int, replay) -> None:
+        """Run one step on `slot` (after its copy), then hand the slot back to
+        the copy stream.  `replay` launches the step (e.g. step.replay)."""
+        cur = torch.cuda.current_stream(self.dev)
+        cur.wait_event(self.ready[slot])
+        if self.direct:
+            self.step.use_slot(slot)
+            self.step.slot_nvalues[slot] = list(self.counts[slot])
+        else:
+            self.install(slot, _record=False)
+        replay()
+        self.free[slot].record(cur)
+        self._freed[slot] = True
+
+    def install(self, slot: int, _record: bool = True) -> None:
+        """Copy `slot` into a slot-less step's inputs (on the current stream,
+        after its H2D copy)."""
         cur = torch.cuda.current_stream(self.dev)
         cur.wait_event(self.ready[slot])
         vals, offs = self.slots[slot]
@@ -61,5 +99,6 @@ class H2DPipeline:
         for f in range(len(vals)):
             self.step.in_values[f][: n[f]].copy_(vals[f][: n[f]], non_blocking=True)
             self.step.in_offsets[f].copy_(offs[f], non_blocking=True)
-        self.free[slot].record(cur)
-        self._freed[slot] = True
+        if _record:
+            self.free[slot].record(cur)
+            self._freed[slot] = True

@@ -41,9 +41,17 @@ class StepCounts:
 
 
 class TrainStep:
+    """One training step over `slots` input slots (each slot: the KJT values,
+    offsets and value counts of one batch, all on the device).  With slots=2 a
+    copy stream fills one slot while the step runs on the other, and
+    capture() records one CUDA graph per slot, so no batch is ever copied
+    device-to-device and any batch up to the value capacities replays the
+    same graph (the counts are read on the device, recd_dedup_ex)."""
+
     def __init__(self, groups: Sequence[Sequence[str]], batch_size: int,
                  value_caps: dict[str, int], tables: dict[str, EmbeddingTable], op: str = "sum",
-                 lr: float = 0.01, mode: str = "dedup", device=None, overlap: bool = True):
+                 lr: float = 0.01, mode: str = "dedup", device=None, overlap: bool = True,
+                 slots: int = 1):
         if mode not in ("dedup", "kjt"):
             raise ValueError(f"unknown mode {mode!r}")
         self.lib = _lib.load()
@@ -53,6 +61,8 @@ class TrainStep:
         self.B = int(batch_size)
         self.mode = mode
         self.op = op
+        if op not in ("sum", "avg", "mean"):
+            raise ValueError(f"the training step needs sum/avg pooling (max has no backward), got {op!r}")
         self.mode_id = _lib.POOL_MODES[op]
         self.lr = float(lr)
         self.overlap = bool(overlap)
@@ -62,15 +72,23 @@ class TrainStep:
         dev, B, D, F = self.dev, self.B, self.D, self.F
         i64 = torch.int64
         self.caps = [max(int(value_caps[k]), 1) for k in self.keys]
-        # KJT input slots
-        self.in_values = [torch.zeros(c, dtype=i64, device=dev) for c in self.caps]
-        self.in_offsets = [torch.zeros(B, dtype=i64, device=dev) for _ in self.keys]
-        self.nvalues = list(self.caps)
+        # KJT input slots: values, offsets, value counts (device)
+        self.nslots = max(1, int(slots))
+        self.slot_values = [[torch.zeros(c, dtype=i64, device=dev) for c in self.caps]
+                            for _ in range(self.nslots)]
+        self.slot_offsets = [[torch.zeros(B, dtype=i64, device=dev) for _ in self.keys]
+                             for _ in range(self.nslots)]
+        # per slot: [B] * F + the value counts -- the KJT's own counts layout
+        # (recd_pool_fwd / _bwd in kjt mode), and the device counts recd_dedup_ex reads
+        self.in_counts = torch.zeros((self.nslots, 2 * F), dtype=i64, device=dev)
+        self.in_counts[:, :F] = B
+        self.slot_nvalues = [[0] * F for _ in range(self.nslots)]
+        self.slot = 0
         # IKJT outputs (worst case) + device counts
         self.inverse = [torch.empty(B, dtype=i64, device=dev) for _ in self.groups]
         self.uoffsets = [torch.empty(B, dtype=i64, device=dev) for _ in self.keys]
         self.uvalues = [torch.empty(c, dtype=i64, device=dev) for c in self.caps]
-        self.counts = torch.zeros(2 * F, dtype=i64, device=dev)
+        self._dcounts = torch.zeros(2 * F, dtype=i64, device=dev)
         self.pooled = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
         self.out = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
         self.grad_out = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
@@ -81,26 +99,58 @@ class TrainStep:
         self.bwd_scratch = torch.empty(
             max(self.lib.recd_pool_bwd_scratch_bytes(F, B, D, _lib.i64s(self.caps)), 256),
             dtype=torch.uint8, device=dev)
+        self.graphs: list = [None] * self.nslots
         self._build_args()
-        self.graph = None
+
+    # current slot's buffers (the step's inputs)
+    @property
+    def in_values(self):
+        return self.slot_values[self.slot]
+
+    @property
+    def in_offsets(self):
+        return self.slot_offsets[self.slot]
+
+    @property
+    def nvalues(self):
+        return self.slot_nvalues[self.slot]
+
+    @property
+    def counts(self):
+        """Device int64[2F] (U per feature, N_u per feature) of the step's IKJT
+        (kjt mode: B and the slot's value counts)."""
+        return self._dcounts if self.mode == "dedup" else self.in_counts[self.slot]
+
+    @property
+    def graph(self):
+        return self.graphs[self.slot]
 
     # ------------------------------------------------------------- inputs
     def load_batch(self, values: dict[str, np.ndarray | torch.Tensor],
-                   offsets: dict[str, np.ndarray | torch.Tensor], non_blocking=False) -> None:
-        """Copy one KJT batch into the input slots (host or device sources)."""
+                   offsets: dict[str, np.ndarray | torch.Tensor], non_blocking=False,
+                   slot: int | None = None) -> None:
+        """Copy one KJT batch (host or device sources) into an input slot
+        (default: the current one).  Any value counts up to the capacities."""
+        s = self.slot if slot is None else int(slot)
+        n = []
         for f, k in enumerate(self.keys):
             v = torch.as_tensor(values[k])
             o = torch.as_tensor(offsets[k])
-            n = v.numel()
-            if n > self.caps[f] or o.numel() != self.B:
+            if v.numel() > self.caps[f] or o.numel() != self.B:
                 raise ValueError(f"feature {k!r}: batch exceeds the step's capacity")
-            self.in_values[f][:n].copy_(v, non_blocking=non_blocking)
-            self.in_offsets[f].copy_(o, non_blocking=non_blocking)
-            self.nvalues[f] = n
+            self.slot_values[s][f][: v.numel()].copy_(v, non_blocking=non_blocking)
+            self.slot_offsets[s][f].copy_(o, non_blocking=non_blocking)
+            n.append(v.numel())
+        self.in_counts[s, self.F:].copy_(torch.tensor(n, dtype=torch.int64),
+                                          non_blocking=non_blocking)
+        self.slot_nvalues[s] = n
+
+    def use_slot(self, slot: int) -> None:
+        """Make `slot` the step's input (eager calls and replay() use it)."""
+        if not 0 <= slot < self.nslots:
+            raise ValueError(f"slot {slot} out of range for {self.nslots} slots")
+        self.slot = int(slot)
         self._build_args()
-        if self.mode == "kjt":
-            c = [self.B] * self.F + list(self.nvalues)
-            self.counts.copy_(torch.tensor(c, dtype=torch.int64))
 
     def fill_grad_out(self, seed: int = 1) -> None:
         g = torch.Generator(device=self.dev)
@@ -114,7 +164,7 @@ class TrainStep:
         self.a_gsizes = L.i32s([len(g) for g in self.groups])
         self.a_in_values = L.ptrs(self.in_values)
         self.a_in_offsets = L.ptrs(self.in_offsets)
-        self.a_nvalues = L.i64s(self.nvalues)
+        self.in_counts_ptr = self.in_counts[self.slot, self.F:].data_ptr()
         self.a_inverse_g = L.ptrs(self.inverse)
         self.a_uoffsets = L.ptrs(self.uoffsets)
         self.a_uvalues = L.ptrs(self.uvalues)
@@ -141,11 +191,13 @@ class TrainStep:
     def dedup(self, stream: int) -> None:
         if self.mode != "dedup":
             return
-        rc = self.lib.recd_dedup(len(self.groups), self.a_gsizes, self.B, self.a_in_values,
-                                 self.a_in_offsets, self.a_nvalues, self.a_inverse_g,
-                                 self.a_uoffsets, self.a_uvalues, self.counts.data_ptr(),
-                                 self.dedup_scratch.data_ptr(), self.dedup_scratch.numel(), stream)
-        _lib.check(rc, "recd_dedup")
+        rc = self.lib.recd_dedup_ex(len(self.groups), self.a_gsizes, self.B, self.a_in_values,
+                                    self.a_in_offsets, self.a_caps, self.in_counts_ptr, 3,
+                                    self.a_inverse_g, self.a_uoffsets, self.a_uvalues,
+                                    self.counts.data_ptr(), None, None,
+                                    self.dedup_scratch.data_ptr(), self.dedup_scratch.numel(),
+                                    stream)
+        _lib.check(rc, "recd_dedup_ex")
 
     def forward(self, stream: int) -> None:
         """Pooled lookup over the unique rows (k_pool_fwd only)."""
@@ -204,21 +256,30 @@ class TrainStep:
         self.backward_finish(main.cuda_stream)
 
     def capture(self) -> None:
-        """Record run() into a CUDA graph (replayed by replay())."""
+        """Record run() into one CUDA graph per input slot (replay() launches
+        the current slot's).  Runs one eager warm-up step on the current slot."""
+        cur = self.slot
         s = torch.cuda.Stream(self.dev)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
             self.run()  # warm-up on the side stream
         torch.cuda.current_stream(self.dev).wait_stream(s)
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self.run()
+        for k in range(self.nslots):
+            self.use_slot(k)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.run()
+            self.graphs[k] = g
+        self.use_slot(cur)
 
-    def replay(self) -> None:
-        if self.graph is None:
+    def replay(self, slot: int | None = None) -> None:
+        if slot is not None and slot != self.slot:
+            self.use_slot(slot)
+        g = self.graphs[self.slot]
+        if g is None:
             self.run()
         else:
-            self.graph.replay()
+            g.replay()
 
     def check(self) -> None:
         """Raise the reference's ValueError (trainer_sim.py:312-320) if the last

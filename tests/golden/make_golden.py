@@ -4,7 +4,7 @@ Run in the build container (where `/root/reference` exists):
 
     python tests/golden/make_golden.py
 
-Writes `tests/golden/{dedup,pool,jagged,slice,datagen,errors,transforms,wire,partial}.npz`.  These
+Writes `tests/golden/{dedup,pool,jagged,slice,datagen,errors,transforms,wire,partial,sdd}.npz`.  These
 fixtures pin the oracle restatement (`oracle/`) and the CUDA path; the GPU box
 never needs `/root/reference`.
 """
@@ -282,6 +282,53 @@ def make_wire():
     np.savez_compressed(OUT / "wire.npz", **store)
 
 
+def make_sdd():
+    """IterationStats of the real forward_iteration (trainer_sim.py:484-586):
+    the sdd all-to-all bytes (trainer_sim.py:281-305), the pooled rows sent
+    back, lookups, activation peak, pooling MACs and index-select elements,
+    dedup vs baseline, R in {1, 2, 4, 8} ranks, element + attention pooling +
+    a plain key.  Inputs: the reference generator's clustered records."""
+    specs = [DG.FeatureSpec("u", "user_sequence", 3.5, 60, 0.3, sync_group="g"),
+             DG.FeatureSpec("v", "user_sequence", 2.0, 60, 0.3, sync_group="g"),
+             DG.FeatureSpec("w", "user_sequence", 6.5, 3000, 0.25),
+             DG.FeatureSpec("x", "user_sequence", 12.0, 3000, 0.1),
+             DG.FeatureSpec("y", "user_sequence", 4.0, 3000, 0.4),
+             DG.FeatureSpec("it", "item", 2.5, 500)]
+    cfg = DG.SessionConfig(num_sessions=90, samples_per_session=DG.SampleCountDist("geometric", 8.0),
+                           seed=3)
+    recs = DG.generate_dataset(cfg, specs)
+    recs.sort(key=lambda r: (r.session_id, r.timestamp))
+    rows = recs[:403]          # not a multiple of 8: split_batch's uneven chunks
+    keys = [s.key for s in specs]
+    dim = 8
+    spec = TS.ModelSpec(
+        tables={k: TS.TableConfig(rows=s.vocab_size, dim=dim) for k, s in zip(keys, specs)},
+        groups=(TS.GroupConfig(("u", "v"), "attention"), TS.GroupConfig(("w",), "sum"),
+                TS.GroupConfig(("x",), "avg"), TS.GroupConfig(("y",), "max")),
+        plain={"it": "sum"}, seed=0)
+    rspec = RD.DataloaderSpec(keys=tuple(keys),
+                              dedup_sparse_features=(("u", "v"), ("w",), ("x",), ("y",)),
+                              batch_size=len(rows))
+    store = {"rows/keys": np.array(keys), "dim": np.array([dim])}
+    kjt = T.build_kjt(rows, keys)
+    for k in keys:
+        store[f"in/{k}/values"] = np.array(kjt.entries[k].values)
+        store[f"in/{k}/offsets"] = np.array(kjt.entries[k].offsets)
+    fields = ["a2a_bytes_fwd", "a2a_bytes_back", "lookup_count", "activation_elements",
+              "pooling_mac_count", "index_select_elements"]
+    store["fields"] = np.array(fields)
+    tables = TS.build_tables(spec)
+    for mode, rs in (("dedup", rspec), ("baseline", rspec.without_dedup())):
+        batch = RD.convert(rows, rs)
+        for R in (1, 2, 4, 8):
+            plan = TS.make_round_robin_plan(spec, R)
+            scores, st = TS.forward_iteration(batch, spec, plan, mode, tables)
+            store[f"{mode}/R{R}/stats"] = np.array([getattr(st, f) for f in fields], dtype=np.int64)
+            store[f"{mode}/R{R}/plan"] = np.array([plan.assignment[k] for k in keys])
+            store[f"{mode}/R{R}/scores"] = scores
+    np.savez_compressed(OUT / "sdd.npz", **store)
+
+
 def shifted_sessions(rng, b, vocab, max_len, p_shift=(0.5, 0.35, 0.15), mean_session=8.0):
     """Session-structured rows of one key: each session draws a length and a
     value pool; consecutive rows shift the window by 0, 1 or 2 (the reference
@@ -333,14 +380,10 @@ def make_partial():
 
 
 if __name__ == "__main__":
-    make_partial()
-    make_wire()
-    make_transforms()
-    make_dedup()
-    make_datagen()
-    make_pool()
-    make_jagged()
-    make_slice()
-    make_errors()
+    makers = {"partial": make_partial, "wire": make_wire, "transforms": make_transforms,
+              "dedup": make_dedup, "datagen": make_datagen, "pool": make_pool,
+              "jagged": make_jagged, "slice": make_slice, "errors": make_errors, "sdd": make_sdd}
+    for name in (sys.argv[1:] or list(makers)):   # e.g. `make_golden.py sdd`
+        makers[name]()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
