@@ -81,3 +81,60 @@ def test_dedup_step_equals_kjt_step_and_is_deterministic(batch):
         scale = float(u_k.abs().max())
         assert scale > 0
         torch.testing.assert_close(u_d, u_k, rtol=1e-5, atol=1e-5 * scale)
+
+
+def test_full_cfg2_against_oracle_touched_rows():
+    """The bench's exact workload -- cfg2 B = 65,536, 26 keys, 26 tables of
+    10M x 128 fp32 (133 GB on one B200) -- one TrainStep (dedup, pooled
+    lookup, expand, backward + fused SGD), then for a length-8, a length-128
+    and a length-256 key: IKJT, expanded pooled output and every SGD-updated
+    table row bit-exact against the oracle (which sees only the touched rows:
+    the unique IDs' rows, remapped into a compact table), untouched rows
+    unchanged.  This exercises the 10M-row / 27M-unique-value code paths
+    (32-bit chunk-relative positions, (f << 24) | u tags, 24-bit sort keys)."""
+    rows, lr = 10_000_000, 0.05
+    nsess = int(np.ceil(B / 16.5 * 1.3)) + 64       # bench.make_batch's session count
+    b = generate_clustered_batch(SessionConfig(nsess, SampleCountDist("geometric", 16.5), 0),
+                                 cfg2_specs(rows), B)
+    keys = list(b.keys)
+    tables = {k: R.EmbeddingTable.create_on_device(k, rows, D, seed=i) for i, k in enumerate(keys)}
+    check = [0, 4, 5]       # list lengths 8, 128, 256
+    w0 = {}
+    for f in check:
+        k = keys[f]
+        inv, [(uv, uo)] = oracle.build_ikjt_arrays([(b.values[k], b.offsets[k])])
+        ids = np.unique(uv)
+        w0[k] = (inv, uv, uo, ids, tables[k].weights[torch.as_tensor(ids, device="cuda")].cpu().numpy())
+    probe = torch.randint(0, rows, (4096,), device="cuda")
+    before = {keys[f]: tables[keys[f]].weights[probe].clone() for f in check}
+    caps = {k: int(b.values[k].size) for k in keys}
+    step = TrainStep([[k] for k in keys], B, caps, tables, "sum", lr, "dedup")
+    step.load_batch(b.values, b.offsets)
+    step.fill_grad_out(11)
+    step.run()
+    torch.cuda.synchronize()
+    step.check()
+    for f in check:
+        k = keys[f]
+        inv, uv, uo, ids, wsub = w0[k]
+        np.testing.assert_array_equal(step.inverse[f].cpu().numpy(), inv)
+        U, NU = int(step.counts[f]), int(step.counts[len(keys) + f])
+        assert (U, NU) == (uo.size, uv.size)
+        np.testing.assert_array_equal(step.uoffsets[f][:U].cpu().numpy(), uo)
+        np.testing.assert_array_equal(step.uvalues[f][:NU].cpu().numpy(), uv)
+        loc = np.searchsorted(ids, uv)            # IDs -> rows of the compact table
+        ref = oracle.expand(oracle.pooled_lookup(loc, uo, wsub, "sum"), inv)
+        np.testing.assert_array_equal(step.out[f].cpu().numpy(), ref, err_msg=k)
+        del ref
+        G = step.grad_out[f].cpu().numpy()
+        gu = oracle.pool_backward(G, inv, uo.size)
+        lids, g = oracle.sparse_table_grad(gu, loc, uo, "sum")
+        assert np.array_equal(lids, np.arange(ids.size))
+        want = wsub - (np.float32(lr) * g).astype(np.float32)
+        got = tables[k].weights[torch.as_tensor(ids, device="cuda")].cpu().numpy()
+        np.testing.assert_array_equal(got, want, err_msg=k)
+        untouched = ~torch.isin(probe, torch.as_tensor(ids, device="cuda"))
+        assert torch.equal(tables[k].weights[probe][untouched], before[k][untouched])
+    del step
+    tables.clear()
+    torch.cuda.empty_cache()
