@@ -34,6 +34,10 @@ constexpr int OS_HCHUNK = OS_TILE * 4;         // elements per histogram block
 constexpr int OS_MAXSEG = 64;
 constexpr int OS_MAXPASS = 4;
 constexpr uint32_t OS_AGG = 1u << 30, OS_PRE = 2u << 30, OS_CNT = (1u << 30) - 1;
+#ifndef RECD_OS_LB
+#define RECD_OS_LB 8
+#endif
+constexpr int OS_LB = RECD_OS_LB;              // look-back tiles per round trip
 
 struct OsSeg {
   int64_t base;          // element offset of the segment
@@ -200,12 +204,29 @@ __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_c
       st_relaxed(my, OS_PRE | cnt);
     } else {
       st_relaxed(my, OS_AGG | cnt);
-      for (int64_t k = lt_ - 1; k >= 0;) {
-        const uint32_t v = ld_relaxed(st_cur + (sg.tcap0 + k) * 256 + tid);
-        if ((v & ~OS_CNT) == 0u) continue;  // not published yet
-        excl += v & OS_CNT;
-        if (v & OS_PRE) break;
-        --k;
+      // decoupled look-back, OS_LB predecessors per round trip: the loads of
+      // tiles k, k-1, ..., k-OS_LB+1 are independent, so a walk over many
+      // in-flight tiles costs one L2 latency per OS_LB tiles instead of per tile;
+      // the words are consumed in order up to the first unpublished one (retried)
+      // or the first inclusive prefix (done); tile 0 always publishes a prefix
+      const uint32_t* col = st_cur + sg.tcap0 * 256 + tid;
+      for (int64_t k = lt_ - 1;;) {
+        uint32_t v[OS_LB];
+#pragma unroll
+        for (int j = 0; j < OS_LB; ++j) v[j] = (k - j >= 0) ? ld_relaxed(col + (k - j) * 256) : OS_PRE;
+        int j = 0;
+        bool done = false;
+#pragma unroll
+        for (int q = 0; q < OS_LB; ++q) {
+          if (done || j < q) continue;                  // stopped earlier in this batch
+          const uint32_t w = v[q];
+          if ((w & ~OS_CNT) == 0u) continue;            // not published yet: retry from here
+          excl += w & OS_CNT;
+          if (w & OS_PRE) done = true;
+          j = q + 1;
+        }
+        if (done) break;
+        k -= j;
       }
       st_relaxed(my, OS_PRE | (excl + cnt));
     }
