@@ -88,6 +88,9 @@ def parse(argv=None):
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
                     help="run the backward's prepare half on the main stream")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="N=1: no cross-step pipelining (the next batch's dedup + backward prepare "
+                         "otherwise run on a side stream during the current step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0,
@@ -457,9 +460,12 @@ def run_single(args, dev):
         tables = {k: R.EmbeddingTable.create_on_device(k, args.rows, args.dim, seed=i, device=dev)
                   for i, k in enumerate(keys)}
     caps = {k: batch.values[k].size for k in keys}
+    pipe = not (args.no_pipeline or args.no_graph or args.profile)
     step = TrainStep([[k] for k in keys], args.batch, caps, tables, "sum", args.lr, args.mode, dev,
-                     overlap=not args.no_overlap, slots=1 if (args.no_e2e or args.profile) else 2)
-    step.load_batch(batch.values, batch.offsets)
+                     overlap=not args.no_overlap, slots=1 if (args.no_e2e or args.profile) else 2,
+                     pipeline=pipe)
+    for s_ in range(step.nslots):
+        step.load_batch(batch.values, batch.offsets, slot=s_)
     step.fill_grad_out(1)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
@@ -480,19 +486,22 @@ def run_single(args, dev):
         step.run()
     if not args.no_graph:
         step.capture()
-    for _ in range(max(1, args.warmup)):
-        step.replay()
+    if pipe:
+        step.prime(0)      # batch 0's IKJT + backward prepare; every replay then
+    for i in range(max(1, args.warmup)):   # trains batch i and prepares batch i + 1
+        step.replay(i % 2 if pipe else None)
     torch.cuda.synchronize()
 
     # ------------------------------------------------------ timed region
     sampler = ClockSampler(dev.index) if not args.profile else None
+    i0 = max(1, args.warmup)
     torch.cuda.synchronize()
     launches0 = R.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        step.replay()
+    for i in range(args.steps):
+        step.replay((i0 + i) % 2 if pipe else None)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -502,9 +511,14 @@ def run_single(args, dev):
     if not args.no_graph:
         # graph replays do not pass through the host counter: count one eager step
         l0 = R.launch_count()
-        step.run()
+        if pipe:
+            step.run_pipelined(0)
+        else:
+            step.run()
         launches_per_step = R.launch_count() - l0
         torch.cuda.synchronize()
+        if pipe:
+            step.use_slot(0, 0)
     value = B / (ms / 1e3)
 
     # --------------------------------------- per-phase timing (roofline)
@@ -556,11 +570,14 @@ def run_single(args, dev):
     # ----------------------------------------------------------- e2e
     e2e = None
     if not args.no_e2e and not args.profile:
-        e2e = e2e_pipelined(step, batch, keys, step.replay, dev, max(4, min(args.steps, 20)), 1)
-        e2e["how"] = ("public TrainStep API: pinned-host KJT -> H2D on a copy stream straight "
-                      "into the step's other input slot (overlaps the previous step; one CUDA "
-                      "graph per slot, value counts read on the device, no device-to-device "
-                      "copy) -> graph replay -> D2H of the step's dedup counts read by the host")
+        if pipe:
+            e2e = e2e_step_pipeline(step, batch, keys, dev, max(4, min(args.steps, 20)))
+        else:
+            e2e = e2e_pipelined(step, batch, keys, step.replay, dev, max(4, min(args.steps, 20)), 1)
+            e2e["how"] = ("public TrainStep API: pinned-host KJT -> H2D on a copy stream straight "
+                          "into the step's other input slot (overlaps the previous step; one CUDA "
+                          "graph per slot, value counts read on the device, no device-to-device "
+                          "copy) -> graph replay -> D2H of the step's dedup counts read by the host")
 
     # ------------------------------------------------------ CPU baseline
     cpu = None
@@ -680,6 +697,52 @@ def e2e_pipelined(step, batch, keys, replay, dev, n_steps, world, dist=None):
     return {"value": world * B / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d * world,
             "d2h_bytes_per_step": res[0].numel() * 8 * world, "ms_per_step": e2e_s * 1e3,
             "h2d_gbs_per_gpu": h2d / e2e_s / 1e9}
+
+
+def e2e_step_pipeline(step, batch, keys, dev, n_steps):
+    """End to end through the pipelined TrainStep: batch i+2 goes H2D (copy
+    stream, pinned host) into the slot batch i came in while graph i trains
+    batch i and deduplicates batch i+1 on its side stream; each step's dedup
+    counts come back D2H and are read by the host (one step of lag).  Every
+    batch is copied, deduplicated and trained inside the timed region."""
+    import torch
+
+    from paper_2211_05239_b200.staging import H2DPipeline
+
+    pin_v = {k: torch.from_numpy(batch.values[k]).pin_memory() for k in keys}
+    pin_o = {k: torch.from_numpy(batch.offsets[k]).pin_memory() for k in keys}
+    h2d = sum(pin_v[k].numel() * 8 + pin_o[k].numel() * 8 for k in keys)
+    pipe = H2DPipeline(step, dev)
+    res = [torch.empty(step.counts.numel(), dtype=torch.int64).pin_memory() for _ in range(2)]
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pipe.prefetch(0, pin_v, pin_o)
+    pipe.prefetch(1, pin_v, pin_o)
+    pipe.wait_ready(0)
+    step.prime(0)
+    for i in range(n_steps):
+        p = i % 2
+        pipe.wait_ready(1 - p)      # batch i+1: deduplicated by this graph's side stream
+        pipe.release(p)             # batch i's slot was consumed by the previous graph
+        step.replay(p)
+        if i + 2 <= n_steps:        # batch i+2 into the freed slot, overlapping this graph
+            pipe.prefetch(p, pin_v, pin_o)
+        res[p].copy_(step.counts, non_blocking=True)
+        done[p].record()
+        if i >= 1:
+            done[1 - p].synchronize()
+            _ = int(res[1 - p][0])
+    torch.cuda.synchronize()
+    _ = int(res[(n_steps - 1) % 2][0])
+    e2e_s = (time.perf_counter() - t0) / n_steps
+    return {"value": step.B / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": res[0].numel() * 8, "ms_per_step": e2e_s * 1e3,
+            "h2d_gbs_per_gpu": h2d / e2e_s / 1e9,
+            "how": "public TrainStep(pipeline=True) API: pinned-host KJT -> H2D on a copy stream "
+                   "into the slot the batch two steps back came in (overlaps the step) -> one graph "
+                   "per step parity (batch i's lookup/expand/backward + SGD, batch i+1's dedup + "
+                   "backward prepare on a side stream) -> D2H of the step's dedup counts"}
 
 
 def run_sharded(args, world, rank, local, dev):

@@ -348,6 +348,50 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
     __syncthreads();
     const int64_t covered = s_uo[nr];
     const int64_t qa = max(j0, s_uo[0]), qb = min(j1, covered);
+    // staged rows all of one length L: row of q = (q - s_uo[0]) / L, stepped
+    // incrementally (no per-value search); 4 values per thread per batch
+    const int64_t L0 = nr > 0 ? s_uo[1] - s_uo[0] : 0;
+    bool uni = L0 > 0 && L0 < (1 << 23);
+    for (int t = tid; t < nr; t += 256) uni &= (s_uo[t + 1] - s_uo[t]) == L0;
+    if (__syncthreads_and(uni)) {
+      const uint32_t L = (uint32_t)L0, dj = 256 / L, dr = 256 % L;
+      const int64_t q_first = qa + tid;
+      uint32_t rr = 0, rem = 0;
+      if (q_first < qb) {
+        const uint32_t rel = (uint32_t)(q_first - s_uo[0]);
+        rr = rel / L;
+        rem = rel - rr * L;
+      }
+      for (int64_t qq = q_first; qq < qb; qq += 4 * 256) {
+        int64_t id[4];
+        uint32_t row[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          row[k] = rr;
+          rr += dj;
+          rem += dr;
+          if (rem >= L) {
+            rem -= L;
+            ++rr;
+          }
+          if (qq + k * 256 < qb) id[k] = __ldg(src + qq + k * 256);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t q = qq + k * 256;
+          if (q < qb) {
+            const bool in = (uint64_t)id[k] < rows;
+            if (!in) *p.bad = 1;
+            keys[dst + q] = in ? (uint32_t)id[k] : 0u;
+            vals[dst + q] = ((uint32_t)f << 24) | (uint32_t)(u0 + row[k]);
+          }
+        }
+      }
+      if (covered >= j1) break;
+      __syncthreads();
+      u0 += nr;
+      continue;
+    }
     int r = 0;
     for (int64_t q = qa + tid; q < qb; q += 256) {
       // row of q: short forward walk from the previous value's row (q moved

@@ -152,10 +152,67 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
       if (plen != len) s_mism[j] = 1u;
       s_len[j] = (int32_t)min(len, (int64_t)INT32_MAX);
     }
-    __syncthreads();
     const int64_t vbeg = s_start[0], vend = s_start[n];
     const int64_t tb0 = vbeg & ~(int64_t)(RS_IT - 1);  // 64-byte aligned tiles
     const bool a16 = (reinterpret_cast<uintptr_t>(val) & 15) == 0;
+    // uniform-length chunk (every row of a fixed-length history feature): the
+    // predecessor of value q is value q - L and its row is (q - vbeg) / L, so
+    // no per-value row search; rows whose length differs from the previous
+    // row's are already heads, and compares can only set flags, so the chunk's
+    // first row needs no special case
+    const int64_t L0 = s_start[1] - s_start[0];
+    bool uni = L0 > 0 && L0 < (1 << 23);
+    for (int j = tid; j < n; j += RS_NT) uni &= (int64_t)s_len[j] == L0;
+    if (__syncthreads_and(uni)) {
+      const uint32_t L = (uint32_t)L0;
+      for (int64_t tb = tb0; tb < vend; tb += (int64_t)RS_NT * RS_IT) {
+        const int64_t q0 = tb + (int64_t)tid * RS_IT;
+        if (q0 >= vend || q0 + RS_IT <= vbeg) continue;
+        int64_t v[RS_IT], pv[RS_IT];
+        const int64_t pq0 = q0 - L0;
+        if (q0 + RS_IT <= nv && a16) {
+          const longlong2* src = reinterpret_cast<const longlong2*>(val + q0);
+#pragma unroll
+          for (int k = 0; k < RS_IT / 2; ++k) {
+            const longlong2 t = __ldg(src + k);
+            v[2 * k] = t.x;
+            v[2 * k + 1] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < RS_IT; ++k) v[k] = (q0 + k < nv) ? __ldg(val + q0 + k) : 0;
+        }
+        if (a16 && pq0 >= 0 && (pq0 & 1) == 0) {
+          const longlong2* src = reinterpret_cast<const longlong2*>(val + pq0);
+#pragma unroll
+          for (int k = 0; k < RS_IT / 2; ++k) {
+            const longlong2 t = __ldg(src + k);
+            pv[2 * k] = t.x;
+            pv[2 * k + 1] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < RS_IT; ++k) pv[k] = __ldg(val + max(pq0 + k, (int64_t)0));
+        }
+        // row of q0 relative to the chunk (q0 may precede vbeg by < 8)
+        const int64_t rel0 = q0 - vbeg;
+        uint32_t j = rel0 >= 0 ? (uint32_t)rel0 / L : 0u;
+        uint32_t rem = rel0 >= 0 ? (uint32_t)rel0 - j * L : 0u;
+#pragma unroll
+        for (int k = 0; k < RS_IT; ++k) {
+          const int64_t q = q0 + k;
+          if (q >= vbeg && q < vend) {
+            if (pv[k] != v[k]) s_mism[j] = 1u;
+            if (++rem == L) {
+              rem = 0;
+              ++j;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     for (int64_t tb = tb0; tb < vend; tb += (int64_t)RS_NT * RS_IT) {
       const int64_t q0 = tb + (int64_t)tid * RS_IT;
       if (q0 >= vend || q0 + RS_IT <= vbeg) continue;
@@ -570,6 +627,50 @@ __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupPar
     __syncthreads();
     const int64_t covered = s_uo[nr];  // values before row u0 + nr
     const int64_t qa = max(j0, s_uo[0]), qb = min(j1, covered);
+    // staged rows all of one length L (fixed-length history features): the row
+    // of value q is (q - s_uo[0]) / L, stepped incrementally; loads batched 4
+    // deep so every thread keeps 4 independent gathers in flight
+    const int64_t L0 = nr > 0 ? s_uo[1] - s_uo[0] : 0;
+    bool uni = L0 > 0 && L0 < (1 << 23);
+    for (int t = tid; t < nr; t += CP_NT) uni &= (s_uo[t + 1] - s_uo[t]) == L0;
+    if (__syncthreads_and(uni)) {
+      const uint32_t L = (uint32_t)L0, dj = CP_NT / L, dr = CP_NT % L;
+      const int64_t q_first = qa + tid;
+      uint32_t r = 0, rem = 0;
+      if (q_first < qb) {
+        const uint32_t rel = (uint32_t)(q_first - s_uo[0]);
+        r = rel / L;
+        rem = rel - r * L;
+      }
+      for (int64_t qq = q_first; qq < qb; qq += 4 * CP_NT) {
+        int64_t a[4], v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          a[k] = s_so[min(r, (uint32_t)(nr - 1))] + rem;
+          r += dj;
+          rem += dr;
+          if (rem >= L) {
+            rem -= L;
+            ++r;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (qq + k * CP_NT < qb) v[k] = __ldg(src + a[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t q = qq + k * CP_NT;
+          if (q < qb) {
+            dst[q] = v[k];
+            if (rdst) rdst[q] = v[k];
+          }
+        }
+      }
+      if (covered >= j1) break;
+      __syncthreads();
+      u0 += nr;
+      continue;
+    }
     // values qa + k * CP_NT + tid: coalesced loads and stores; the row of each
     // value by a search over the staged rows, starting from the previous one
     int r = 0;

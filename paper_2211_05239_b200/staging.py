@@ -11,6 +11,10 @@ copied device-to-device: `run(slot, replay)` makes the step wait for the
 slot's copy, replays that slot's graph and releases the slot to the copy
 stream when the step is done with it.  Any batch up to the capacities works.
 
+A pipelined step (`TrainStep(pipeline=True)`) deduplicates batch i+1 on its
+side stream while batch i trains, so the copy of batch i+2 goes into the slot
+batch i came in (`wait_ready` / `release` around each replay).
+
 Steps without slots (the sharded steps, whose graphs are bound to one set of
 input buffers and value counts) get the slot copied into their inputs by
 `install(slot)` (one device-to-device copy per step).
@@ -82,6 +86,19 @@ class H2DPipeline:
             self.install(slot, _record=False)
         replay()
         self.free[slot].record(cur)
+        self._freed[slot] = True
+
+    def wait_ready(self, slot: int) -> None:
+        """The current stream waits for `slot`'s H2D copy (pipelined steps: the
+        side stream of the next graph deduplicates that slot)."""
+        torch.cuda.current_stream(self.dev).wait_event(self.ready[slot])
+        if self.direct:
+            self.step.slot_nvalues[slot] = list(self.counts[slot])
+
+    def release(self, slot: int) -> None:
+        """Everything enqueued so far on the current stream is done with
+        `slot`: the next prefetch into it may start once the stream gets here."""
+        self.free[slot].record(torch.cuda.current_stream(self.dev))
         self._freed[slot] = True
 
     def install(self, slot: int, _record: bool = True) -> None:

@@ -5,15 +5,24 @@ at worst-case size, pooled/expanded outputs, gradients, scratch) and the
 ctypes argument arrays, so a step is four C-ABI calls with no allocation and
 no host synchronisation -- capturable as one CUDA graph:
 
-    recd_dedup       KJT -> IKJT for every group              (skipped in "kjt" mode)
+    recd_dedup_ex    KJT -> IKJT for every group              (skipped in "kjt" mode)
     recd_pool_fwd    pooled lookup over unique rows
     recd_expand      expansion of the pooled rows to [B, D] via inverse_lookup
     recd_pool_bwd    grad segment-reduce + sorted scatter-add + fused SGD
 
 With overlap=True (default) the backward is split: recd_pool_bwd_prepare
 (inverse CSR + occurrence sort, gradient-independent) runs on a side stream
-right after recd_dedup, concurrently with the pooled lookup and expansion,
+right after the dedup, concurrently with the pooled lookup and expansion,
 and recd_pool_bwd_finish joins on the main stream.
+
+pipeline=True goes one step further, the way the reference splits its reader
+from its trainer (reader.convert builds the IKJTs of the next batch while
+the trainer runs, reader.py:160-175): the IKJT-only half of batch i+1 -- the
+dedup and the backward's prepare half -- runs on the side stream while the
+main stream runs batch i's pooled lookup, expansion and backward + SGD.
+Nothing of batch i+1 touches the tables, so every batch's results are
+bit-identical to the sequential step; two IKJT stages alternate (stage =
+slot = step parity) and each parity is one captured CUDA graph.
 
 This is the device-side equivalent of one `forward_iteration`'s sparse part
 (trainer_sim.py:484-574) plus the backward the reference does not have.
@@ -40,6 +49,56 @@ class StepCounts:
     N_u: list[int]    # unique values per feature
 
 
+class _Stage:
+    """One set of IKJT outputs + the scratch of the dedup and the backward
+    (the prepare half writes the backward scratch, the finish half reads it)."""
+
+    def __init__(self, step: "TrainStep"):
+        dev, B, F, i64 = step.dev, step.B, step.F, torch.int64
+        lib = step.lib
+        self.inverse = [torch.empty(B, dtype=i64, device=dev) for _ in step.groups]
+        self.uoffsets = [torch.empty(B, dtype=i64, device=dev) for _ in step.keys]
+        self.uvalues = [torch.empty(c, dtype=i64, device=dev) for c in step.caps]
+        self.dcounts = torch.zeros(2 * F, dtype=i64, device=dev)
+        self.err = torch.full((2,), _lib.RECD_NO_ERROR, dtype=i64, device=dev)
+        self.dedup_scratch = torch.empty(
+            max(lib.recd_dedup_scratch_bytes(len(step.groups), F, B), 256), dtype=torch.uint8,
+            device=dev)
+        self.bwd_scratch = torch.empty(
+            max(lib.recd_pool_bwd_scratch_bytes(F, B, step.D, _lib.i64s(step.caps)), 256),
+            dtype=torch.uint8, device=dev)
+
+
+class _Args:
+    """ctypes argument arrays of one (stage, input slot) pair."""
+
+    def __init__(self, step: "TrainStep", stage: int, slot: int):
+        L, st = _lib, step.stages[stage]
+        vals, offs = step.slot_values[slot], step.slot_offsets[slot]
+        self.gsizes = L.i32s([len(g) for g in step.groups])
+        self.in_values, self.in_offsets = L.ptrs(vals), L.ptrs(offs)
+        self.in_counts_ptr = step.in_counts[slot, step.F:].data_ptr()
+        self.inverse_g = L.ptrs(st.inverse)
+        self.uoffsets, self.uvalues = L.ptrs(st.uoffsets), L.ptrs(st.uvalues)
+        self.tables = L.ptrs([t.weights for t in step.tables])
+        self.rows = L.i64s([t.rows for t in step.tables])
+        self.caps = L.i64s(step.caps)
+        self.grad, self.out = L.ptrs(step.grad_out), L.ptrs(step.out)
+        if step.mode == "dedup":
+            inv_f = []
+            for gi, g in enumerate(step.groups):
+                inv_f += [st.inverse[gi]] * len(g)
+            self.inverse_f = L.ptrs(inv_f)
+            self.pooled = L.ptrs(step.pooled)
+            self.feat_vals, self.feat_offs, self.feat_vals_t = self.uvalues, self.uoffsets, st.uvalues
+            self.counts_ptr = st.dcounts.data_ptr()
+        else:
+            self.inverse_f = L.ptrs([None] * step.F)
+            self.pooled = self.out  # no expansion: pooled rows are the batch rows
+            self.feat_vals, self.feat_offs, self.feat_vals_t = self.in_values, self.in_offsets, vals
+            self.counts_ptr = step.in_counts[slot].data_ptr()
+
+
 class TrainStep:
     """One training step over `slots` input slots (each slot: the KJT values,
     offsets and value counts of one batch, all on the device).  With slots=2 a
@@ -51,9 +110,11 @@ class TrainStep:
     def __init__(self, groups: Sequence[Sequence[str]], batch_size: int,
                  value_caps: dict[str, int], tables: dict[str, EmbeddingTable], op: str = "sum",
                  lr: float = 0.01, mode: str = "dedup", device=None, overlap: bool = True,
-                 slots: int = 1):
+                 slots: int = 1, pipeline: bool = False):
         if mode not in ("dedup", "kjt"):
             raise ValueError(f"unknown mode {mode!r}")
+        if op not in ("sum", "avg", "mean"):
+            raise ValueError(f"the training step needs sum/avg pooling (max has no backward), got {op!r}")
         self.lib = _lib.load()
         self.groups = [tuple(g) for g in groups]
         self.keys = [k for g in self.groups for k in g]
@@ -61,11 +122,10 @@ class TrainStep:
         self.B = int(batch_size)
         self.mode = mode
         self.op = op
-        if op not in ("sum", "avg", "mean"):
-            raise ValueError(f"the training step needs sum/avg pooling (max has no backward), got {op!r}")
         self.mode_id = _lib.POOL_MODES[op]
         self.lr = float(lr)
         self.overlap = bool(overlap)
+        self.pipeline = bool(pipeline)
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         self.tables = [tables[k] for k in self.keys]
         self.D = self.tables[0].dim
@@ -73,7 +133,7 @@ class TrainStep:
         i64 = torch.int64
         self.caps = [max(int(value_caps[k]), 1) for k in self.keys]
         # KJT input slots: values, offsets, value counts (device)
-        self.nslots = max(1, int(slots))
+        self.nslots = 2 if self.pipeline else max(1, int(slots))
         self.slot_values = [[torch.zeros(c, dtype=i64, device=dev) for c in self.caps]
                             for _ in range(self.nslots)]
         self.slot_offsets = [[torch.zeros(B, dtype=i64, device=dev) for _ in self.keys]
@@ -84,25 +144,29 @@ class TrainStep:
         self.in_counts[:, :F] = B
         self.slot_nvalues = [[0] * F for _ in range(self.nslots)]
         self.slot = 0
-        # IKJT outputs (worst case) + device counts
-        self.inverse = [torch.empty(B, dtype=i64, device=dev) for _ in self.groups]
-        self.uoffsets = [torch.empty(B, dtype=i64, device=dev) for _ in self.keys]
-        self.uvalues = [torch.empty(c, dtype=i64, device=dev) for c in self.caps]
-        self._dcounts = torch.zeros(2 * F, dtype=i64, device=dev)
         self.pooled = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
         self.out = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
         self.grad_out = [torch.empty((B, D), dtype=torch.float32, device=dev) for _ in self.keys]
-        self.err = torch.empty(2, dtype=i64, device=dev)  # [first bad ID, work counter]
-        self.dedup_scratch = torch.empty(
-            max(self.lib.recd_dedup_scratch_bytes(len(self.groups), F, B), 256),
-            dtype=torch.uint8, device=dev)
-        self.bwd_scratch = torch.empty(
-            max(self.lib.recd_pool_bwd_scratch_bytes(F, B, D, _lib.i64s(self.caps)), 256),
-            dtype=torch.uint8, device=dev)
+        # IKJT stages (two alternate in pipeline mode)
+        self.stages = [_Stage(self) for _ in range(2 if self.pipeline else 1)]
+        self.stage = 0
+        self._args: dict = {}
         self.graphs: list = [None] * self.nslots
-        self._build_args()
+        self._side = torch.cuda.Stream(dev)
+        self._ev_fork = torch.cuda.Event()
+        self._ev_join = torch.cuda.Event()
 
-    # current slot's buffers (the step's inputs)
+    # ------------------------------------------- current stage / slot views
+    def _st(self, stage=None) -> _Stage:
+        return self.stages[self.stage if stage is None else stage]
+
+    def args(self, stage=None, slot=None) -> _Args:
+        key = (self.stage if stage is None else stage, self.slot if slot is None else slot)
+        a = self._args.get(key)
+        if a is None:
+            a = self._args[key] = _Args(self, *key)
+        return a
+
     @property
     def in_values(self):
         return self.slot_values[self.slot]
@@ -116,10 +180,26 @@ class TrainStep:
         return self.slot_nvalues[self.slot]
 
     @property
+    def inverse(self):
+        return self._st().inverse
+
+    @property
+    def uoffsets(self):
+        return self._st().uoffsets
+
+    @property
+    def uvalues(self):
+        return self._st().uvalues
+
+    @property
+    def err(self):
+        return self._st().err
+
+    @property
     def counts(self):
         """Device int64[2F] (U per feature, N_u per feature) of the step's IKJT
         (kjt mode: B and the slot's value counts)."""
-        return self._dcounts if self.mode == "dedup" else self.in_counts[self.slot]
+        return self._st().dcounts if self.mode == "dedup" else self.in_counts[self.slot]
 
     @property
     def graph(self):
@@ -145,12 +225,13 @@ class TrainStep:
                                           non_blocking=non_blocking)
         self.slot_nvalues[s] = n
 
-    def use_slot(self, slot: int) -> None:
-        """Make `slot` the step's input (eager calls and replay() use it)."""
+    def use_slot(self, slot: int, stage: int | None = None) -> None:
+        """Make `slot` (and `stage`) the step's current input / IKJT."""
         if not 0 <= slot < self.nslots:
             raise ValueError(f"slot {slot} out of range for {self.nslots} slots")
         self.slot = int(slot)
-        self._build_args()
+        if stage is not None:
+            self.stage = int(stage)
 
     def fill_grad_out(self, seed: int = 1) -> None:
         g = torch.Generator(device=self.dev)
@@ -158,81 +239,54 @@ class TrainStep:
         for t in self.grad_out:
             t.normal_(generator=g)
 
-    # ---------------------------------------------------------------- args
-    def _build_args(self) -> None:
-        L = _lib
-        self.a_gsizes = L.i32s([len(g) for g in self.groups])
-        self.a_in_values = L.ptrs(self.in_values)
-        self.a_in_offsets = L.ptrs(self.in_offsets)
-        self.in_counts_ptr = self.in_counts[self.slot, self.F:].data_ptr()
-        self.a_inverse_g = L.ptrs(self.inverse)
-        self.a_uoffsets = L.ptrs(self.uoffsets)
-        self.a_uvalues = L.ptrs(self.uvalues)
-        self.a_tables = L.ptrs([t.weights for t in self.tables])
-        self.a_rows = L.i64s([t.rows for t in self.tables])
-        self.a_caps = L.i64s(self.caps)
-        self.a_grad = L.ptrs(self.grad_out)
-        self.a_out = L.ptrs(self.out)
-        if self.mode == "dedup":
-            inv_f = []
-            for gi, g in enumerate(self.groups):
-                inv_f += [self.inverse[gi]] * len(g)
-            self.a_inverse_f = L.ptrs(inv_f)
-            self.a_pooled = L.ptrs(self.pooled)
-            self.a_feat_vals, self.a_feat_offs = self.a_uvalues, self.a_uoffsets
-            self.a_feat_vals_t = self.uvalues
-        else:
-            self.a_inverse_f = L.ptrs([None] * self.F)
-            self.a_pooled = L.ptrs(self.out)  # no expansion: pooled rows are the batch rows
-            self.a_feat_vals, self.a_feat_offs = self.a_in_values, self.a_in_offsets
-            self.a_feat_vals_t = self.in_values
-
     # ---------------------------------------------------------------- step
-    def dedup(self, stream: int) -> None:
+    def dedup(self, stream: int, stage=None, slot=None) -> None:
         if self.mode != "dedup":
             return
-        rc = self.lib.recd_dedup_ex(len(self.groups), self.a_gsizes, self.B, self.a_in_values,
-                                    self.a_in_offsets, self.a_caps, self.in_counts_ptr, 3,
-                                    self.a_inverse_g, self.a_uoffsets, self.a_uvalues,
-                                    self.counts.data_ptr(), None, None,
-                                    self.dedup_scratch.data_ptr(), self.dedup_scratch.numel(),
-                                    stream)
+        a, st = self.args(stage, slot), self._st(stage)
+        rc = self.lib.recd_dedup_ex(len(self.groups), a.gsizes, self.B, a.in_values, a.in_offsets,
+                                    a.caps, a.in_counts_ptr, 3, a.inverse_g, a.uoffsets,
+                                    a.uvalues, st.dcounts.data_ptr(), None, None,
+                                    st.dedup_scratch.data_ptr(), st.dedup_scratch.numel(), stream)
         _lib.check(rc, "recd_dedup_ex")
 
-    def forward(self, stream: int) -> None:
+    def forward(self, stream: int, stage=None, slot=None) -> None:
         """Pooled lookup over the unique rows (k_pool_fwd only)."""
-        rc = self.lib.recd_pool_fwd(self.F, self.B, self.D, self.mode_id, self.a_tables,
-                                    self.a_rows, self.a_feat_vals, self.a_feat_offs,
-                                    self.counts.data_ptr(), self.a_inverse_f, self.a_pooled,
-                                    None, self.err.data_ptr(), stream)
+        a, st = self.args(stage, slot), self._st(stage)
+        rc = self.lib.recd_pool_fwd(self.F, self.B, self.D, self.mode_id, a.tables, a.rows,
+                                    a.feat_vals, a.feat_offs, a.counts_ptr, a.inverse_f, a.pooled,
+                                    None, st.err.data_ptr(), stream)
         _lib.check(rc, "recd_pool_fwd")
 
-    def expand(self, stream: int) -> None:
+    def expand(self, stream: int, stage=None, slot=None) -> None:
         """out[i] = pooled[inverse[i]] (k_expand; nothing to do in kjt mode)."""
         if self.mode != "dedup":
             return
-        rc = self.lib.recd_expand(self.F, self.B, self.D, self.a_inverse_f, self.a_pooled,
-                                  self.a_out, stream)
+        a = self.args(stage, slot)
+        rc = self.lib.recd_expand(self.F, self.B, self.D, a.inverse_f, a.pooled, a.out, stream)
         _lib.check(rc, "recd_expand")
 
-    def _bwd_args(self, stream: int):
-        inv = self.a_inverse_f if self.mode == "dedup" else None
-        return (self.F, self.B, self.D, self.mode_id, self.a_tables, self.a_rows, self.a_feat_vals,
-                self.a_feat_offs, self.a_caps, self.counts.data_ptr(), inv, self.a_grad,
-                C.c_float(self.lr), 1, None, None, None, self.bwd_scratch.data_ptr(),
-                self.bwd_scratch.numel(), stream)
+    def _bwd_args(self, stream: int, stage=None, slot=None):
+        a, st = self.args(stage, slot), self._st(stage)
+        inv = a.inverse_f if self.mode == "dedup" else None
+        return (self.F, self.B, self.D, self.mode_id, a.tables, a.rows, a.feat_vals, a.feat_offs,
+                a.caps, a.counts_ptr, inv, a.grad, C.c_float(self.lr), 1, None, None, None,
+                st.bwd_scratch.data_ptr(), st.bwd_scratch.numel(), stream)
 
-    def backward(self, stream: int) -> None:
-        _lib.check(self.lib.recd_pool_bwd(*self._bwd_args(stream)), "recd_pool_bwd")
+    def backward(self, stream: int, stage=None, slot=None) -> None:
+        _lib.check(self.lib.recd_pool_bwd(*self._bwd_args(stream, stage, slot)), "recd_pool_bwd")
 
-    def backward_prepare(self, stream: int) -> None:
+    def backward_prepare(self, stream: int, stage=None, slot=None) -> None:
         """Gradient-independent half of the backward (may run on a side stream)."""
-        _lib.check(self.lib.recd_pool_bwd_prepare(*self._bwd_args(stream)), "recd_pool_bwd_prepare")
+        _lib.check(self.lib.recd_pool_bwd_prepare(*self._bwd_args(stream, stage, slot)),
+                   "recd_pool_bwd_prepare")
 
-    def backward_finish(self, stream: int) -> None:
-        _lib.check(self.lib.recd_pool_bwd_finish(*self._bwd_args(stream)), "recd_pool_bwd_finish")
+    def backward_finish(self, stream: int, stage=None, slot=None) -> None:
+        _lib.check(self.lib.recd_pool_bwd_finish(*self._bwd_args(stream, stage, slot)),
+                   "recd_pool_bwd_finish")
 
     def run(self, stream: int | None = None) -> None:
+        """One whole step on the current slot / stage (dedup .. SGD)."""
         if stream is not None or not self.overlap:
             s = _lib.stream_ptr(self.dev) if stream is None else stream
             self.dedup(s)
@@ -241,10 +295,6 @@ class TrainStep:
             self.backward(s)
             return
         main = torch.cuda.current_stream(self.dev)
-        if not hasattr(self, "_side"):
-            self._side = torch.cuda.Stream(self.dev)
-            self._ev_fork = torch.cuda.Event()
-            self._ev_join = torch.cuda.Event()
         self.dedup(main.cuda_stream)
         self._ev_fork.record(main)
         self._side.wait_event(self._ev_fork)
@@ -255,29 +305,70 @@ class TrainStep:
         main.wait_event(self._ev_join)
         self.backward_finish(main.cuda_stream)
 
+    # ------------------------------------------------------ pipeline mode
+    def prime(self, slot: int = 0) -> None:
+        """Pipeline start: dedup + backward prepare of the batch in `slot` into
+        stage `slot`, on the current stream."""
+        s = torch.cuda.current_stream(self.dev).cuda_stream
+        self.dedup(s, slot, slot)
+        self.backward_prepare(s, slot, slot)
+
+    def run_pipelined(self, p: int) -> None:
+        """Step on the batch in slot p (primed into stage p) -- pooled lookup,
+        expansion, backward + SGD on the main stream -- while the side stream
+        deduplicates the batch in slot 1-p and prepares its backward into
+        stage 1-p (the next step's IKJT)."""
+        if not self.pipeline:
+            raise ValueError("run_pipelined needs TrainStep(pipeline=True)")
+        q = 1 - p
+        main = torch.cuda.current_stream(self.dev)
+        self._ev_fork.record(main)
+        self._side.wait_event(self._ev_fork)
+        ss = self._side.cuda_stream
+        self.dedup(ss, q, q)
+        self.backward_prepare(ss, q, q)
+        self._ev_join.record(self._side)
+        ms = main.cuda_stream
+        self.forward(ms, p, p)
+        self.expand(ms, p, p)
+        self.backward_finish(ms, p, p)
+        main.wait_event(self._ev_join)
+        self.use_slot(p, p)
+
     def capture(self) -> None:
-        """Record run() into one CUDA graph per input slot (replay() launches
-        the current slot's).  Runs one eager warm-up step on the current slot."""
-        cur = self.slot
+        """Record one CUDA graph per input slot (replay(slot) launches it):
+        run() on that slot, or run_pipelined(slot) in pipeline mode.  Runs one
+        eager warm-up step first (on the current slot)."""
+        cur, cur_stage = self.slot, self.stage
         s = torch.cuda.Stream(self.dev)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
-            self.run()  # warm-up on the side stream
+            if self.pipeline:
+                self.prime(cur)
+                self.run_pipelined(cur)
+            else:
+                self.run()  # warm-up on the side stream
         torch.cuda.current_stream(self.dev).wait_stream(s)
         for k in range(self.nslots):
-            self.use_slot(k)
+            self.use_slot(k, k if self.pipeline else cur_stage)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self.run()
+                if self.pipeline:
+                    self.run_pipelined(k)
+                else:
+                    self.run()
             self.graphs[k] = g
-        self.use_slot(cur)
+        self.use_slot(cur, cur_stage)
 
     def replay(self, slot: int | None = None) -> None:
         if slot is not None and slot != self.slot:
-            self.use_slot(slot)
+            self.use_slot(slot, slot if self.pipeline else None)
         g = self.graphs[self.slot]
         if g is None:
-            self.run()
+            if self.pipeline:
+                self.run_pipelined(self.slot)
+            else:
+                self.run()
         else:
             g.replay()
 
@@ -290,7 +381,7 @@ class TrainStep:
         if e == _lib.RECD_NO_ERROR:
             return
         f, pos = e >> 40, e & ((1 << 40) - 1)
-        vals = self.a_feat_vals_t[f]
+        vals = self.args().feat_vals_t[f]
         raise ValueError(f"feature {self.keys[f]!r}: ID {int(vals[pos])} at position {pos} "
                          f"out of range [0, {self.tables[f].rows})")
 

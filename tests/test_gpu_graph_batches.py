@@ -76,3 +76,59 @@ def test_one_graph_twenty_batches(mode):
             w[k][ids] = w[k][ids] - (np.float32(lr) * g).astype(np.float32)
             np.testing.assert_array_equal(tables[k].weights.cpu().numpy(), w[k],
                                           err_msg=f"batch {i} {k}")
+
+
+@pytest.mark.parametrize("mode", ["dedup", "kjt"])
+def test_pipelined_step_matches_oracle(mode):
+    """TrainStep(pipeline=True): graph i trains batch i while its side stream
+    deduplicates batch i+1 (and sorts its occurrences); batches arrive through
+    the H2D pipeline.  Every batch's outputs and table updates stay bit-exact
+    against the sequential oracle."""
+    b, vocab, dim, lr, n = 1024, 4000, 32, 0.05, 12
+    batches = _batches(n + 1, b)
+    keys = [s.key for s in SPECS]
+    caps = {k: max(x.values[k].size for x in batches) for k in keys}
+    rng = np.random.default_rng(1)
+    w = {k: rng.uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32) for k in keys}
+    tables = {k: R.EmbeddingTable(k, vocab, dim, torch.as_tensor(w[k], device="cuda").clone())
+              for k in keys}
+    grads = {k: rng.standard_normal((b, dim)).astype(np.float32) for k in keys}
+    step = TrainStep([[k] for k in keys], b, caps, tables, "sum", lr, mode, pipeline=True)
+    for f, k in enumerate(keys):
+        step.grad_out[f].copy_(torch.as_tensor(grads[k]))
+    for s in range(2):
+        step.load_batch(batches[0].values, batches[0].offsets, slot=s)
+    step.capture()
+    torch.cuda.synchronize()
+    for k in keys:
+        tables[k].weights.copy_(torch.as_tensor(w[k]))
+    pipe = H2DPipeline(step)
+    pin = [({k: torch.from_numpy(x.values[k]).pin_memory() for k in keys},
+            {k: torch.from_numpy(x.offsets[k]).pin_memory() for k in keys}) for x in batches]
+    pipe.prefetch(0, *pin[0])
+    pipe.prefetch(1, *pin[1])
+    pipe.wait_ready(0)
+    step.prime(0)
+    for i in range(n):
+        p = i % 2
+        pipe.wait_ready(1 - p)
+        pipe.release(p)
+        step.replay(p)
+        if i + 2 <= n:
+            pipe.prefetch(p, *pin[i + 2])
+        torch.cuda.synchronize()
+        step.check()
+        x = batches[i]
+        for f, k in enumerate(keys):
+            v, o = x.values[k], x.offsets[k]
+            if mode == "dedup":
+                inv, [(uv, uo)] = oracle.build_ikjt_arrays([(v, o)])
+            else:
+                inv, uv, uo = np.arange(b), v, o
+            ref = oracle.expand(oracle.pooled_lookup(uv, uo, w[k], "sum"), inv)
+            np.testing.assert_array_equal(step.out[f].cpu().numpy(), ref, err_msg=f"batch {i} {k}")
+            gu = oracle.pool_backward(grads[k], inv, uo.size)
+            ids, g = oracle.sparse_table_grad(gu, uv, uo, "sum")
+            w[k][ids] = w[k][ids] - (np.float32(lr) * g).astype(np.float32)
+            np.testing.assert_array_equal(tables[k].weights.cpu().numpy(), w[k],
+                                          err_msg=f"batch {i} {k}")
