@@ -457,6 +457,9 @@ __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t
 #define RECD_SC_RS 6
 #endif
 constexpr int SC_RS = RECD_SC_RS;  // table rows prefetched ahead per warp (shared-memory ring)
+#ifndef RECD_SC_PIPE
+#define RECD_SC_PIPE 0
+#endif
 #ifndef RECD_SC_BATCH
 #define RECD_SC_BATCH 6
 #endif
@@ -551,6 +554,87 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
     int32_t bnd = (nruns > 1) ? (int32_t)starts[1] : pe;  // end of run r
     float acc[V];
     C::zero(acc);
+#if RECD_SC_PIPE
+    // software-pipelined: the gradient rows of the next SC_BATCH positions are
+    // in flight while the current SC_BATCH are reduced (the gathers, not the
+    // table RMW, are what the warps wait on -- ncu source view)
+    float xa[SC_BATCH][V], xb[SC_BATCH][V];
+    auto load_batch = [&](float (&x)[SC_BATCH][V], int32_t k) {
+      if (k + SC_BATCH > wbase + 32) {
+        __syncwarp();
+        wbase = k;
+        win[lane] = (k + lane < pe) ? __ldg(Vl + k + lane) : 0u;
+        __syncwarp();
+      }
+#pragma unroll
+      for (int t = 0; t < SC_BATCH; ++t) {
+        if (k + t < pe) {
+          const uint32_t vv = win[k + t - wbase];
+          const float* gp = SINGLE ? gs + (uint64_t)(vv & 0xffffffu) * D32
+                                   : p.grow[vv >> 24] + lo_f + (uint64_t)(vv & 0xffffffu) * D32;
+          if constexpr (HINT && RECD_SCATTER_L2 >= 2) {
+            if (C::FULL || ok) {
+              const float4 q = ld_v4_hint(gp, pol_keep);
+              x[t][0] = q.x; x[t][1] = q.y; x[t][2] = q.z; x[t][3] = q.w;
+            } else {
+              C::zero(x[t]);
+            }
+          } else {
+            C::ld(gp, ok, x[t]);
+          }
+        }
+      }
+    };
+    auto consume = [&](float (&x)[SC_BATCH][V], int32_t k0) {
+#pragma unroll
+      for (int t = 0; t < SC_BATCH; ++t) {
+        if (k0 + t < pe) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[e] = __fadd_rn(acc[e], x[t][e]);
+          if (k0 + t + 1 == bnd) {  // run r complete (warp-uniform)
+            const uint32_t id = rids[r];
+            if (apply) {
+              cp_async_wait<SC_RS - 1>();
+              float* slot = ring + (r % SC_RS) * C::CB;
+              float wv[V];
+#pragma unroll
+              for (int e = 0; e < V; ++e) wv[e] = __fsub_rn(slot[e], __fmul_rn(p.lr, acc[e]));
+              if constexpr (HINT) {
+                if (C::FULL || ok)
+                  st_v4_hint(table + (uint64_t)id * D32, wv[0], wv[1], wv[2], wv[3], pol_stream);
+                if (r + SC_RS < nruns && ok)
+                  cp_async16_hint(slot, table + (uint64_t)rids[r + SC_RS] * D32, pol_stream);
+              } else {
+                C::st(table + (uint64_t)id * D32, ok, wv);
+                if (r + SC_RS < nruns && ok)
+                  cp_async<V * 4>(slot, table + (uint64_t)rids[r + SC_RS] * D32);
+              }
+              cp_async_commit();
+            } else {
+              const int64_t ri = run_base + r;
+              if (lo_f == 0) p.grad_ids[s][ri] = (int64_t)id;
+              C::st(p.grad_rows[s] + ri * p.D + lo_f, ok, acc);
+            }
+            ++r;
+            C::zero(acc);
+            bnd = (r + 1 < nruns) ? (int32_t)starts[r + 1] : pe;
+          }
+        }
+      }
+    };
+    int32_t kl = starts[0];
+    load_batch(xa, kl);
+    kl += SC_BATCH;
+    for (int32_t k0 = starts[0]; k0 < pe; k0 += 2 * SC_BATCH) {
+      load_batch(xb, kl);
+      kl += SC_BATCH;
+      consume(xa, k0);
+      if (k0 + SC_BATCH >= pe) break;
+      load_batch(xa, kl);
+      kl += SC_BATCH;
+      consume(xb, k0 + SC_BATCH);
+    }
+#else
     float x[SC_BATCH][V];
     for (int32_t k0 = starts[0]; k0 < pe; k0 += SC_BATCH) {
       if (k0 + SC_BATCH > wbase + 32) {
@@ -613,6 +697,7 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
         }
       }
     }
+#endif
     if (apply) cp_async_wait<0>();
     __syncwarp();
   }

@@ -14,6 +14,10 @@ V = {
     "gcs": ["RECD_GUF_CS=1"],
     "xrf16": ["RECD_EXPAND_RF=16"],
     "xrf4": ["RECD_EXPAND_RF=4"],
+    "sp4m4": ["RECD_SC_PIPE=1", "RECD_SC_BATCH=4", "RECD_SCATTER_MINB=4"],
+    "sp4m3": ["RECD_SC_PIPE=1", "RECD_SC_BATCH=4", "RECD_SCATTER_MINB=3"],
+    "sp6m3": ["RECD_SC_PIPE=1", "RECD_SC_BATCH=6", "RECD_SCATTER_MINB=3"],
+    "sp3m4": ["RECD_SC_PIPE=1", "RECD_SC_BATCH=3", "RECD_SCATTER_MINB=4"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
