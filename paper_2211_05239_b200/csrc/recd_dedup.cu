@@ -589,7 +589,10 @@ __global__ void __launch_bounds__(256) k_num_inv(const __grid_constant__ DedupPa
 // spans in shared memory with one independent load chain per row, then the
 // block copies the values with consecutive threads on consecutive values.
 constexpr int CP_NT = 256;
-constexpr int CP_IT = 16;
+#ifndef RECD_CP_IT
+#define RECD_CP_IT 16
+#endif
+constexpr int CP_IT = RECD_CP_IT;
 constexpr int CP_CH = CP_NT * CP_IT;  // unique values per block
 constexpr int CP_MAXR = 512;          // rows staged per pass
 
