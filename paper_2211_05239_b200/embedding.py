@@ -32,6 +32,7 @@ __all__ = [
     "pooled_lookup_backward",
     "DedupEmbeddingBagCollection",
     "ELEMENT_POOLING",
+    "raise_lookup_error",
 ]
 
 ELEMENT_POOLING = ("sum", "avg", "max")  # trainer_sim.py:58
@@ -126,10 +127,16 @@ def _counts_tensor(features: Sequence[JaggedTensor], dev) -> torch.Tensor:
 def pooled_lookup(features: Sequence[JaggedTensor], tables: Sequence[EmbeddingTable], op: str,
                   inverses: Sequence[torch.Tensor | None] | None = None,
                   batch_size: int | None = None, keys: Sequence[str] | None = None,
-                  counts: torch.Tensor | None = None) -> list[torch.Tensor]:
+                  counts: torch.Tensor | None = None, err: torch.Tensor | None = None
+                  ) -> list[torch.Tensor]:
     """For each feature f: pool(embedding_lookup(features[f], tables[f]))
     expanded by inverses[f] (None = the rows are the batch rows).  Returns
-    one [B, D] tensor per feature.  One fused launch pair for all features."""
+    one [B, D] tensor per feature.  One fused launch pair for all features.
+
+    The out-of-range check reads one device word back (a host sync).  Pass
+    an `err` tensor (int64[2], device) to defer it: nothing is read, the call
+    is capturable in a CUDA graph, and `raise_lookup_error(err, ...)` raises
+    the reference's ValueError later."""
     if op not in ELEMENT_POOLING:
         raise ValueError(f"unknown pooling op {op!r}")
     lib = _lib.load()
@@ -153,7 +160,9 @@ def pooled_lookup(features: Sequence[JaggedTensor], tables: Sequence[EmbeddingTa
             pooled.append(torch.empty((max(features[f].row_count, 1), D), dtype=torch.float32,
                                       device=dev))
             outs.append(torch.empty((B, D), dtype=torch.float32, device=dev))
-    err = torch.empty(2, dtype=torch.int64, device=dev)  # [first bad ID, work counter]
+    deferred = err is not None
+    if not deferred:
+        err = torch.empty(2, dtype=torch.int64, device=dev)  # [first bad ID, work counter]
     rc = lib.recd_pool_fwd(F, B, D, _lib.POOL_MODES[op], _lib.ptrs([t.weights for t in tables]),
                            _lib.i64s([t.rows for t in tables]),
                            _lib.ptrs([f.values for f in features]),
@@ -161,13 +170,21 @@ def pooled_lookup(features: Sequence[JaggedTensor], tables: Sequence[EmbeddingTa
                            _lib.ptrs(inverses), _lib.ptrs(pooled), _lib.ptrs(outs),
                            err.data_ptr(), _lib.stream_ptr(dev))
     _lib.check(rc, "recd_pool_fwd")
+    if not deferred:
+        raise_lookup_error(err, features, tables, keys)
+    return outs
+
+
+def raise_lookup_error(err: torch.Tensor, features: Sequence[JaggedTensor],
+                       tables: Sequence[EmbeddingTable], keys: Sequence[str] | None = None) -> None:
+    """Raise the reference's ValueError (trainer_sim.py:312-320) if the lookup
+    that wrote `err` saw an ID outside [0, rows) (one host read)."""
     e = int(err[0].item())
     if e != _lib.RECD_NO_ERROR:
         f, p = e >> 40, e & ((1 << 40) - 1)
         key = keys[f] if keys else tables[f].key
         raise ValueError(f"feature {key!r}: ID {int(features[f].values[p])} at position {p} "
                          f"out of range [0, {tables[f].rows})")
-    return outs
 
 
 def pooled_lookup_backward(features: Sequence[JaggedTensor], tables: Sequence[EmbeddingTable],
@@ -229,8 +246,8 @@ class _PooledFn(torch.autograd.Function):
     forwards may be in flight before their backwards run."""
 
     @staticmethod
-    def forward(ctx, anchor, lr, tables, features, inverses, counts, op, B, sink):
-        outs = pooled_lookup(features, tables, op, inverses, B, counts=counts)
+    def forward(ctx, anchor, lr, tables, features, inverses, counts, op, B, sink, err):
+        outs = pooled_lookup(features, tables, op, inverses, B, counts=counts, err=err)
         ctx.lr, ctx.tables, ctx.features, ctx.inverses, ctx.counts, ctx.op, ctx.B, ctx.sink = (
             lr, tables, features, inverses, counts, op, B, sink)
         return tuple(outs)
@@ -245,7 +262,7 @@ class _PooledFn(torch.autograd.Function):
                                      counts=ctx.counts)
         if res is not None:
             ctx.sink.extend(res)
-        return (None,) * 9
+        return (None,) * 10
 
 
 class DedupEmbeddingBagCollection(torch.nn.Module):
@@ -262,7 +279,7 @@ class DedupEmbeddingBagCollection(torch.nn.Module):
     """
 
     def __init__(self, tables: Mapping[str, EmbeddingTable], pooling: Mapping[str, str] | str = "sum",
-                 lr: float | None = None):
+                 lr: float | None = None, defer_checks: bool = False):
         super().__init__()
         self.tables = dict(tables)
         dims = {t.dim for t in self.tables.values()}
@@ -282,6 +299,9 @@ class DedupEmbeddingBagCollection(torch.nn.Module):
         self.lr = lr
         self.sparse_grads: list = []
         self._anchor = torch.nn.Parameter(torch.zeros(0))
+        # defer_checks: forward never reads the device (capturable); check() raises
+        self.defer_checks = bool(defer_checks)
+        self._pending: list = []   # (err, features, tables, keys) of deferred lookups
 
     def forward(self, ikjts: Sequence[IKJT] = (), kjt: KJT | None = None) -> dict[str, torch.Tensor]:
         if isinstance(ikjts, IKJT):
@@ -309,11 +329,23 @@ class DedupEmbeddingBagCollection(torch.nn.Module):
             tables = [self.tables[j[0]] for j in js]
             counts = _counts_tensor(feats, feats[0].device)
             invs = [j[2] for j in js]
+            err = None
+            if self.defer_checks:
+                err = torch.empty(2, dtype=torch.int64, device=feats[0].device)
+                self._pending.append((err, feats, tables, [j[0] for j in js]))
             if op == "max":   # forward-only (no backward exists for max): no autograd node
-                res = pooled_lookup(feats, tables, op, invs, B, counts=counts)
+                res = pooled_lookup(feats, tables, op, invs, B, counts=counts, err=err)
             else:
                 res = _PooledFn.apply(self._anchor, self.lr, tables, feats, invs, counts, op, B,
-                                      self.sparse_grads)
+                                      self.sparse_grads, err)
             for j, r in zip(js, res):
                 out[j[0]] = r
         return out
+
+    def check(self) -> None:
+        """Raise the first deferred lookup error (defer_checks=True), in call
+        order, and forget the checked lookups.  The fused SGD of a batch with
+        an out-of-range ID updates nothing (the backward skips it)."""
+        pending, self._pending = self._pending, []
+        for err, feats, tables, keys in pending:
+            raise_lookup_error(err, feats, tables, keys)

@@ -132,3 +132,26 @@ def test_out_of_range_id_reports_and_leaves_tables_intact(bad, graph):
     torch.cuda.synchronize()
     step.check()
     assert not np.array_equal(tables[keys[1]].weights.cpu().numpy(), w0s[keys[1]])
+
+
+def test_module_deferred_checks():
+    """DedupEmbeddingBagCollection(defer_checks=True): forward + backward never
+    read the device; check() raises the reference's error afterwards and the
+    fused SGD left the table untouched for that batch."""
+    b, vocab, dim = 256, 1000, 16
+    batch = _batch(b, [6], vocab, seed=9)
+    k = batch.keys[0]
+    vals = batch.values[k].copy()
+    vals[11] = vocab + 5
+    w0 = np.random.default_rng(0).uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32)
+    t = R.EmbeddingTable(k, vocab, dim, torch.as_tensor(w0, device="cuda").clone())
+    ebc = R.DedupEmbeddingBagCollection({k: t}, "sum", lr=0.1, defer_checks=True)
+    ik = R.kjt_to_ikjt(R.KJT(b, {k: R.JaggedTensor(vals, batch.offsets[k])}), [k])
+    out = ebc(ik)
+    out[k].sum().backward()
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match=rf"feature '{k}': ID {vocab + 5} at position \d+ "
+                                         rf"out of range \[0, {vocab}\)"):
+        ebc.check()
+    np.testing.assert_array_equal(t.weights.cpu().numpy(), w0)
+    ebc.check()   # errors are reported once
