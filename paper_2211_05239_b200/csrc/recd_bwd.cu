@@ -1138,10 +1138,13 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   s->grad_u = a.take<float>((need & NEED_GRADU) ? (size_t)pl.F * B * D : 1);
   const size_t occ = (need & NEED_OCC) ? (size_t)pl.occ_total : 1;
   // diagonal runs: row flags, head (tag, length), per-k_occ-block head counts
-  const int64_t ob = (need & NEED_OCC) ? ceil_div(pl.occ_total, OC_CH) + pl.F + 1 : 1;
-  s->dirty = a.take<uint8_t>((need & NEED_OCC) ? (size_t)pl.F * B : 1);
-  s->head_tag = a.take<uint32_t>(occ);
-  s->head_len = a.take<uint32_t>(occ);
+  // (only the full backward can use runs: its row count B is known to the
+  // scratch-size query; the owner-side sparse SGD's is not)
+  const bool rn = (need & NEED_OCC) && (need & NEED_GRADU);
+  const int64_t ob = rn ? ceil_div(pl.occ_total, OC_CH) + pl.F + 1 : 1;
+  s->dirty = a.take<uint8_t>(rn ? (size_t)pl.F * B : 1);
+  s->head_tag = a.take<uint32_t>(rn ? occ : 1);
+  s->head_len = a.take<uint32_t>(rn ? occ : 1);
   s->blk_heads = a.take<int64_t>(ob);
   s->heads_total = a.take<int64_t>(1);
   {
@@ -1307,7 +1310,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   p.head_tag = sc.head_tag;
   p.head_len = sc.head_len;
   p.blk_heads = sc.blk_heads;
-  const bool runs = do_scatter && use_runs();
+  const bool runs = bm == BwdMode::Full && do_scatter && use_runs();
 
   const bool prep = (phase & PH_PREP) != 0, fin = (phase & PH_FINISH) != 0;
   // sorted buffers: a stable LSD sort of `bits` bits ends in the alternate
