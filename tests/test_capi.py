@@ -55,3 +55,29 @@ def test_no_cpu_fallback():
     from paper_2211_05239_b200 import _lib
     with pytest.raises(ValueError, match="no CPU fallback"):
         _lib.require_cuda(torch.zeros(1))
+
+
+def test_scratch_sizes_cover_every_backward_entry_point():
+    """The scratch-size queries must cover what each entry point carves: with
+    exactly the queried size the call gets past the scratch check (no GPU here,
+    so it then fails launching: RECD_ERR_CUDA = 2, not RECD_ERR_SCRATCH = 3)."""
+    import ctypes as C
+    from paper_2211_05239_b200 import _lib
+    lib = _lib.load()
+    F, rows, D = 2, 3000, 8
+    caps = _lib.i64s([500, 700])
+    fake = [C.c_void_p(4096 * (i + 1)) for i in range(8)]
+    P = lambda *xs: (C.c_void_p * len(xs))(*[x.value for x in xs])  # noqa: E731
+    nb = lib.recd_sparse_sgd_scratch_bytes(F, caps)
+    for fn in (lib.recd_sparse_sgd, lib.recd_sparse_sgd_prepare, lib.recd_sparse_sgd_finish):
+        rc = fn(F, rows, D, P(fake[0], fake[1]), _lib.i64s([rows, rows]), P(fake[2], fake[3]),
+                P(fake[4], fake[5]), caps, fake[6].value, P(fake[6], fake[7]), C.c_float(0.1), 1,
+                None, None, None, fake[7].value, nb, None)
+        assert rc != 3, rc
+    B = 1024
+    nb = lib.recd_pool_bwd_scratch_bytes(F, B, D, caps)
+    for fn in (lib.recd_pool_bwd, lib.recd_pool_bwd_prepare, lib.recd_pool_bwd_finish):
+        rc = fn(F, B, D, 0, P(fake[0], fake[1]), _lib.i64s([rows, rows]), P(fake[2], fake[3]),
+                P(fake[4], fake[5]), caps, fake[6].value, P(fake[6], fake[6]), P(fake[7], fake[7]),
+                C.c_float(0.1), 1, None, None, None, fake[7].value, nb, None)
+        assert rc != 3, rc
