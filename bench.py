@@ -395,15 +395,12 @@ def run_reference(args):
 # --------------------------------------------------------------- launcher
 def spawn_ranks(args):
     """`--gpus N` without a launcher: run this script under
-    torch.distributed.run with N ranks (127.0.0.1 rendezvous) and pass its exit
-    code through; rank 0's stdout is the JSON line."""
-    import socket
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
-           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    torch.distributed.run with N ranks (standalone rendezvous on 127.0.0.1,
+    free port chosen by the launcher) and pass its exit code through; rank
+    0's stdout is the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--local-addr",
+           "127.0.0.1", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           os.path.abspath(__file__), *sys.argv[1:]]
     env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "4"))
     return subprocess.call(cmd, env=env)
 

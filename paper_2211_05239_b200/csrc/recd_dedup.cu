@@ -108,9 +108,16 @@ __device__ __forceinline__ uint64_t finalize_hash(uint64_t h, uint64_t mask) {
 #define RECD_RS_IT 8
 #endif
 constexpr int RS_NT = 256;
-constexpr int RS_RPB = RECD_RS_RPB;  // rows per block
+constexpr int RS_RPB = RECD_RS_RPB;  // rows per block (long rows)
+// short rows: more rows per block, so a block still streams ~16 KB of values
+// (a 256-row block of length-8 rows is one 8-value load per thread, all
+// latency); the class of a group is chosen from its average row length
+#ifndef RECD_RS_SHORT
+#define RECD_RS_SHORT 1
+#endif
 constexpr int RS_IT = RECD_RS_IT;    // consecutive values per thread
 
+template <int RS_RPB>
 __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ DedupParams p) {
   const int g = p.rs_group[blockIdx.y];
   const int tid = threadIdx.x;
@@ -122,6 +129,7 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
   __shared__ int64_t s_start[RS_RPB + 1];
   __shared__ int32_t s_len[RS_RPB];
   __shared__ uint32_t s_mism[RS_RPB];
+  __shared__ int s_hashG;  // lanes per head row in the hash pass (32: warp per row)
 
   {  // clear this block's slice of the group's hash table
     const int64_t lo = r0 * p.C / p.B, hi = r1 * p.C / p.B;
@@ -161,10 +169,16 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
     // row's are already heads, and compares can only set flags, so the chunk's
     // first row needs no special case
     const int64_t L0 = s_start[1] - s_start[0];
-    bool uni = L0 > 0 && L0 < (1 << 23);
+    bool uni = L0 > 0 && L0 < (int64_t)(1u << 31) / RS_RPB;  // (q - vbeg) fits 32 bits
     for (int j = tid; j < n; j += RS_NT) uni &= (int64_t)s_len[j] == L0;
+    if (tid == 0) s_hashG = 32;
     if (__syncthreads_and(uni)) {
       const uint32_t L = (uint32_t)L0;
+      if (tid == 0 && fbeg + 1 == fend && L0 < 32) {
+        int G = 1;
+        while (G < L0) G <<= 1;
+        s_hashG = G;
+      }
       for (int64_t tb = tb0; tb < vend; tb += (int64_t)RS_NT * RS_IT) {
         const int64_t q0 = tb + (int64_t)tid * RS_IT;
         if (q0 >= vend || q0 + RS_IT <= vbeg) continue;
@@ -274,9 +288,33 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
   uint8_t* head = p.head + (int64_t)g * p.B;
   for (int j = tid; j < n; j += RS_NT) head[r0 + j] = s_mism[j] ? 1 : 0;
   // content hash of the chunk's heads (their values were just streamed, so
-  // the re-read is mostly served by L2): warp per head row, lane-strided
+  // the re-read is mostly served by L2).  A single-feature group whose rows
+  // share one length L hashes 32 / G rows per warp at once (G = lanes per row,
+  // the power of two >= L, <= 32); otherwise a warp per head row, lane-strided.
   const int warp = tid >> 5, lane = tid & 31;
   uint64_t* hash = p.hash + (int64_t)g * p.B;
+  const int G = s_hashG;
+  if (G < 32) {
+    const int gid = lane / G, gl = lane % G, per = 32 / G;
+    const int64_t* off = p.offsets[fbeg];
+    const int64_t* val0 = p.values[fbeg];
+    for (int j0 = warp * per; j0 < n; j0 += (RS_NT / 32) * per) {  // warp-uniform trips
+      const int j = j0 + gid;
+      const bool mine = j < n && s_mism[j];
+      uint64_t h = 0;
+      if (mine) {
+        const int64_t st = s_start[j];
+        const int64_t len = s_start[j + 1] - st;   // == L <= G
+        if (gl == 0) h += len_hash(len, 0);
+        if (gl < len) h += elem_hash(__ldg(val0 + st + gl), gl, 0);
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1)
+        if (d < G) h += __shfl_xor_sync(0xffffffffu, h, d);
+      if (mine && gl == 0) hash[r0 + j] = finalize_hash(h, p.hash_mask);
+    }
+    return;
+  }
   for (int j = warp; j < n; j += RS_NT / 32) {
     if (!s_mism[j]) continue;
     const int64_t row = r0 + j;
@@ -820,6 +858,7 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
     p.treps = s.treps + (int64_t)g0 * C;
 
     const int64_t rows = (int64_t)p.G * B;
+    double rs_avg[RECD_MAX_FEAT];
     {  // groups with the most values first (their blocks are the longest)
       std::vector<std::pair<int64_t, int>> order;
       for (int g = 0; g < p.G; ++g) {
@@ -829,9 +868,32 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
       }
       std::stable_sort(order.begin(), order.end());
       for (int k = 0; k < p.G; ++k) p.rs_group[k] = order[k].second;
+      // row-scan class per group by its average row length (values per row)
+      for (int k = 0; k < p.G; ++k) rs_avg[k] = (double)(-order[k].first) / (double)B;
     }
     if (phase & DD_NUMBER) {
-      k_rowscan<<<dim3((unsigned)ceil_div(B, RS_RPB), p.G), RS_NT, 0, stream>>>(p);
+      {
+        // groups are ordered by value count (most first): long-row groups take
+        // 256-row blocks, rows of <= 12 values 2048-row blocks, <= 48 1024
+        int k0 = 0;
+        auto launch_class = [&](int k1, int rpb) {
+          if (k1 <= k0) return;
+          DedupParams q = p;
+          for (int k = k0; k < k1; ++k) q.rs_group[k - k0] = p.rs_group[k];
+          const dim3 grid((unsigned)ceil_div(B, rpb), (unsigned)(k1 - k0));
+          if (rpb == 2048) k_rowscan<2048><<<grid, RS_NT, 0, stream>>>(q);
+          else if (rpb == 1024) k_rowscan<1024><<<grid, RS_NT, 0, stream>>>(q);
+          else k_rowscan<RS_RPB><<<grid, RS_NT, 0, stream>>>(q);
+          note_launch();
+          k0 = k1;
+        };
+        int k1 = 0;
+        while (k1 < p.G && (!RECD_RS_SHORT || rs_avg[k1] > 48.0)) ++k1;
+        launch_class(k1, RS_RPB);
+        while (k1 < p.G && rs_avg[k1] > 12.0) ++k1;
+        launch_class(k1, 1024);
+        launch_class(p.G, 2048);
+      }
       k_insert<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
       k_resolve<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
       k_fallback<<<p.G, FB_NT, 0, stream>>>(p);
@@ -840,7 +902,7 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
       k_num_scan<<<p.G, NB_NT, 0, stream>>>(p);
       k_num_down<<<ng, NB_NT, 0, stream>>>(p);
       k_num_inv<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
-      note_launch(8);
+      note_launch(7);
     }
     if (phase & DD_COPY) {
       int64_t cblk = 0;
