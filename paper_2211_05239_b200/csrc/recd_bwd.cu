@@ -42,7 +42,9 @@
 
 namespace recd {
 
-constexpr int RC = 256;  // sorted positions per scatter work item
+constexpr int RC_BIG = 256;   // sorted positions per scatter work item
+constexpr int RC_SMALL = 64;  // ... when the occurrence arrays are small (latency-bound)
+static int rc_for(int64_t occ_total) { return occ_total >= (4ll << 20) ? RC_BIG : RC_SMALL; }
 
 struct BwdParams {
   int F;
@@ -210,7 +212,8 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
 // end), gathering grad_out rows 8 positions at a time across run boundaries, so
 // no per-row dependent chain (CSR start -> row ids -> gradient rows) stalls it.
 // Same order as k_grad_u (ascending batch row within each unique row).
-constexpr int GU_CH = 256;
+constexpr int GU_CH = 256;     // positions per warp task (32 for small batches: more tasks)
+constexpr int GU_CH_SMALL = 32;
 __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t n, uint32_t id,
                                            int lane);
 #ifndef RECD_GUF_CS
@@ -219,7 +222,7 @@ __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t
 #ifndef RECD_GUF_MINB
 #define RECD_GUF_MINB 3
 #endif
-template <class C>
+template <class C, int GU_CH>
 __global__ void __launch_bounds__(256, RECD_GUF_MINB) k_grad_u_flat(const __grid_constant__ BwdParams p) {
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
   const int ncb = col_blocks<C>(p.D);
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(256, RECD_GUF_MINB) k_grad_u_flat(const __grid
 // spans in shared memory, and consecutive threads handle consecutive values
 // (coalesced loads of the unique values, coalesced pair stores).
 #ifndef RECD_OC_CH
-#define RECD_OC_CH 4096
+#define RECD_OC_CH 16384
 #endif
 constexpr int OC_CH = RECD_OC_CH;
 constexpr int OC_MAXR = 512;
@@ -661,6 +664,7 @@ __device__ __forceinline__ int rc_seg(const BwdParams& p, int64_t chunk) {
 }
 
 // number of run starts per RC chunk (grad-output mode)
+template <int RC>
 __global__ void __launch_bounds__(RC) k_run_count(const __grid_constant__ BwdParams p) {
   const int64_t chunk = blockIdx.x;
   const int s = rc_seg(p, chunk);
@@ -691,6 +695,9 @@ constexpr int SC_RS = RECD_SC_RS;  // table rows prefetched ahead per warp (shar
 #ifndef RECD_SC_PIPE
 #define RECD_SC_PIPE 0
 #endif
+#ifndef RECD_SC_REV
+#define RECD_SC_REV 0
+#endif
 #ifndef RECD_SC_BATCH
 #define RECD_SC_BATCH 6
 #endif
@@ -703,7 +710,7 @@ constexpr int SC_BATCH = RECD_SC_BATCH;  // unique-row gradient gathers in fligh
 // per-warp shared ring while grad_u rows (L2-resident) are gathered 8 positions
 // at a time across run boundaries; at each run end the row is updated and
 // stored, and its slot refilled with the row of run r + SC_RS.
-template <class C, bool SINGLE, bool RUNS>
+template <class C, bool SINGLE, bool RUNS, int RC>
 __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid_constant__ BwdParams p) {
   constexpr int V = C::VW;
   __shared__ uint16_t s_starts[8][RC + 2];
@@ -724,8 +731,11 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   const uint64_t pol_stream = HINT ? l2_evict_first() : 0;
   const uint64_t pol_keep = (HINT && RECD_SCATTER_L2 >= 2) ? l2_evict_last() : 0;
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
-    const int64_t chunk = (ncb == 1) ? w : w / ncb;
-    const int lo_f = (int)(w - chunk * ncb) * C::CB + lane * V;  // this lane's first float
+    const int64_t wc = (ncb == 1) ? w : w / ncb;
+    // RECD_SC_REV: last table segment first -- k_grad_u_flat wrote the unique-row
+    // gradients in feature order, so the last features' are still in L2
+    const int64_t chunk = RECD_SC_REV ? p.total_rc_chunks - 1 - wc : wc;
+    const int lo_f = (int)(w - wc * ncb) * C::CB + lane * V;  // this lane's first float
     const bool ok = lo_f < p.D;
     const uint32_t D32 = (uint32_t)p.D;
     const int s = rc_seg(p, chunk);
@@ -1062,6 +1072,7 @@ struct Plan {
   std::vector<int64_t> table_rows;  // max rows per table seg
   std::vector<int64_t> ts_base, ts_cap, ts_chunk0;
   int64_t occ_total, rc_chunks;
+  int rc;  // scatter chunk (RC_BIG / RC_SMALL)
 };
 
 Plan make_plan(int F, const int64_t* const* inverse, float* const* tables, const int64_t* rows,
@@ -1096,11 +1107,14 @@ Plan make_plan(int F, const int64_t* const* inverse, float* const* tables, const
   pl.nis = (int)pl.inverse.size();
   pl.nts = (int)pl.table.size();
   int64_t base = 0, chunk = 0;
+  for (int s = 0; s < pl.nts; ++s) base += pl.ts_cap[s];
+  pl.rc = rc_for(base);
+  base = 0;
   for (int s = 0; s < pl.nts; ++s) {
     pl.ts_base.push_back(base);
     pl.ts_chunk0.push_back(chunk);
     base += pl.ts_cap[s];
-    chunk += std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RC));
+    chunk += std::max<int64_t>(1, ceil_div(pl.ts_cap[s], pl.rc));
   }
   pl.occ_total = base;
   pl.rc_chunks = chunk;
@@ -1171,7 +1185,7 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   // run-count scan partials (one scan segment per table)
   std::vector<ScanDesc> sd;
   for (int t = 0; t < pl.nts; ++t) {
-    const int64_t nch = std::max<int64_t>(1, ceil_div(pl.ts_cap[t], RC));
+    const int64_t nch = std::max<int64_t>(1, ceil_div(pl.ts_cap[t], pl.rc));
     sd.push_back({nullptr, nullptr, nch, nullptr, nullptr});
   }
   s->scan_part = a.take<int64_t>(std::max<int64_t>(scan_part_words(sd.data(), (int)sd.size()), 1));
@@ -1394,20 +1408,28 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         note_launch();
       }
       if (RECD_GU_FLAT && any_inv) {
+        const bool small = B < 32768;  // latency-bound: 32-position tasks
+        const int ch = small ? GU_CH_SMALL : GU_CH;
         const unsigned gf = (unsigned)std::min<int64_t>(
-            ceil_div(ceil_div(B, GU_CH) * F * ncb, 8), (int64_t)num_sms() * 16);
-        k_grad_u_flat<C><<<std::max(gf, 1u), 256, 0, stream>>>(p);
+            ceil_div(ceil_div(B, ch) * F * ncb, 8), (int64_t)num_sms() * 16);
+        if (small)
+          k_grad_u_flat<C, GU_CH_SMALL><<<std::max(gf, 1u), 256, 0, stream>>>(p);
+        else
+          k_grad_u_flat<C, GU_CH><<<std::max(gf, 1u), 256, 0, stream>>>(p);
         note_launch();
       }
     }
     // 5. sorted scatter-add (+ fused SGD)
     if (do_scatter) {
       if (!apply_sgd) {
-        k_run_count<<<(unsigned)pl.rc_chunks, RC, 0, stream>>>(p);
+        if (pl.rc == RC_BIG)
+          k_run_count<RC_BIG><<<(unsigned)pl.rc_chunks, RC_BIG, 0, stream>>>(p);
+        else
+          k_run_count<RC_SMALL><<<(unsigned)pl.rc_chunks, RC_SMALL, 0, stream>>>(p);
         note_launch();
         std::vector<ScanDesc> sd;
         for (int s = 0; s < pl.nts; ++s) {
-          const int64_t nch = std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RC));
+          const int64_t nch = std::max<int64_t>(1, ceil_div(pl.ts_cap[s], pl.rc));
           sd.push_back({sc.run_part + pl.ts_chunk0[s], sc.run_part + pl.ts_chunk0[s], nch,
                         nullptr, p.grad_count[s]});
         }
@@ -1418,15 +1440,27 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
           (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks * ncb, 8), (int64_t)num_sms() * 16);
       hook_before("k_scatter", stream);
       if (runs) {
+        if (pl.rc == RC_BIG) {
+          if (single)
+            k_scatter<C, true, true, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          else
+            k_scatter<C, false, true, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+        } else {
+          if (single)
+            k_scatter<C, true, true, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          else
+            k_scatter<C, false, true, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+        }
+      } else if (pl.rc == RC_BIG) {
         if (single)
-          k_scatter<C, true, true><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          k_scatter<C, true, false, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
         else
-          k_scatter<C, false, true><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          k_scatter<C, false, false, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
       } else {
         if (single)
-          k_scatter<C, true, false><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          k_scatter<C, true, false, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
         else
-          k_scatter<C, false, false><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          k_scatter<C, false, false, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
       }
       hook_after("k_scatter", stream);
       note_launch();

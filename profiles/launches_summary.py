@@ -8,7 +8,7 @@ for r in data:
     if len(r) <= vi: continue
     name = r[ki].split('(')[0].split('<')[0].replace('void ','')
     seq.append((int(r[ii]), name, float(r[vi].replace(',',''))))
-idx = [i for i,(id_,n,v) in enumerate(seq) if n.endswith('k_rowscan')]
+idx = [i for i,(id_,n,v) in enumerate(seq) if n.endswith('k_insert')]
 last = seq[idx[-2]:idx[-1]] if len(idx) > 1 else seq
 s = sum(v for _,_,v in last)
 print('launches in step', len(last), 'sum ms', s/1e6)

@@ -18,6 +18,8 @@ V = {
     "sp4m3": ["RECD_SC_PIPE=1", "RECD_SC_BATCH=4", "RECD_SCATTER_MINB=3"],
     "sp6m3": ["RECD_SC_PIPE=1", "RECD_SC_BATCH=6", "RECD_SCATTER_MINB=3"],
     "sp3m4": ["RECD_SC_PIPE=1", "RECD_SC_BATCH=3", "RECD_SCATTER_MINB=4"],
+    "screv": ["RECD_SC_REV=1"],
+    "rsold": ["RECD_RS_SHORT=0"],
     "cp32": ["RECD_CP_IT=32", "RECD_OC_CH=8192"],
     "cp64": ["RECD_CP_IT=64", "RECD_OC_CH=16384"],
 }
