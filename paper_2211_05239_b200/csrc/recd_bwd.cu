@@ -95,6 +95,7 @@ struct BwdParams {
   uint32_t* head_len;     // [occ cap] run length k (rows tag .. tag + k - 1)
   int64_t* blk_heads;     // [occ blocks] heads per k_occ block -> exclusive prefix
   int64_t occ_blk0[RECD_MAX_FEAT + 1];  // k_occ: first block of each feature (capacity)
+  int64_t oc_ch;                         // k_occ / k_runs: unique values per block
   // optional scatter of grad_u rows to peers (fused source -> owner push): row u
   // of feature f goes to gseg_dst[f][j] + (*gseg_row0[f][j] + u) * D, j < gsegs
   int gsegs;
@@ -328,16 +329,17 @@ __global__ void __launch_bounds__(256, RECD_GUF_MINB) k_grad_u_flat(const __grid
 #ifndef RECD_OC_CH
 #define RECD_OC_CH 16384
 #endif
-constexpr int OC_CH = RECD_OC_CH;
+constexpr int OC_CH = RECD_OC_CH;   // values per block on big batches
+constexpr int OC_CH_SMALL = 4096;  // ... and on small ones (more blocks in flight)
 constexpr int OC_MAXR = 512;
 __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p, uint32_t* keys,
                                              uint32_t* vals) {
   int f = 0;
   while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
-  const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * OC_CH;
+  const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * p.oc_ch;
   const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
   if (j0 >= NV) return;
-  const int64_t j1 = min(NV, j0 + (int64_t)OC_CH);
+  const int64_t j1 = min(NV, j0 + p.oc_ch);
   const int tid = threadIdx.x;
   const int64_t* uo = p.uoffsets[f];
   const int64_t* src = p.uvalues[f];
@@ -555,7 +557,7 @@ __global__ void __launch_bounds__(256) k_runs(const __grid_constant__ BwdParams 
                                               uint32_t* vals) {
   int f = 0;
   while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
-  const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * OC_CH;
+  const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * p.oc_ch;
   const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
   const int tid = threadIdx.x;
   __shared__ int64_t s_scan[32];
@@ -563,7 +565,7 @@ __global__ void __launch_bounds__(256) k_runs(const __grid_constant__ BwdParams 
     if (!EMIT && tid == 0) p.blk_heads[blockIdx.x] = 0;
     return;
   }
-  const int64_t j1 = min(NV, j0 + (int64_t)OC_CH);
+  const int64_t j1 = min(NV, j0 + p.oc_ch);
   const int64_t* uo = p.uoffsets[f];
   const int64_t* src = p.uvalues[f];
   const uint8_t* dirty = p.dirty + (int64_t)f * p.B;
@@ -1155,7 +1157,7 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   // (only the full backward can use runs: its row count B is known to the
   // scratch-size query; the owner-side sparse SGD's is not)
   const bool rn = (need & NEED_OCC) && (need & NEED_GRADU);
-  const int64_t ob = rn ? ceil_div(pl.occ_total, OC_CH) + pl.F + 1 : 1;
+  const int64_t ob = rn ? ceil_div(pl.occ_total, OC_CH_SMALL) + pl.F + 1 : 1;
   s->dirty = a.take<uint8_t>(rn ? (size_t)pl.F * B : 1);
   s->head_tag = a.take<uint32_t>(rn ? occ : 1);
   s->head_len = a.take<uint32_t>(rn ? occ : 1);
@@ -1358,9 +1360,10 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     // 3-4. occurrences, sorted by ID per table segment
     if (do_scatter) {
       int64_t ob = 0;
+      p.oc_ch = pl.occ_total >= (8ll << 20) ? OC_CH : OC_CH_SMALL;
       for (int f = 0; f < F; ++f) {
         p.occ_blk0[f] = ob;
-        ob += std::max<int64_t>(1, ceil_div(do_scatter ? value_caps[f] : 1, OC_CH));
+        ob += std::max<int64_t>(1, ceil_div(do_scatter ? value_caps[f] : 1, p.oc_ch));
       }
       p.occ_blk0[F] = ob;
       if (runs) {
