@@ -23,6 +23,9 @@
 #ifndef RECD_POOL_RING
 #define RECD_POOL_RING 1
 #endif
+#ifndef RECD_RING_CA
+#define RECD_RING_CA 0
+#endif
 #ifndef RECD_RING_K
 #define RECD_RING_K 2
 #endif
@@ -254,7 +257,16 @@ struct RingRows {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t id = __shfl_sync(0xffffffffu, cur, sh + k);
-        if (ok && p0 + k < n) cp_async<16>(dst + k * 128, Wl + (uint64_t)id * D);
+        if (ok && p0 + k < n) {
+#if RECD_RING_CA  // L1-allocating: the 8 warps of a CTA pool consecutive unique rows,
+                  // which in session data are shifted windows of each other
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + k * 128);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                       "l"(Wl + (uint64_t)id * D));
+#else
+          cp_async<16>(dst + k * 128, Wl + (uint64_t)id * D);
+#endif
+        }
       }
     }
     cp_async_commit();

@@ -1,5 +1,6 @@
 // Library-level bookkeeping: version, launch counter, SM count cache.
 #include <atomic>
+#include <cstdlib>
 #include <string>
 
 #include "recd_common.cuh"
@@ -26,6 +27,9 @@ int num_sms() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
   if (!cached[dev]) {
+    // experiment knob: L2 set-aside for evict_last / persisting lines (MB)
+    if (const char* e = getenv("RECD_L2_PERSIST_MB"))
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(e) << 20);
     int n = 0;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
       n = 148;

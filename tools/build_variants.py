@@ -20,6 +20,14 @@ V = {
     "sp3m4": ["RECD_SC_PIPE=1", "RECD_SC_BATCH=3", "RECD_SCATTER_MINB=4"],
     "screv": ["RECD_SC_REV=1"],
     "rsold": ["RECD_RS_SHORT=0"],
+    "os12m4": ["RECD_OS_ITEMS=12", "RECD_OS_MINB=4"],
+    "os8m5": ["RECD_OS_ITEMS=8", "RECD_OS_MINB=5"],
+    "os16m4": ["RECD_OS_MINB=4"],
+    "oslb16": ["RECD_OS_LB=16"],
+    "ca2": ["RECD_RING_CA=1"],
+    "ca1m3": ["RECD_RING_CA=1", "RECD_RING_K=1"],
+    "ca1m4": ["RECD_RING_CA=1", "RECD_RING_K=1", "RECD_RING_MINB=4"],
+    "k1m4": ["RECD_RING_K=1", "RECD_RING_MINB=4"],
     "cp32": ["RECD_CP_IT=32", "RECD_OC_CH=8192"],
     "cp64": ["RECD_CP_IT=64", "RECD_OC_CH=16384"],
 }
