@@ -123,6 +123,37 @@ __device__ __forceinline__ float4 ld_v4_hint(const float* p, uint64_t pol) {
   return v;
 }
 
+// TMA bulk copies (cp.async.bulk, no tensor map): one thread moves a
+// contiguous global range (16-byte aligned, size a multiple of 16) into shared
+// memory; completion is counted on an mbarrier as transaction bytes.
+__device__ __forceinline__ void mbar_init1(uint64_t* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(m))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(m)),
+      "r"(parity)
+      : "memory");
+}
+// arrive on `m` expecting `bytes`, then (bytes > 0) copy them global -> shared
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* m) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(m);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+               : "memory");
+  if (bytes)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(smem)),
+        "l"(gmem), "r"(bytes), "r"(mb)
+        : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" :: RECD_CLOB);
 }

@@ -119,6 +119,15 @@ constexpr int RS_RPB = RECD_RS_RPB;  // rows per block (long rows)
 #define RECD_RS_SHORT 0
 #endif
 constexpr int RS_IT = RECD_RS_IT;    // consecutive values per thread
+// uniform chunks stream their values through shared memory with TMA bulk
+// copies (3 stages of RT_T values, one thread issues, mbarrier completion):
+// every value is read from HBM once, the predecessor row comes from the same
+// or the previous stage, and the loads are in flight 2 tiles ahead
+#ifndef RECD_RS_TMA
+#define RECD_RS_TMA 1
+#endif
+constexpr int RT_T = 2048;                                    // values per stage (16 KB)
+constexpr int RT_SMEM = RECD_RS_TMA ? 3 * RT_T * 8 : 0;       // dynamic shared memory
 
 template <int RS_RPB>
 __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ DedupParams p) {
@@ -133,6 +142,15 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
   __shared__ int32_t s_len[RS_RPB];
   __shared__ uint32_t s_mism[RS_RPB];
   __shared__ int s_hashG;  // lanes per head row in the hash pass (32: warp per row)
+#if RECD_RS_TMA
+  extern __shared__ __align__(128) int64_t s_stage[];  // [3][RT_T]
+  __shared__ __align__(8) uint64_t s_bar[3];
+  uint32_t tiles_seen = 0;  // staged tiles of earlier features: tile sequence number base
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) mbar_init1(&s_bar[b]);
+    mbar_fence_init();
+  }
+#endif
 
   {  // clear this block's slice of the group's hash table
     const int64_t lo = r0 * p.C / p.B, hi = r1 * p.C / p.B;
@@ -182,6 +200,80 @@ __global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ Dedup
         while (G < L0) G <<= 1;
         s_hashG = G;
       }
+#if RECD_RS_TMA
+      if (a16 && L0 <= RT_T) {
+        // tiles [tbeg + t RT_T, +RT_T) of the chunk's values, 16-byte aligned;
+        // the copied part of a tile ends at an even value <= vend, a last odd
+        // value is read from global memory
+        const int64_t tbeg = vbeg & ~(int64_t)1;
+        const int ntiles = (int)ceil_div(vend - tbeg, (int64_t)RT_T);
+        // tile t is the block's (tiles_seen + t)-th staged tile: stage and
+        // barrier (that % 3), barrier phase parity (that / 3) & 1
+        auto issue = [&](int t) {
+          const int64_t a = tbeg + (int64_t)t * RT_T;
+          const int64_t e = min(a + (int64_t)RT_T, vend) & ~(int64_t)1;
+          const uint32_t sq = tiles_seen + (uint32_t)t;
+          bulk_load(s_stage + (sq % 3) * RT_T, val + a, (uint32_t)(max(e - a, (int64_t)0) * 8),
+                    &s_bar[sq % 3]);
+        };
+        if (tid == 0) {
+          issue(0);
+          if (ntiles > 1) issue(1);
+        }
+        const uint32_t dj = RS_NT / L, dr = RS_NT % L;
+        for (int t = 0; t < ntiles; ++t) {
+          const uint32_t sq = tiles_seen + (uint32_t)t;
+          const int b = (int)(sq % 3);
+          mbar_wait_parity(&s_bar[b], (sq / 3) & 1u);
+          const int64_t a = tbeg + (int64_t)t * RT_T;
+          const int64_t ecp = min(a + (int64_t)RT_T, vend) & ~(int64_t)1;  // copied part
+          const int64_t* cur = s_stage + b * RT_T;
+          const int64_t* prv = s_stage + ((sq + 2) % 3) * RT_T;           // tile t - 1
+          // values q = a + k * RS_NT + tid (consecutive threads, consecutive
+          // values: conflict-free shared loads); row stepped incrementally
+          const int64_t q_first = a + tid;
+          uint32_t j = 0, rem = 0;
+          if (q_first >= vbeg) {
+            const uint32_t rel = (uint32_t)(q_first - vbeg);
+            j = rel / L;
+            rem = rel - j * L;
+          } else {  // only in the first tile, before the chunk's first value
+            const uint32_t back = (uint32_t)(vbeg - q_first);  // 1 (tbeg = vbeg - 1)
+            rem = L - back;   // the position just before row 0 (skipped below)
+            j = 0;
+          }
+#pragma unroll 4
+          for (int k = 0; k < RT_T / RS_NT; ++k) {
+            const int64_t q = q_first + (int64_t)k * RS_NT;
+            if (q >= vbeg && q < vend) {
+              const int64_t v = q < ecp ? cur[q - a] : __ldg(val + q);
+              const int64_t pq = q - L0;
+              int64_t pv;
+              if (pq >= a) pv = cur[pq - a];
+              else if (t > 0 && pq >= a - RT_T) pv = prv[pq - (a - RT_T)];
+              else pv = __ldg(val + max(pq, (int64_t)0));
+              if (pv != v) s_mism[j] = 1u;
+            }
+            if (q >= vbeg) {
+              j += dj;
+              rem += dr;
+              if (rem >= L) {
+                rem -= L;
+                ++j;
+              }
+            } else {   // q = vbeg - 1: the next value of this thread is vbeg - 1 + RS_NT
+              const uint32_t rel = (uint32_t)(q + RS_NT - vbeg);
+              j = rel / L;
+              rem = rel - j * L;
+            }
+          }
+          __syncthreads();  // every thread is done with tile t - 1's stage
+          if (tid == 0 && t + 2 < ntiles) issue(t + 2);
+        }
+        tiles_seen += (uint32_t)ntiles;
+        continue;
+      }
+#endif
       for (int64_t tb = tb0; tb < vend; tb += (int64_t)RS_NT * RS_IT) {
         const int64_t q0 = tb + (int64_t)tid * RS_IT;
         if (q0 >= vend || q0 + RS_IT <= vbeg) continue;
@@ -879,14 +971,28 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
         // groups are ordered by value count (most first): long-row groups take
         // 256-row blocks, rows of <= 12 values 2048-row blocks, <= 48 1024
         int k0 = 0;
+        if (RT_SMEM > 0) {  // opt in to the staged row scan's dynamic shared memory
+          static bool attr[64] = {};
+          int dev = 0;
+          RECD_CUDA_CHECK(cudaGetDevice(&dev));
+          if (dev < 0 || dev >= 64 || !attr[dev]) {
+            RECD_CUDA_CHECK(cudaFuncSetAttribute(k_rowscan<RS_RPB>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, RT_SMEM));
+            RECD_CUDA_CHECK(cudaFuncSetAttribute(k_rowscan<1024>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, RT_SMEM));
+            RECD_CUDA_CHECK(cudaFuncSetAttribute(k_rowscan<2048>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, RT_SMEM));
+            if (dev >= 0 && dev < 64) attr[dev] = true;
+          }
+        }
         auto launch_class = [&](int k1, int rpb) {
           if (k1 <= k0) return;
           DedupParams q = p;
           for (int k = k0; k < k1; ++k) q.rs_group[k - k0] = p.rs_group[k];
           const dim3 grid((unsigned)ceil_div(B, rpb), (unsigned)(k1 - k0));
-          if (rpb == 2048) k_rowscan<2048><<<grid, RS_NT, 0, stream>>>(q);
-          else if (rpb == 1024) k_rowscan<1024><<<grid, RS_NT, 0, stream>>>(q);
-          else k_rowscan<RS_RPB><<<grid, RS_NT, 0, stream>>>(q);
+          if (rpb == 2048) k_rowscan<2048><<<grid, RS_NT, RT_SMEM, stream>>>(q);
+          else if (rpb == 1024) k_rowscan<1024><<<grid, RS_NT, RT_SMEM, stream>>>(q);
+          else k_rowscan<RS_RPB><<<grid, RS_NT, RT_SMEM, stream>>>(q);
           note_launch();
           k0 = k1;
         };
