@@ -122,9 +122,11 @@ constexpr int RS_IT = RECD_RS_IT;    // consecutive values per thread
 // uniform chunks stream their values through shared memory with TMA bulk
 // copies (3 stages of RT_T values, one thread issues, mbarrier completion):
 // every value is read from HBM once, the predecessor row comes from the same
-// or the previous stage, and the loads are in flight 2 tiles ahead
+// or the previous stage, and the loads are in flight 2 tiles ahead.  Exact
+// (113 dedup/step/fullsize tests green with it on) but slower: row scan 0.465
+// vs 0.395 ms, dedup 0.68 vs 0.61 ms (profiles/r2_rowscan_tma_ab.txt); off.
 #ifndef RECD_RS_TMA
-#define RECD_RS_TMA 1
+#define RECD_RS_TMA 0
 #endif
 constexpr int RT_T = 2048;                                    // values per stage (16 KB)
 constexpr int RT_SMEM = RECD_RS_TMA ? 3 * RT_T * 8 : 0;       // dynamic shared memory
