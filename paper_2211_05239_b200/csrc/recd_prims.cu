@@ -17,6 +17,7 @@
 // are ranked in segment order, so every pass is stable and the result
 // deterministic.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "recd_prims.cuh"
@@ -289,12 +290,16 @@ int64_t sort_hist_words(const SegDesc* segs, int S) {
   return words;
 }
 
+// persistent sort CTAs per SM (RECD_OS_CTAS env: fewer than the occupancy
+// limit leaves SM slots to a kernel running beside the sort on another stream)
 static int os_grid() {
   static int g = 0;
   if (!g) {
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_onesweep, OS_NT, 0);
-    g = num_sms() * std::max(per, 1);
+    per = std::max(per, 1);
+    if (const char* e = getenv("RECD_OS_CTAS")) per = std::max(1, std::min(per, atoi(e)));
+    g = num_sms() * per;
   }
   return g;
 }

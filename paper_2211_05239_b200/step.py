@@ -31,6 +31,7 @@ This is the device-side equivalent of one `forward_iteration`'s sparse part
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -349,10 +350,15 @@ class TrainStep:
             else:
                 self.run()  # warm-up on the side stream
         torch.cuda.current_stream(self.dev).wait_stream(s)
+        # the main stream's kernels (lookup, expand, backward finish) are captured
+        # at high priority: when the side stream's occurrence sort runs beside
+        # them, the block scheduler fills free SM slots with theirs first
+        prio = int(os.environ.get("RECD_MAIN_PRIORITY", "0"))
+        cap = torch.cuda.Stream(self.dev, priority=prio) if prio else None
         for k in range(self.nslots):
             self.use_slot(k, k if self.pipeline else cur_stage)
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=cap):
                 if self.pipeline:
                     self.run_pipelined(k)
                 else:
