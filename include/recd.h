@@ -191,6 +191,9 @@ int recd_dedup_ex(int32_t num_groups, const int32_t* group_sizes, int64_t batch_
  * apply_sgd = 0: grad_ids_out[f][k], grad_rows_out[f][k] = k-th distinct ID
  *                and its gradient, grad_counts_out[f] = number of IDs.
  * Features sharing an inverse pointer share one inverse CSR.  Only sum/avg.
+ * An ID outside [0, table_rows[f]) anywhere in the call (negative, or >= rows:
+ * the lookup reports it, trainer_sim.py:312-320) suppresses every table update
+ * and gradient output of the call -- nothing is written out of bounds.
  *   value_caps  host [F] capacity of uvalues[f] (worst-case N_u)
  */
 size_t recd_pool_bwd_scratch_bytes(int32_t num_features, int64_t batch_size, int32_t dim,
