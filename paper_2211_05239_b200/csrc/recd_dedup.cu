@@ -131,8 +131,11 @@ constexpr int RS_IT = RECD_RS_IT;    // consecutive values per thread
 constexpr int RT_T = 2048;                                    // values per stage (16 KB)
 constexpr int RT_SMEM = RECD_RS_TMA ? 3 * RT_T * 8 : 0;       // dynamic shared memory
 
+#ifndef RECD_RS_MINB
+#define RECD_RS_MINB 4
+#endif
 template <int RS_RPB>
-__global__ void __launch_bounds__(RS_NT) k_rowscan(const __grid_constant__ DedupParams p) {
+__global__ void __launch_bounds__(RS_NT, RECD_RS_MINB) k_rowscan(const __grid_constant__ DedupParams p) {
   const int g = p.rs_group[blockIdx.y];
   const int tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * RS_RPB;

@@ -25,6 +25,8 @@ V = {
     "os16m4": ["RECD_OS_MINB=4"],
     "oslb16": ["RECD_OS_LB=16"],
     "notma": ["RECD_RS_TMA=0"],
+    "rsm5": ["RECD_RS_MINB=5"],
+    "rsm6": ["RECD_RS_MINB=6"],
     "ca2": ["RECD_RING_CA=1"],
     "ca1m3": ["RECD_RING_CA=1", "RECD_RING_K=1"],
     "ca1m4": ["RECD_RING_CA=1", "RECD_RING_K=1", "RECD_RING_MINB=4"],
