@@ -89,11 +89,16 @@ struct BwdParams {
   uint32_t* occ_vals;     // tag = (f << 24) | u
   int64_t* run_part;      // [total_rc_chunks] exclusive run counts (grad-output mode)
   int32_t* bad;           // set by k_occ when an ID is outside [0, rows): no table update
-  // diagonal-run occurrences (RECD_BWD_RUNS): see k_runs_*
-  uint8_t* dirty;         // [F][B] unique row holds some ID twice
+  // diagonal-run occurrences (RECD_BWD_RUNS): see k_runs_detect / k_runs_expand
   uint32_t* head_tag;     // [occ cap] tag of each run head (indexed by the sort's value)
   uint32_t* head_len;     // [occ cap] run length k (rows tag .. tag + k - 1)
-  int64_t* blk_heads;     // [occ blocks] heads per k_occ block -> exclusive prefix
+  int64_t* head_count;    // [nts] run heads per table segment (the heads sort's counts)
+  int64_t* head_off;      // [occ cap] run lengths in sorted order -> exclusive offsets
+  int32_t* fallback;      // set when some ID's runs need per-value occurrences
+  uint32_t* exp_keys;     // expanded occurrences (the scatter's input)
+  uint32_t* exp_vals;
+  const int32_t* occ_gate;              // k_occ runs only if null or *occ_gate != 0
+  int64_t ex_chunk0[RECD_MAX_FEAT];     // k_runs_expand: first RC_EXP chunk of each segment
   int64_t occ_blk0[RECD_MAX_FEAT + 1];  // k_occ: first block of each feature (capacity)
   int64_t oc_ch;                         // k_occ / k_runs: unique values per block
   // optional scatter of grad_u rows to peers (fused source -> owner push): row u
@@ -106,7 +111,11 @@ struct BwdParams {
 __global__ void k_bwd_setup(const __grid_constant__ BwdParams p) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   *p.bad = 0;
-  for (int s = 0; s < p.nts; ++s) p.seg_count[s] = 0;
+  *p.fallback = 0;
+  for (int s = 0; s < p.nts; ++s) {
+    p.seg_count[s] = 0;
+    p.head_count[s] = 0;
+  }
   for (int f = 0; f < p.F; ++f) {
     const int s = p.feat_ts[f];
     p.feat_base[f] = p.seg_count[s];
@@ -334,6 +343,7 @@ constexpr int OC_CH_SMALL = 4096;  // ... and on small ones (more blocks in flig
 constexpr int OC_MAXR = 512;
 __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p, uint32_t* keys,
                                              uint32_t* vals) {
+  if (p.occ_gate && !*(volatile const int32_t*)p.occ_gate) return;  // runs fallback only
   int f = 0;
   while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
   const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * p.oc_ch;
@@ -435,111 +445,36 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
 }
 
 // ---------------------------------------------------------------------------
-// Diagonal-run occurrences.  In session data consecutive unique rows of a
-// history feature are windows shifted by one: the ID at (u, p) is usually the
-// ID at (u - 1, p + 1).  Such a diagonal of occurrences -- one ID in rows u,
-// u + 1, ..., u + k - 1 -- is emitted as ONE sort element (ID, head index)
-// carrying (tag of row u, k), so the occurrence sort handles ~N_ids elements
-// instead of N_u (3.3x fewer at cfg2).  The scatter then adds grad_u rows
-// tag .. tag + k - 1 for each run.
+// Diagonal-run occurrences (RECD_BWD_RUNS=1).  In session data consecutive
+// unique rows of a history feature are windows shifted by one: the ID at
+// (u, p) is usually the ID at (u - 1, p + 1).  A diagonal of occurrences --
+// one ID in rows u .. u + k - 1 at positions p, p - 1, ... -- becomes ONE sort
+// element (ID, head index) carrying (tag of row u, k), so the occurrence sort
+// orders ~N_ids run heads instead of N_u values (3.3x fewer at cfg2), and
+// k_runs_expand writes the per-value (ID, tag) array the scatter reads.
 //
 // Exactness: the oracle adds, per ID, grad_u[t] over its occurrences in
-// ascending (tag, position) order; equal tags add the same row, so any order
-// with non-decreasing tags and the same multiplicities is bit-identical.  Runs
-// only pass through rows that hold no ID twice ("clean" rows, k_runs_dirty),
-// so two runs of one ID never share a row; a row holding an ID twice emits each
-// of its occurrences as its own run of length 1.  Hence an ID's runs are
-// disjoint tag ranges, and the stable sort (input in ascending head tag)
-// delivers them in ascending tag order: concatenating them is exactly the
-// oracle's order.
+// non-decreasing tag order (equal tags add the same row, so their order does
+// not matter).  The expansion sorts each ID's runs by head tag; if no two runs
+// of the ID overlap in tags, concatenating them is exactly that order.  Runs
+// overlap only when a row holds the ID twice; such an ID (or one with more than
+// 32 runs) sets `fallback`, and the batch's occurrences are then rebuilt per
+// value (k_occ + the full sort, gated on the flag) -- slower, never different.
 // ---------------------------------------------------------------------------
-constexpr uint32_t DT_EMPTY = 0xffffffffu;
-constexpr int DT_SLOTS = 1024;  // per-warp hash slots; rows longer than DT_MAXLEN count as dirty
-constexpr int DT_MAXLEN = 512;
-
-// warp per (feature, unique row): does the row hold some ID twice?
-__global__ void __launch_bounds__(256) k_runs_dirty(const __grid_constant__ BwdParams p) {
-  __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
-  __shared__ uint32_t s_tab[8][DT_SLOTS];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int f = 0; f < p.F; ++f) {
-      s_pref[f] = acc;
-      acc += p.counts[f];
-    }
-    s_pref[p.F] = acc;
-  }
-  uint32_t* tab = s_tab[warp];
-  for (int i = lane; i < DT_SLOTS; i += 32) tab[i] = DT_EMPTY;
-  __syncthreads();
-  const int64_t total = s_pref[p.F];
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
-    const int f = find_seg(s_pref, p.F, w);
-    const int64_t u = w - s_pref[f];
-    const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
-    const int64_t* uo = p.uoffsets[f];
-    const int64_t a = uo[u];
-    const int64_t len = ((u + 1 < U) ? uo[u + 1] : NV) - a;
-    bool dup = len > DT_MAXLEN;
-    if (!dup && len > 1) {
-      uint32_t mine[DT_MAXLEN / 32];
-#pragma unroll
-      for (int it = 0; it < DT_MAXLEN / 32; ++it) {
-        mine[it] = DT_EMPTY;
-        const int64_t k = (int64_t)it * 32 + lane;
-        if (k < len) {
-          const int64_t v = __ldg(p.uvalues[f] + a + k);
-          const uint32_t key = (uint32_t)v;
-          if (key == DT_EMPTY || ((uint64_t)v >> 32)) {
-            dup = true;  // outside the 32-bit key space: conservatively dirty
-          } else {
-            uint32_t slot = (key * 2654435761u) >> 22;  // 10 bits
-            while (true) {
-              const uint32_t old = atomicCAS(&tab[slot], DT_EMPTY, key);
-              if (old == DT_EMPTY) {
-                mine[it] = slot;
-                break;
-              }
-              if (old == key) {
-                dup = true;
-                break;
-              }
-              slot = (slot + 1) & (DT_SLOTS - 1);
-            }
-          }
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int it = 0; it < DT_MAXLEN / 32; ++it)
-        if (mine[it] != DT_EMPTY) tab[mine[it]] = DT_EMPTY;
-      __syncwarp();
-    }
-    dup = __any_sync(0xffffffffu, dup);
-    if (lane == 0) p.dirty[(int64_t)f * p.B + u] = dup ? 1 : 0;
-  }
-}
-
 __device__ __forceinline__ int64_t urow_end(const int64_t* uo, int64_t U, int64_t NV, int64_t u) {
   return (u + 1 < U) ? __ldg(uo + u + 1) : NV;
 }
 
 // 0 if the occurrence (u, p) of ID v continues the run of (u - 1, p + 1), else
-// the length k >= 1 of the run it heads (rows u .. u + k - 1, positions p, p - 1, ...)
-__device__ __forceinline__ uint32_t run_head_len(const int64_t* uv, const int64_t* uo,
-                                                 const uint8_t* dirty, int64_t U, int64_t NV,
-                                                 int64_t u, int64_t p, int64_t v, bool want_len) {
-  const bool clean = !dirty[u];
-  if (clean && u >= 1 && !dirty[u - 1]) {
+// the length k >= 1 of the run it heads
+__device__ __forceinline__ uint32_t run_head_len(const int64_t* uv, const int64_t* uo, int64_t U,
+                                                 int64_t NV, int64_t u, int64_t p, int64_t v) {
+  if (u >= 1) {
     const int64_t b = __ldg(uo + u - 1);
     if (b + p + 1 < __ldg(uo + u) && __ldg(uv + b + p + 1) == v) return 0u;
   }
-  if (!want_len || !clean) return 1u;
   uint32_t k = 1;
   for (int64_t j = 1; u + j < U && p - j >= 0; ++j) {
-    if (dirty[u + j]) break;
     const int64_t a = __ldg(uo + u + j);
     if (a + p - j >= urow_end(uo, U, NV, u + j)) break;
     if (__ldg(uv + a + p - j) != v) break;
@@ -548,42 +483,31 @@ __device__ __forceinline__ uint32_t run_head_len(const int64_t* uv, const int64_
   return k;
 }
 
-// value-parallel pass over the unique values (the k_occ block decomposition):
-// EMIT = false counts the run heads of each block into blk_heads; EMIT = true
-// writes (ID, head index) pairs + head (tag, k) at the block's scanned base,
-// in value order (a block-wide scan ranks the heads of each 256-value round).
-template <bool EMIT>
-__global__ void __launch_bounds__(256) k_runs(const __grid_constant__ BwdParams p, uint32_t* keys,
-                                              uint32_t* vals) {
+// value-parallel (the k_occ block decomposition): run heads of a block are
+// written at a block range taken from the segment's head counter (their order
+// inside an ID is restored by the expansion's tag sort)
+__global__ void __launch_bounds__(256) k_runs_detect(const __grid_constant__ BwdParams p,
+                                                     uint32_t* keys, uint32_t* vals) {
   int f = 0;
   while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
   const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * p.oc_ch;
   const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
-  const int tid = threadIdx.x;
-  __shared__ int64_t s_scan[32];
-  if (j0 >= NV) {
-    if (!EMIT && tid == 0) p.blk_heads[blockIdx.x] = 0;
-    return;
-  }
+  if (j0 >= NV) return;
   const int64_t j1 = min(NV, j0 + p.oc_ch);
+  const int tid = threadIdx.x;
   const int64_t* uo = p.uoffsets[f];
   const int64_t* src = p.uvalues[f];
-  const uint8_t* dirty = p.dirty + (int64_t)f * p.B;
-  const uint64_t rows = (uint64_t)p.ts_rows[p.feat_ts[f]];
-  int64_t dst = 0;
-  if (EMIT) {  // the block's first head: segment base + feature base + blocks before it
-    dst = p.ts_base[p.feat_ts[f]] + p.feat_base[f] + p.blk_heads[blockIdx.x] -
-          p.blk_heads[p.occ_blk0[f]];
-  }
-  __shared__ int64_t s_u0;
+  const int ts = p.feat_ts[f];
+  const uint64_t rows = (uint64_t)p.ts_rows[ts];
+  __shared__ int64_t s_u0, s_base;
   __shared__ int64_t s_uo[OC_MAXR + 1];
+  __shared__ int64_t s_scan[32];
   if (tid < 32) {
     const int64_t u = warp_last_le(uo, U, j0, tid);
     if (tid == 0) s_u0 = u;
   }
   __syncthreads();
   int64_t u0 = s_u0;
-  int64_t cnt = 0;
   while (true) {
     const int nr = (int)min((int64_t)OC_MAXR, U - u0);
     for (int t = tid; t <= nr; t += 256) {
@@ -610,16 +534,15 @@ __global__ void __launch_bounds__(256) k_runs(const __grid_constant__ BwdParams 
           while (s_uo[r + 1] <= q) ++r;
         }
         v = __ldg(src + q);
-        k = run_head_len(src, uo, dirty, U, NV, u0 + r, q - s_uo[r], v, EMIT);
-      }
-      if (!EMIT) {
-        cnt += k ? 1 : 0;
-        continue;
+        k = run_head_len(src, uo, U, NV, u0 + r, q - s_uo[r], v);
       }
       int64_t tot;
       const int64_t rank = block_exclusive_scan<256>(k ? 1 : 0, s_scan, &tot);
+      if (tid == 0) s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(p.head_count + ts),
+                                             (unsigned long long)tot) : 0;
+      __syncthreads();
       if (k) {
-        const int64_t o = dst + rank;
+        const int64_t o = p.ts_base[ts] + s_base + rank;
         const bool in = (uint64_t)v < rows;
         if (!in) *p.bad = 1;
         keys[o] = in ? (uint32_t)v : 0u;
@@ -627,32 +550,119 @@ __global__ void __launch_bounds__(256) k_runs(const __grid_constant__ BwdParams 
         p.head_tag[o] = ((uint32_t)f << 24) | (uint32_t)(u0 + r);
         p.head_len[o] = k;
       }
-      dst += tot;
+      __syncthreads();
     }
     if (covered >= j1) break;
     __syncthreads();
     u0 += nr;
   }
-  if (!EMIT) {
-    int64_t tot;
-    block_exclusive_scan<256>(cnt, s_scan, &tot);
-    if (tid == 0) p.blk_heads[blockIdx.x] = tot;
-  }
 }
 
-// after the scan of blk_heads: heads per feature -> feature bases inside its
-// table segment and the segment counts (the sort's element counts)
-__global__ void k_runs_bases(const __grid_constant__ BwdParams p, int64_t total_blocks,
-                             const int64_t* heads_total) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int s = 0; s < p.nts; ++s) p.seg_count[s] = 0;
-  for (int f = 0; f < p.F; ++f) {
-    const int64_t b0 = p.occ_blk0[f], b1 = p.occ_blk0[f + 1];
-    const int64_t end = (b1 < total_blocks) ? p.blk_heads[b1] : *heads_total;
-    const int64_t h = end - p.blk_heads[b0];
-    const int s = p.feat_ts[f];
-    p.feat_base[f] = p.seg_count[s];
-    p.seg_count[s] += h;
+// sorted head j -> its run length (scanned into expanded offsets next)
+__global__ void k_runs_lens(const __grid_constant__ BwdParams p, const uint32_t* svals,
+                            int64_t total_cap) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= total_cap) return;
+  int s = 0;
+  while (s + 1 < p.nts && p.ts_base[s + 1] <= j) ++s;
+  p.head_off[j] = (j - p.ts_base[s] < p.head_count[s]) ? (int64_t)p.head_len[svals[j]] : 0;
+}
+
+// warp per RC_EXP sorted heads: every ID group (run of equal sorted keys)
+// starting in the chunk is written out per value in tag order
+constexpr int RC_EXP = 256;
+__global__ void __launch_bounds__(256) k_runs_expand(const __grid_constant__ BwdParams p,
+                                                     const uint32_t* skeys, const uint32_t* svals,
+                                                     int64_t total_chunks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total_chunks;
+       w += nwarps) {
+    int s = 0;
+    while (s + 1 < p.nts && p.ex_chunk0[s + 1] <= w) ++s;
+    const int64_t n = p.head_count[s];
+    const int64_t lo = (w - p.ex_chunk0[s]) * RC_EXP;
+    if (lo >= n) continue;
+    const int64_t hi = min(n, lo + (int64_t)RC_EXP);
+    const uint32_t* K = skeys + p.ts_base[s];
+    const uint32_t* Vs = svals;                 // head indices are absolute
+    const int64_t* off = p.head_off + p.ts_base[s];
+    uint32_t* ok_ = p.exp_keys + p.ts_base[s];
+    uint32_t* ov_ = p.exp_vals + p.ts_base[s];
+    for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+      const int64_t j = j0 + lane;
+      bool st = false, single = false;
+      uint32_t id = 0;
+      if (j < hi) {
+        id = __ldg(K + j);
+        st = (j == 0) || __ldg(K + j - 1) != id;
+        single = st && (j + 1 == n || __ldg(K + j + 1) != id);
+      }
+      if (single) {  // the common case: the ID has one run -> lane writes it
+        const uint32_t hid = __ldg(Vs + p.ts_base[s] + j);
+        const uint32_t tag = __ldg(p.head_tag + hid), len = __ldg(p.head_len + hid);
+        const int64_t base = off[j];
+        for (uint32_t r = 0; r < len; ++r) {
+          ok_[base + r] = id;
+          ov_[base + r] = tag + r;
+        }
+      }
+      unsigned b = __ballot_sync(0xffffffffu, st && !single);
+      while (b) {  // IDs with several runs: sorted by head tag, checked, written
+        const int src = __ffs(b) - 1;
+        b &= b - 1;
+        const int64_t g = j0 + src;
+        const uint32_t gid = __shfl_sync(0xffffffffu, id, src);
+        const int64_t m = run_end(K, g + 1, n, gid, lane) - g;
+        if (m > 32) {
+          if (lane == 0) *p.fallback = 1;
+          continue;
+        }
+        uint32_t tag = 0xffffffffu, len = 0;
+        if (lane < m) {
+          const uint32_t hid = __ldg(Vs + p.ts_base[s] + g + lane);
+          tag = __ldg(p.head_tag + hid);
+          len = __ldg(p.head_len + hid);
+        }
+#pragma unroll
+        for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+          for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
+            const uint32_t ot = __shfl_xor_sync(0xffffffffu, tag, jj);
+            const uint32_t ol = __shfl_xor_sync(0xffffffffu, len, jj);
+            const bool up = (lane & k2) == 0, lower = (lane & jj) == 0;
+            const bool take = (lower == up) ? ot < tag : ot > tag;
+            if (take) {
+              tag = ot;
+              len = ol;
+            }
+          }
+        }
+        // runs of one ID must not share a row: tag[i + 1] >= tag[i] + len[i]
+        const uint32_t nt = __shfl_down_sync(0xffffffffu, tag, 1);
+        if (__any_sync(0xffffffffu, lane + 1 < m && nt < tag + len)) {
+          if (lane == 0) *p.fallback = 1;
+          continue;
+        }
+        uint32_t incl = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += y;
+        }
+        const uint32_t excl = incl - len;
+        const int64_t base = off[g];
+        for (int h = 0; h < m; ++h) {
+          const uint32_t t0 = __shfl_sync(0xffffffffu, tag, h);
+          const uint32_t l0 = __shfl_sync(0xffffffffu, len, h);
+          const uint32_t e0 = __shfl_sync(0xffffffffu, excl, h);
+          for (uint32_t r = lane; r < l0; r += 32) {
+            ok_[base + e0 + r] = gid;
+            ov_[base + e0 + r] = t0 + r;
+          }
+        }
+      }
+    }
   }
 }
 
@@ -712,7 +722,7 @@ constexpr int SC_BATCH = RECD_SC_BATCH;  // unique-row gradient gathers in fligh
 // per-warp shared ring while grad_u rows (L2-resident) are gathered 8 positions
 // at a time across run boundaries; at each run end the row is updated and
 // stored, and its slot refilled with the row of run r + SC_RS.
-template <class C, bool SINGLE, bool RUNS, int RC>
+template <class C, bool SINGLE, int RC>
 __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid_constant__ BwdParams p) {
   constexpr int V = C::VW;
   __shared__ uint16_t s_starts[8][RC + 2];
@@ -797,114 +807,6 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
     int32_t bnd = (nruns > 1) ? (int32_t)starts[1] : pe;  // end of run r
     float acc[V];
     C::zero(acc);
-    if constexpr (RUNS) {
-      // sorted elements are run heads: K = ID, Vv = head index -> (tag, k); the
-      // occurrences of the chunk's runs are walked flat, SC_BATCH gradient rows
-      // in flight, through a window of 32 heads (lane i: head wb + i, its tag,
-      // length and inclusive length prefix)
-      int32_t wb = 0;
-      uint32_t wt = 0, wl = 0, wi = 0, wtot = 0;
-      bool wg = false;  // lane's head is the last of its ID (run) group
-      const uint32_t* Kl = K + lo;
-      auto load_win = [&](int32_t b) {
-        wb = b;
-        wt = 0;
-        wl = 0;
-        wg = false;
-        if (b + lane < pe) {
-          const uint32_t hid = __ldg(Vl + b + lane);
-          wt = __ldg(p.head_tag + hid);
-          wl = __ldg(p.head_len + hid);
-          wg = (b + lane + 1 == pe) || __ldg(Kl + b + lane + 1) != __ldg(Kl + b + lane);
-        }
-        wi = wl;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
-          if (lane >= d) wi += y;
-        }
-        wtot = __shfl_sync(0xffffffffu, wi, 31);
-      };
-      load_win(starts[0]);
-      uint32_t o = 0, obase = 0;
-      bool more = true;
-      float x[SC_BATCH][V];
-      while (more) {
-        uint32_t vmask = 0, dmask = 0;  // occurrence t valid / completes its run
-#pragma unroll
-        for (int t = 0; t < SC_BATCH; ++t) {
-          if (more && o >= obase + wtot) {  // past the window: the next 32 heads
-            if (wb + 32 >= pe) {
-              more = false;
-            } else {
-              obase += wtot;
-              load_win(wb + 32);
-            }
-          }
-          if (more) {
-            const uint32_t rel = o - obase;
-            const int h = __popc(__ballot_sync(0xffffffffu, wi <= rel));
-            const uint32_t before = __shfl_sync(0xffffffffu, wi, max(h - 1, 0));
-            const uint32_t tagh = __shfl_sync(0xffffffffu, wt, h);
-            const uint32_t lenh = __shfl_sync(0xffffffffu, wl, h);
-            const bool gend = __shfl_sync(0xffffffffu, wg, h);
-            const uint32_t off = rel - (h ? before : 0u);
-            const uint32_t tag = tagh + off;
-            vmask |= 1u << t;
-            if (gend && off + 1 == lenh) dmask |= 1u << t;
-            const float* gp = (SINGLE ? gs : p.grow[tag >> 24] + lo_f) + (uint64_t)(tag & 0xffffffu) * D32;
-            if constexpr (HINT && RECD_SCATTER_L2 >= 2) {
-              if (C::FULL || ok) {
-                const float4 q = ld_v4_hint(gp, pol_keep);
-                x[t][0] = q.x; x[t][1] = q.y; x[t][2] = q.z; x[t][3] = q.w;
-              } else {
-                C::zero(x[t]);
-              }
-            } else {
-              C::ld(gp, ok, x[t]);
-            }
-            ++o;
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < SC_BATCH; ++t) {
-          if (vmask & (1u << t)) {
-#pragma unroll
-            for (int e = 0; e < V; ++e) acc[e] = __fadd_rn(acc[e], x[t][e]);
-            if (dmask & (1u << t)) {  // run r complete (warp-uniform)
-              const uint32_t id = rids[r];
-              if (apply) {
-                cp_async_wait<SC_RS - 1>();
-                float* slot = ring + (r % SC_RS) * C::CB;
-                float wv[V];
-#pragma unroll
-                for (int e = 0; e < V; ++e) wv[e] = __fsub_rn(slot[e], __fmul_rn(p.lr, acc[e]));
-                if constexpr (HINT) {
-                  if (C::FULL || ok)
-                    st_v4_hint(table + (uint64_t)id * D32, wv[0], wv[1], wv[2], wv[3], pol_stream);
-                  if (r + SC_RS < nruns && ok)
-                    cp_async16_hint(slot, table + (uint64_t)rids[r + SC_RS] * D32, pol_stream);
-                } else {
-                  C::st(table + (uint64_t)id * D32, ok, wv);
-                  if (r + SC_RS < nruns && ok)
-                    cp_async<V * 4>(slot, table + (uint64_t)rids[r + SC_RS] * D32);
-                }
-                cp_async_commit();
-              } else {
-                const int64_t ri = run_base + r;
-                if (lo_f == 0) p.grad_ids[s][ri] = (int64_t)id;
-                C::st(p.grad_rows[s] + ri * p.D + lo_f, ok, acc);
-              }
-              ++r;
-              C::zero(acc);
-            }
-          }
-        }
-      }
-      if (apply) cp_async_wait<0>();
-      __syncwarp();
-      continue;
-    }
 #if RECD_SC_PIPE
     // software-pipelined: the gradient rows of the next SC_BATCH positions are
     // in flight while the current SC_BATCH are reduced (the gathers, not the
@@ -1126,9 +1028,9 @@ Plan make_plan(int F, const int64_t* const* inverse, float* const* tables, const
 struct BwdScratch {
   int64_t *feat_base, *seg_count, *is_count, *run_part, *scan_part;
   int32_t* bad;
-  uint8_t* dirty;
   uint32_t *head_tag, *head_len;
-  int64_t *blk_heads, *heads_total, *runs_scan_part;
+  int64_t *head_count, *head_off, *runs_scan_part;
+  int32_t* fallback;
   uint32_t *inv_k0, *inv_v0, *inv_k1, *inv_v1, *hist;
   int32_t* csr_start;
   float* grad_u;
@@ -1153,19 +1055,18 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   s->csr_start = a.take<int32_t>((need & NEED_INV) ? (size_t)std::max(pl.nis, 1) * (B + 1) : 1);
   s->grad_u = a.take<float>((need & NEED_GRADU) ? (size_t)pl.F * B * D : 1);
   const size_t occ = (need & NEED_OCC) ? (size_t)pl.occ_total : 1;
-  // diagonal runs: row flags, head (tag, length), per-k_occ-block head counts
-  // (only the full backward can use runs: its row count B is known to the
-  // scratch-size query; the owner-side sparse SGD's is not)
+  // diagonal runs: head (tag, length), head counts per segment, the heads'
+  // expanded offsets (only the full backward uses runs)
   const bool rn = (need & NEED_OCC) && (need & NEED_GRADU);
-  const int64_t ob = rn ? ceil_div(pl.occ_total, OC_CH_SMALL) + pl.F + 1 : 1;
-  s->dirty = a.take<uint8_t>(rn ? (size_t)pl.F * B : 1);
   s->head_tag = a.take<uint32_t>(rn ? occ : 1);
   s->head_len = a.take<uint32_t>(rn ? occ : 1);
-  s->blk_heads = a.take<int64_t>(ob);
-  s->heads_total = a.take<int64_t>(1);
+  s->head_off = a.take<int64_t>(rn ? occ : 1);
+  s->head_count = a.take<int64_t>(RECD_MAX_FEAT);
+  s->fallback = a.take<int32_t>(1);
   {
-    ScanDesc d{nullptr, nullptr, ob, nullptr, nullptr};
-    s->runs_scan_part = a.take<int64_t>(std::max<int64_t>(scan_part_words(&d, 1), 1));
+    std::vector<ScanDesc> d;
+    for (int t = 0; t < pl.nts; ++t) d.push_back({nullptr, nullptr, rn ? pl.ts_cap[t] : 1, nullptr, nullptr});
+    s->runs_scan_part = a.take<int64_t>(std::max<int64_t>(scan_part_words(d.data(), (int)d.size()), 1));
   }
   s->occ_k0 = a.take<uint32_t>(occ);
   s->occ_v0 = a.take<uint32_t>(occ);
@@ -1200,7 +1101,7 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
 //   scatter : occurrences -> sort -> scatter, reading caller unique-row grads
 enum class BwdMode { Full, GradOnly, ScatterOnly };
 
-// Occurrences as diagonal runs (k_runs_*) instead of one sort element per
+// Occurrences as diagonal runs (k_runs_detect / _expand) instead of one sort element per
 // unique value.  Exact and 2.2x cheaper to sort at cfg2, but the run
 // detection (0.57 ms) + clean-row check (0.29 ms) + the scatter's run walk
 // (+0.8 ms) cost more than the sort saves (0.45 ms): step 5.93 vs 4.93 ms
@@ -1322,10 +1223,11 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   p.csr_start = sc.csr_start;
   p.run_part = sc.run_part;
   p.bad = sc.bad;
-  p.dirty = sc.dirty;
   p.head_tag = sc.head_tag;
   p.head_len = sc.head_len;
-  p.blk_heads = sc.blk_heads;
+  p.head_off = sc.head_off;
+  p.head_count = sc.head_count;
+  p.fallback = sc.fallback;
   const bool runs = bm == BwdMode::Full && do_scatter && use_runs();
 
   const bool prep = (phase & PH_PREP) != 0, fin = (phase & PH_FINISH) != 0;
@@ -1336,8 +1238,13 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   for (int s = 0; s < pl.nts; ++s) maxrows = std::max(maxrows, pl.table_rows[s]);
   p.inv_keys = odd_passes(bits_for(B)) ? sc.inv_k1 : sc.inv_k0;
   p.inv_rows = odd_passes(bits_for(B)) ? sc.inv_v1 : sc.inv_v0;
-  p.occ_keys = odd_passes(bits_for(maxrows)) ? sc.occ_k1 : sc.occ_k0;
-  p.occ_vals = odd_passes(bits_for(maxrows)) ? sc.occ_v1 : sc.occ_v0;
+  const bool odd = odd_passes(bits_for(maxrows));
+  // the scatter's sorted occurrences: per-value sort result, or with runs the
+  // expansion's output (the buffer pair the heads sort did not end in)
+  p.occ_keys = (odd != runs) ? sc.occ_k1 : sc.occ_k0;
+  p.occ_vals = (odd != runs) ? sc.occ_v1 : sc.occ_v0;
+  p.exp_keys = p.occ_keys;
+  p.exp_vals = p.occ_vals;
 
   // ---- prepare: everything that depends on the IKJT only (no gradient)
   if (prep) {
@@ -1367,17 +1274,48 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       }
       p.occ_blk0[F] = ob;
       if (runs) {
-        // clean rows -> run heads per block -> block bases -> heads written in
-        // value order (the stable sort then keeps each ID's runs in tag order)
-        const unsigned gd = (unsigned)std::min<int64_t>(ceil_div((int64_t)F * B, 8),
-                                                        (int64_t)num_sms() * 8);
-        k_runs_dirty<<<std::max(gd, 1u), 256, 0, stream>>>(p);
-        k_runs<false><<<(unsigned)ob, 256, 0, stream>>>(p, nullptr, nullptr);
-        ScanDesc d{sc.blk_heads, sc.blk_heads, ob, nullptr, sc.heads_total};
-        int rs = seg_exclusive_scan(&d, 1, sc.runs_scan_part, stream);
-        if (rs != RECD_OK) return rs;
-        k_runs_bases<<<1, 32, 0, stream>>>(p, ob, sc.heads_total);
-        k_runs<true><<<(unsigned)ob, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
+        // 1. run heads (ID, head index) + (tag, k), per table segment
+        k_runs_detect<<<(unsigned)ob, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
+        std::vector<SegDesc> hs;
+        for (int s = 0; s < pl.nts; ++s) hs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.head_count + s});
+        bool halt = false;
+        int r1 = seg_sort_pairs(hs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
+                                sc.occ_k1, sc.occ_v1, sc.hist, &halt, stream);
+        if (r1 != RECD_OK) return r1;
+        uint32_t* Hk = halt ? sc.occ_k1 : sc.occ_k0;
+        uint32_t* Hv = halt ? sc.occ_v1 : sc.occ_v0;
+        // 2. run lengths in sorted order -> expanded offsets per segment
+        k_runs_lens<<<(unsigned)ceil_div(pl.occ_total, 256), 256, 0, stream>>>(p, Hv, pl.occ_total);
+        std::vector<ScanDesc> sd;
+        for (int s = 0; s < pl.nts; ++s)
+          sd.push_back({sc.head_off + pl.ts_base[s], sc.head_off + pl.ts_base[s], pl.ts_cap[s],
+                        sc.head_count + s, nullptr});
+        int r2 = seg_exclusive_scan(sd.data(), (int)sd.size(), sc.runs_scan_part, stream);
+        if (r2 != RECD_OK) return r2;
+        // 3. per-value occurrences in (ID, tag) order into the other buffer pair
+        int64_t ec = 0;
+        for (int s = 0; s < pl.nts; ++s) {
+          p.ex_chunk0[s] = ec;
+          ec += std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RC_EXP));
+        }
+        const unsigned ge = (unsigned)std::min<int64_t>(ceil_div(ec, 8), (int64_t)num_sms() * 16);
+        k_runs_expand<<<std::max(ge, 1u), 256, 0, stream>>>(p, Hk, Hv, ec);
+        // 4. fallback (an ID whose runs share a row, or > 32 runs): per-value
+        //    occurrences + the full sort, gated on the flag; the sort is set up
+        //    so that its result lands in the expansion's buffers
+        uint32_t* Xk = odd ? Hk : p.exp_keys;
+        uint32_t* Xv = odd ? Hv : p.exp_vals;
+        uint32_t* Yk = odd ? p.exp_keys : Hk;
+        uint32_t* Yv = odd ? p.exp_vals : Hv;
+        BwdParams q = p;
+        q.occ_gate = sc.fallback;
+        k_occ<<<(unsigned)ob, 256, 0, stream>>>(q, Xk, Xv);
+        std::vector<SegDesc> vs;
+        for (int s = 0; s < pl.nts; ++s) vs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
+        bool valt = false;
+        int r3 = seg_sort_pairs(vs.data(), pl.nts, (int)bits_for(maxrows), Xk, Xv, Yk, Yv, sc.hist,
+                                &valt, stream, sc.fallback);
+        if (r3 != RECD_OK) return r3;
         note_launch(4);
       } else {
         k_occ<<<(unsigned)ob, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
@@ -1442,28 +1380,16 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       const unsigned g2 =
           (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks * ncb, 8), (int64_t)num_sms() * 16);
       hook_before("k_scatter", stream);
-      if (runs) {
-        if (pl.rc == RC_BIG) {
-          if (single)
-            k_scatter<C, true, true, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
-          else
-            k_scatter<C, false, true, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
-        } else {
-          if (single)
-            k_scatter<C, true, true, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
-          else
-            k_scatter<C, false, true, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
-        }
-      } else if (pl.rc == RC_BIG) {
+      if (pl.rc == RC_BIG) {
         if (single)
-          k_scatter<C, true, false, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          k_scatter<C, true, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
         else
-          k_scatter<C, false, false, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          k_scatter<C, false, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
       } else {
         if (single)
-          k_scatter<C, true, false, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          k_scatter<C, true, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
         else
-          k_scatter<C, false, false, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          k_scatter<C, false, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
       }
       hook_after("k_scatter", stream);
       note_launch();

@@ -60,7 +60,12 @@ struct OsParams {
   int64_t* tile0;      // [S + 1] prefix of actual tiles
   uint32_t* counters;  // [OS_MAXPASS] tile tickets
   uint32_t* status;    // [2][total_tcap][256]
+  const int32_t* gate; // nullable: run only if *gate != 0
 };
+
+__device__ __forceinline__ bool os_gated_off(const OsParams& p) {
+  return p.gate && *(volatile const int32_t*)p.gate == 0;
+}
 
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
@@ -72,6 +77,7 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
 }
 
 __global__ void __launch_bounds__(OS_NT) k_os_hist(const __grid_constant__ OsParams p) {
+  if (os_gated_off(p)) return;
   const int64_t chunk = blockIdx.x;
   int s = 0;
   while (s + 1 < p.S && p.seg[s + 1].hchunk0 <= chunk) ++s;
@@ -114,6 +120,7 @@ __global__ void __launch_bounds__(OS_NT) k_os_hist(const __grid_constant__ OsPar
 
 // block per (segment, pass): exclusive digit scan; block 0 also the tile prefix
 __global__ void __launch_bounds__(OS_NT) k_os_setup(const __grid_constant__ OsParams p) {
+  if (os_gated_off(p)) return;
   __shared__ int64_t s_scan[32];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     int64_t t = 0;
@@ -135,6 +142,7 @@ __global__ void __launch_bounds__(OS_NT) k_os_setup(const __grid_constant__ OsPa
 #define RECD_OS_MINB 3
 #endif
 __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_constant__ OsParams p) {
+  if (os_gated_off(p)) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t mask = (1u << p.nbits) - 1u;
   const unsigned lt = lanemask_lt();
@@ -306,7 +314,7 @@ static int os_grid() {
 
 int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_t* vals,
                    uint32_t* keys_alt, uint32_t* vals_alt, uint32_t* hist, bool* in_alt,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, const int32_t* gate) {
   *in_alt = false;
   if (S <= 0 || bits <= 0) return RECD_OK;
   const int npass = (bits + 7) / 8;
@@ -318,6 +326,7 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
     build_os_params(segs + s0, std::min(OS_MAXSEG, S - s0), &p);
     p.npass = npass;
     p.bits = bits;
+    p.gate = gate;
     p.ghist = hist;
     p.tile0 = reinterpret_cast<int64_t*>(hist + (int64_t)OS_MAXSEG * OS_MAXPASS * 256);
     p.counters = reinterpret_cast<uint32_t*>(p.tile0 + OS_MAXSEG + 1);

@@ -20,9 +20,10 @@ struct SegDesc {
 // back only if an odd number of passes ran: *in_alt tells where it is).
 // hist scratch: sort_hist_words(...) uint32 words.
 int64_t sort_hist_words(const SegDesc* segs, int S);
+// gate (device, nullable): the sort's kernels do nothing unless *gate != 0
 int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_t* vals,
                    uint32_t* keys_alt, uint32_t* vals_alt, uint32_t* hist, bool* in_alt,
-                   cudaStream_t stream);
+                   cudaStream_t stream, const int32_t* gate = nullptr);
 
 struct ScanDesc {
   const int64_t* in;
