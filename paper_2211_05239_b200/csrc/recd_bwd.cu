@@ -18,6 +18,7 @@
 //                    prefetches the table rows of 4 runs at a time, reduces each
 //                    run in order and RMWs the row (or emits a sparse gradient row).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <vector>
@@ -558,14 +559,14 @@ __global__ void __launch_bounds__(256) k_runs_detect(const __grid_constant__ Bwd
   }
 }
 
-// sorted head j -> its run length (scanned into expanded offsets next)
-__global__ void k_runs_lens(const __grid_constant__ BwdParams p, const uint32_t* svals,
-                            int64_t total_cap) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= total_cap) return;
-  int s = 0;
-  while (s + 1 < p.nts && p.ts_base[s + 1] <= j) ++s;
-  p.head_off[j] = (j - p.ts_base[s] < p.head_count[s]) ? (int64_t)p.head_len[svals[j]] : 0;
+// sorted head j of segment blockIdx.y -> its run length (scanned into expanded
+// offsets next); grid-stride over the segment's device head count
+__global__ void k_runs_lens(const __grid_constant__ BwdParams p, const uint32_t* svals) {
+  const int s = blockIdx.y;
+  const int64_t n = p.head_count[s], base = p.ts_base[s];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    p.head_off[base + j] = (int64_t)p.head_len[svals[base + j]];
 }
 
 // warp per RC_EXP sorted heads: every ID group (run of equal sorted keys)
@@ -1285,7 +1286,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         uint32_t* Hk = halt ? sc.occ_k1 : sc.occ_k0;
         uint32_t* Hv = halt ? sc.occ_v1 : sc.occ_v0;
         // 2. run lengths in sorted order -> expanded offsets per segment
-        k_runs_lens<<<(unsigned)ceil_div(pl.occ_total, 256), 256, 0, stream>>>(p, Hv, pl.occ_total);
+        k_runs_lens<<<dim3((unsigned)num_sms() * 2, (unsigned)pl.nts), 256, 0, stream>>>(p, Hv);
         std::vector<ScanDesc> sd;
         for (int s = 0; s < pl.nts; ++s)
           sd.push_back({sc.head_off + pl.ts_base[s], sc.head_off + pl.ts_base[s], pl.ts_cap[s],
@@ -1320,13 +1321,13 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       } else {
         k_occ<<<(unsigned)ob, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
         note_launch();
+        std::vector<SegDesc> segs;
+        for (int s = 0; s < pl.nts; ++s) segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
+        bool alt = false;
+        int r2 = seg_sort_pairs(segs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
+                                sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream);
+        if (r2 != RECD_OK) return r2;
       }
-      std::vector<SegDesc> segs;
-      for (int s = 0; s < pl.nts; ++s) segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
-      bool alt = false;
-      int r2 = seg_sort_pairs(segs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
-                              sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream);
-      if (r2 != RECD_OK) return r2;
     }
   }
   if (!fin) {
