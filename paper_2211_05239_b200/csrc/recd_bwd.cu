@@ -1102,12 +1102,11 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
 //   scatter : occurrences -> sort -> scatter, reading caller unique-row grads
 enum class BwdMode { Full, GradOnly, ScatterOnly };
 
-// Occurrences as diagonal runs (k_runs_detect / _expand) instead of one sort element per
-// unique value.  Exact and 2.2x cheaper to sort at cfg2, but the run
-// detection (0.57 ms) + clean-row check (0.29 ms) + the scatter's run walk
-// (+0.8 ms) cost more than the sort saves (0.45 ms): step 5.93 vs 4.93 ms
-// (profiles/r2_runs_ab.txt), so it is off by default.  RECD_BWD_RUNS=1 in the
-// environment (read per call) selects it.
+// Occurrences as diagonal runs (k_runs_detect / _expand) instead of one sort
+// element per unique value: exact, but slower at cfg2 (detection + expansion
+// cost more than the smaller sort saves, and rows that repeat an ID trigger the
+// per-value fallback), so it is off by default.  RECD_BWD_RUNS=1
+// in the environment (read per call) selects it.
 #ifndef RECD_BWD_RUNS
 #define RECD_BWD_RUNS 0
 #endif
