@@ -99,6 +99,8 @@ struct BwdParams {
   uint32_t* exp_keys;     // expanded occurrences (the scatter's input)
   uint32_t* exp_vals;
   const int32_t* occ_gate;              // k_occ runs only if null or *occ_gate != 0
+  uint32_t* occ_hist;                   // k_occ: add the sort's digit counts here (or null)
+  int occ_bits;                         //        over this many key bits
   int64_t ex_chunk0[RECD_MAX_FEAT];     // k_runs_expand: first RC_EXP chunk of each segment
   int64_t occ_blk0[RECD_MAX_FEAT + 1];  // k_occ: first block of each feature (capacity)
   int64_t oc_ch;                         // k_occ / k_runs: unique values per block
@@ -358,6 +360,14 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
   const uint64_t rows = (uint64_t)p.ts_rows[p.feat_ts[f]];
   __shared__ int64_t s_u0;
   __shared__ int64_t s_uo[OC_MAXR + 1];
+  // digit counts of every radix pass of the occurrence sort (the sort then
+  // skips reading the keys once more for its histogram)
+  __shared__ uint32_t s_hist[SORT_HIST_PASSES][256];
+  uint32_t* const hist = p.occ_hist;
+  const int npass = hist ? (p.occ_bits + 7) / 8 : 0;
+  if (hist) {
+    for (int i = tid; i < SORT_HIST_PASSES * 256; i += 256) (&s_hist[0][0])[i] = 0u;
+  }
   if (tid < 32) {
     const int64_t u = warp_last_le(uo, U, j0, tid);
     if (tid == 0) s_u0 = u;
@@ -407,7 +417,9 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
           if (q < qb) {
             const bool in = (uint64_t)id[k] < rows;
             if (!in) *p.bad = 1;
-            keys[dst + q] = in ? (uint32_t)id[k] : 0u;
+            const uint32_t key = in ? (uint32_t)id[k] : 0u;
+            keys[dst + q] = key;
+            for (int ps = 0; ps < npass; ++ps) atomicAdd(&s_hist[ps][(key >> (8 * ps)) & 255u], 1u);
             vals[dst + q] = ((uint32_t)f << 24) | (uint32_t)(u0 + row[k]);
           }
         }
@@ -436,12 +448,22 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
       // must not address the table: flag it, and the scatter skips every update
       const bool in = (uint64_t)id < rows;
       if (!in) *p.bad = 1;
-      keys[dst + q] = in ? (uint32_t)id : 0u;
+      const uint32_t key = in ? (uint32_t)id : 0u;
+      keys[dst + q] = key;
+      for (int ps = 0; ps < npass; ++ps) atomicAdd(&s_hist[ps][(key >> (8 * ps)) & 255u], 1u);
       vals[dst + q] = ((uint32_t)f << 24) | (uint32_t)(u0 + r);
     }
     if (covered >= j1) break;
     __syncthreads();
     u0 += nr;
+  }
+  if (hist) {  // the block's digit counts into the sort's histogram
+    __syncthreads();
+    const int64_t row0 = (int64_t)p.feat_ts[f] * SORT_HIST_PASSES * 256;
+    for (int i = tid; i < npass * 256; i += 256) {
+      const uint32_t c = (&s_hist[0][0])[i];
+      if (c) atomicAdd(&hist[row0 + i], c);
+    }
   }
 }
 
@@ -710,6 +732,9 @@ constexpr int SC_RS = RECD_SC_RS;  // table rows prefetched ahead per warp (shar
 #endif
 #ifndef RECD_SC_REV
 #define RECD_SC_REV 0
+#endif
+#ifndef RECD_OCC_HIST  // k_occ counts the occurrence sort's digits (no k_os_hist pass)
+#define RECD_OCC_HIST 1
 #endif
 #ifndef RECD_SC_BATCH
 #define RECD_SC_BATCH 6
@@ -1318,13 +1343,23 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         if (r3 != RECD_OK) return r3;
         note_launch(4);
       } else {
-        k_occ<<<(unsigned)ob, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
+        // k_occ counts the sort's digits as it writes the keys (no histogram
+        // pass over the keys in the sort)
+        const bool fuse = RECD_OCC_HIST && pl.nts <= RECD_MAX_FEAT;
+        if (fuse) {
+          int rh = sort_hist_clear(pl.nts, sc.hist, stream);
+          if (rh != RECD_OK) return rh;
+        }
+        BwdParams q = p;
+        q.occ_hist = fuse ? sc.hist : nullptr;
+        q.occ_bits = (int)bits_for(maxrows);
+        k_occ<<<(unsigned)ob, 256, 0, stream>>>(q, sc.occ_k0, sc.occ_v0);
         note_launch();
         std::vector<SegDesc> segs;
         for (int s = 0; s < pl.nts; ++s) segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
         bool alt = false;
         int r2 = seg_sort_pairs(segs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
-                                sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream);
+                                sc.occ_k1, sc.occ_v1, sc.hist, &alt, stream, nullptr, fuse);
         if (r2 != RECD_OK) return r2;
       }
     }

@@ -314,7 +314,7 @@ static int os_grid() {
 
 int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_t* vals,
                    uint32_t* keys_alt, uint32_t* vals_alt, uint32_t* hist, bool* in_alt,
-                   cudaStream_t stream, const int32_t* gate) {
+                   cudaStream_t stream, const int32_t* gate, bool hist_ready) {
   *in_alt = false;
   if (S <= 0 || bits <= 0) return RECD_OK;
   const int npass = (bits + 7) / 8;
@@ -331,11 +331,21 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
     p.tile0 = reinterpret_cast<int64_t*>(hist + (int64_t)OS_MAXSEG * OS_MAXPASS * 256);
     p.counters = reinterpret_cast<uint32_t*>(p.tile0 + OS_MAXSEG + 1);
     p.status = p.counters + 64;
-    RECD_CUDA_CHECK(cudaMemsetAsync(p.ghist, 0, sizeof(uint32_t) * p.S * OS_MAXPASS * 256, stream));
     p.kin = keys;
-    k_os_hist<<<(unsigned)p.total_hchunks, OS_NT, 0, stream>>>(p);
-    k_os_setup<<<p.S * npass, OS_NT, 0, stream>>>(p);
-    note_launch(2);
+    if (hist_ready && S <= OS_MAXSEG) {
+      // the producer of the keys already counted every pass's digits into
+      // ghist (sort_hist_clear + its own smem histograms): only the ticket
+      // counters and the first pass's tile status words need clearing
+      RECD_CUDA_CHECK(cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * OS_MAXPASS, stream));
+      RECD_CUDA_CHECK(cudaMemsetAsync(p.status, 0, sizeof(uint32_t) * p.total_tcap * 256, stream));
+      k_os_setup<<<p.S * npass, OS_NT, 0, stream>>>(p);
+      note_launch(1);
+    } else {
+      RECD_CUDA_CHECK(cudaMemsetAsync(p.ghist, 0, sizeof(uint32_t) * p.S * OS_MAXPASS * 256, stream));
+      k_os_hist<<<(unsigned)p.total_hchunks, OS_NT, 0, stream>>>(p);
+      k_os_setup<<<p.S * npass, OS_NT, 0, stream>>>(p);
+      note_launch(2);
+    }
     uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
     for (int pass = 0; pass < npass; ++pass) {
       p.pass = pass;
@@ -350,6 +360,12 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
   }
   *in_alt = (npass % 2) == 1;
   RECD_LAUNCH_CHECK();
+  return RECD_OK;
+}
+
+int sort_hist_clear(int S, uint32_t* hist, cudaStream_t stream) {
+  RECD_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * std::min(S, OS_MAXSEG) * OS_MAXPASS * 256,
+                                  stream));
   return RECD_OK;
 }
 

@@ -20,10 +20,15 @@ struct SegDesc {
 // back only if an odd number of passes ran: *in_alt tells where it is).
 // hist scratch: sort_hist_words(...) uint32 words.
 int64_t sort_hist_words(const SegDesc* segs, int S);
-// gate (device, nullable): the sort's kernels do nothing unless *gate != 0
+// gate (device, nullable): the sort's kernels do nothing unless *gate != 0.
+// hist_ready: the keys' producer already added every pass's digit counts of
+// segment s into hist[(s * 4 + pass) * 256 + digit] (after sort_hist_clear),
+// so the sort skips its own histogram read of the keys.
 int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_t* vals,
                    uint32_t* keys_alt, uint32_t* vals_alt, uint32_t* hist, bool* in_alt,
-                   cudaStream_t stream, const int32_t* gate = nullptr);
+                   cudaStream_t stream, const int32_t* gate = nullptr, bool hist_ready = false);
+int sort_hist_clear(int S, uint32_t* hist, cudaStream_t stream);
+constexpr int SORT_HIST_PASSES = 4;  // hist row stride: passes per segment
 
 struct ScanDesc {
   const int64_t* in;

@@ -26,6 +26,9 @@ V = {
     "oslb16": ["RECD_OS_LB=16"],
     "notma": ["RECD_RS_TMA=0"],
     "rsm5": ["RECD_RS_MINB=5"],
+    "nohist": ["RECD_OCC_HIST=0"],
+    "sl1": ["RECD_SCATTER_L2=1"],
+    "sl0": ["RECD_SCATTER_L2=0"],
     "rsm6": ["RECD_RS_MINB=6"],
     "ca2": ["RECD_RING_CA=1"],
     "ca1m3": ["RECD_RING_CA=1", "RECD_RING_K=1"],
