@@ -100,6 +100,8 @@ struct BwdParams {
   uint32_t* exp_vals;
   const int32_t* occ_gate;              // k_occ runs only if null or *occ_gate != 0
   uint32_t* occ_hist;                   // k_occ: add the sort's digit counts here (or null)
+  uint64_t gu_mask;                     // k_grad_u(_flat): features to reduce (bit f)
+  int64_t sc_chunk_lo, sc_chunk_hi;     // k_scatter: chunk window [lo, hi) of this launch
   int occ_bits;                         //        over this many key bits
   int64_t ex_chunk0[RECD_MAX_FEAT];     // k_runs_expand: first RC_EXP chunk of each segment
   int64_t occ_blk0[RECD_MAX_FEAT + 1];  // k_occ: first block of each feature (capacity)
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
     int64_t acc = 0;
     for (int f = 0; f < p.F; ++f) {
       s_pref[f] = acc;
-      if (!RECD_GU_FLAT || p.feat_is[f] < 0) acc += p.counts[f] * ncb;
+      if ((!RECD_GU_FLAT || p.feat_is[f] < 0) && ((p.gu_mask >> f) & 1ull)) acc += p.counts[f] * ncb;
     }
     s_pref[p.F] = acc;
   }
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(256, RECD_GUF_MINB) k_grad_u_flat(const __grid
     int64_t acc = 0;
     for (int f = 0; f < p.F; ++f) {
       s_pref[f] = acc;
-      if (p.feat_is[f] >= 0) acc += nch * ncb;
+      if (p.feat_is[f] >= 0 && ((p.gu_mask >> f) & 1ull)) acc += nch * ncb;
     }
     s_pref[p.F] = acc;
   }
@@ -758,7 +760,7 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   const int ncb = col_blocks<C>(p.D);
-  const int64_t total = p.total_rc_chunks * ncb;
+  const int64_t total = (p.sc_chunk_hi - p.sc_chunk_lo) * ncb;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   if (*(volatile const int32_t*)p.bad) return;  // out-of-range ID in the batch: no update
   uint16_t* starts = s_starts[warp];
@@ -769,11 +771,11 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   const uint64_t pol_stream = HINT ? l2_evict_first() : 0;
   const uint64_t pol_keep = (HINT && RECD_SCATTER_L2 >= 2) ? l2_evict_last() : 0;
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
-    const int64_t wc = (ncb == 1) ? w : w / ncb;
+    const int64_t wc = ((ncb == 1) ? w : w / ncb) + p.sc_chunk_lo;
     // RECD_SC_REV: last table segment first -- k_grad_u_flat wrote the unique-row
     // gradients in feature order, so the last features' are still in L2
-    const int64_t chunk = RECD_SC_REV ? p.total_rc_chunks - 1 - wc : wc;
-    const int lo_f = (int)(w - wc * ncb) * C::CB + lane * V;  // this lane's first float
+    const int64_t chunk = RECD_SC_REV ? p.sc_chunk_hi - 1 - (wc - p.sc_chunk_lo) : wc;
+    const int lo_f = (int)(w - (wc - p.sc_chunk_lo) * ncb) * C::CB + lane * V;  // this lane's first float
     const bool ok = lo_f < p.D;
     const uint32_t D32 = (uint32_t)p.D;
     const int s = rc_seg(p, chunk);
@@ -1371,7 +1373,23 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   // ---- finish: gradient-dependent work
   if (do_scatter && !apply_sgd)
     RECD_CUDA_CHECK(cudaMemsetAsync(grad_counts_out, 0, sizeof(int64_t) * F, stream));
-  int rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, RECD_BWD_FULLOK, {
+  // Fused SGD: unique-row gradients and the scatter may run in groups of
+  // table segments (RECD_SC_GROUP env: segments per group), so a group's
+  // gradients are still in L2 when its scatter gathers them.
+  int group = 0;
+  if (const char* e = getenv("RECD_SC_GROUP")) group = atoi(e);
+  if (!(do_grad && do_scatter && apply_sgd) || group <= 0 || group >= pl.nts) group = pl.nts;
+  int rc = RECD_OK;
+  for (int s0 = 0; s0 < pl.nts && rc == RECD_OK; s0 += group) {
+    const int s1 = std::min(pl.nts, s0 + group);
+    uint64_t mask = 0;
+    for (int f = 0; f < F; ++f)
+      if (pl.feat_ts[f] >= s0 && pl.feat_ts[f] < s1) mask |= 1ull << f;
+    if (group == pl.nts) mask = ~0ull;
+    p.gu_mask = mask;
+    p.sc_chunk_lo = pl.ts_chunk0[s0];
+    p.sc_chunk_hi = s1 < pl.nts ? pl.ts_chunk0[s1] : pl.rc_chunks;
+    rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, RECD_BWD_FULLOK, {
     const int ncb = col_blocks<C>(dim);
     // 2. unique-row gradients
     if (do_grad) {
@@ -1397,7 +1415,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     }
     // 5. sorted scatter-add (+ fused SGD)
     if (do_scatter) {
-      if (!apply_sgd) {
+      if (!apply_sgd && s0 == 0) {
         if (pl.rc == RC_BIG)
           k_run_count<RC_BIG><<<(unsigned)pl.rc_chunks, RC_BIG, 0, stream>>>(p);
         else
@@ -1413,7 +1431,8 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         if (r3 != RECD_OK) return r3;
       }
       const unsigned g2 =
-          (unsigned)std::min<int64_t>(ceil_div(pl.rc_chunks * ncb, 8), (int64_t)num_sms() * 16);
+          (unsigned)std::min<int64_t>(ceil_div((p.sc_chunk_hi - p.sc_chunk_lo) * ncb, 8),
+                                      (int64_t)num_sms() * 16);
       hook_before("k_scatter", stream);
       if (pl.rc == RC_BIG) {
         if (single)
@@ -1430,6 +1449,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       note_launch();
     }
   });
+  }
   if (rc != RECD_OK) return rc;
   RECD_LAUNCH_CHECK();
   return RECD_OK;
