@@ -65,6 +65,9 @@ enum {
 };
 
 enum { RECD_POOL_SUM = 0, RECD_POOL_AVG = 1, RECD_POOL_MAX = 2 };
+/* recd_pool_fwd mode flag: the lookup runs beside a kernel on another stream
+ * (e.g. recd_pool_bwd_prepare); its persistent grid leaves one CTA slot per SM. */
+#define RECD_POOL_SHARE 0x100
 enum { RECD_XF_IDENTITY = 0, RECD_XF_MOD_HASH = 1, RECD_XF_CLAMP = 2 };
 
 /* Value of an error slot when no error occurred. */
@@ -116,6 +119,7 @@ int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t batch_siz
  *   pooled_out  host [F] device float[U_cap x dim]  (may alias out[f] when inverse[f] is NULL)
  *   err         device int64[2]: [0] first bad ID as (f << 40) | position, or RECD_NO_ERROR;
  *               [1] scratch (work counter of the launch)
+ *   mode        RECD_POOL_SUM / AVG / MAX, optionally | RECD_POOL_SHARE
  */
 int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
                   const float* const* tables, const int64_t* table_rows,

@@ -20,6 +20,7 @@ _lib = None
 RECD_OK = 0
 RECD_NO_ERROR = 0x7F7F7F7F7F7F7F7F
 POOL_MODES = {"sum": 0, "avg": 1, "mean": 1, "max": 2}
+POOL_SHARE = 0x100  # recd_pool_fwd mode flag (include/recd.h)
 _ERRORS = {1: "invalid argument", 2: "CUDA error", 3: "scratch buffer too small",
            4: "unsupported configuration"}
 

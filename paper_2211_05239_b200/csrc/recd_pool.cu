@@ -481,19 +481,35 @@ __global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_
 
 // k_pool_ring for sum / avg with float4 lanes, k_pool_fwd otherwise
 template <class C>
-static int launch_pool_fwd(const PoolParams& p, int mode, unsigned grid, cudaStream_t stream) {
+static int launch_pool_fwd(const PoolParams& p, int mode, bool share, unsigned grid,
+                           cudaStream_t stream) {
   if constexpr (C::VW == 4 && RECD_POOL_RING) {
     if (mode != RECD_POOL_MAX) {
       constexpr int K = RECD_RING_K;  // batches of 8 rows in flight per warp
       constexpr int smem = 8 * K * 8 * 128 * (int)sizeof(float);
       static bool attr[64] = {};
+      static int resident[64] = {};
       int dev = 0;
       RECD_CUDA_CHECK(cudaGetDevice(&dev));
       if (dev < 0 || dev >= 64 || !attr[dev]) {
         RECD_CUDA_CHECK(cudaFuncSetAttribute(k_pool_ring<C, K>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        if (dev >= 0 && dev < 64) attr[dev] = true;
+        int per = 0;
+        RECD_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pool_ring<C, K>, 256, smem));
+        if (dev >= 0 && dev < 64) attr[dev] = true, resident[dev] = std::max(per, 1);
       }
+      // Persistent grid (one wave: each CTA's ring warms up once).  With
+      // RECD_POOL_SHARE one slot per SM is left to a kernel running beside
+      // the lookup on another stream (TrainStep's occurrence sort).  The
+      // RECD_POOL_CTAS env overrides the CTAs per SM.
+      static int env_ctas = -1;
+      if (env_ctas < 0) {
+        const char* e = getenv("RECD_POOL_CTAS");
+        env_ctas = e ? std::max(1, atoi(e)) : 0;
+      }
+      const int res = (dev >= 0 && dev < 64) ? resident[dev] : 1;
+      const int per_sm = env_ctas ? env_ctas : std::max(1, share ? res - 1 : res);
+      grid = std::min<unsigned>(grid, (unsigned)(num_sms() * per_sm));
       k_pool_ring<C, K><<<grid, 256, smem, stream>>>(p);
       return RECD_OK;
     }
@@ -519,6 +535,8 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
                              float* const* pooled_out, float* const* out, int64_t* err,
                              recd_stream_t stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
+  const bool share = (mode & RECD_POOL_SHARE) != 0;
+  mode &= ~RECD_POOL_SHARE;
   if (num_features <= 0 || batch_size < 0 || dim <= 0 || mode < 0 || mode > 2 || !counts || !err)
     return RECD_ERR_ARG;
   RECD_CUDA_CHECK(cudaMemsetAsync(err, 0x7f, sizeof(int64_t), stream));
@@ -551,7 +569,7 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
     int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, 1, {
       const unsigned grid = grid_for(batch_size * p.F * col_blocks<C>(dim));
       hook_before("k_pool_fwd", stream);
-      const int lrc = launch_pool_fwd<C>(p, mode, grid, stream);
+      const int lrc = launch_pool_fwd<C>(p, mode, share, grid, stream);
       if (lrc != RECD_OK) return lrc;
       hook_after("k_pool_fwd", stream);
       note_launch();
@@ -606,7 +624,7 @@ extern "C" int recd_pool_fwd_scatter(int32_t num_features, int64_t batch_size, i
     if (!p.tables[f] || !p.uoffsets[f] || !p.seg_row0[f]) return RECD_ERR_ARG;
   }
   int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, 1, {
-    const int lrc = launch_pool_fwd<C>(p, mode, grid_for(batch_size * p.F * col_blocks<C>(dim)), stream);
+    const int lrc = launch_pool_fwd<C>(p, mode, false, grid_for(batch_size * p.F * col_blocks<C>(dim)), stream);
     if (lrc != RECD_OK) return lrc;
     note_launch();
   });

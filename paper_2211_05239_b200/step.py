@@ -153,7 +153,9 @@ class TrainStep:
         self.stage = 0
         self._args: dict = {}
         self.graphs: list = [None] * self.nslots
-        self._side = torch.cuda.Stream(dev)
+        # RECD_SIDE_PRIORITY (e.g. -1): the side stream's occurrence sort gets
+        # free SM slots ahead of the main stream's lookup
+        self._side = torch.cuda.Stream(dev, priority=int(os.environ.get("RECD_SIDE_PRIORITY", "0")))
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
 
@@ -251,10 +253,12 @@ class TrainStep:
                                     st.dedup_scratch.data_ptr(), st.dedup_scratch.numel(), stream)
         _lib.check(rc, "recd_dedup_ex")
 
-    def forward(self, stream: int, stage=None, slot=None) -> None:
-        """Pooled lookup over the unique rows (k_pool_fwd only)."""
+    def forward(self, stream: int, stage=None, slot=None, share: bool = False) -> None:
+        """Pooled lookup over the unique rows (k_pool_fwd only).  share: the
+        side stream's backward prepare runs beside it (RECD_POOL_SHARE)."""
         a, st = self.args(stage, slot), self._st(stage)
-        rc = self.lib.recd_pool_fwd(self.F, self.B, self.D, self.mode_id, a.tables, a.rows,
+        mode = self.mode_id | (_lib.POOL_SHARE if share else 0)
+        rc = self.lib.recd_pool_fwd(self.F, self.B, self.D, mode, a.tables, a.rows,
                                     a.feat_vals, a.feat_offs, a.counts_ptr, a.inverse_f, a.pooled,
                                     None, st.err.data_ptr(), stream)
         _lib.check(rc, "recd_pool_fwd")
@@ -301,7 +305,7 @@ class TrainStep:
         self._side.wait_event(self._ev_fork)
         self.backward_prepare(self._side.cuda_stream)
         self._ev_join.record(self._side)
-        self.forward(main.cuda_stream)
+        self.forward(main.cuda_stream, share=True)
         self.expand(main.cuda_stream)
         main.wait_event(self._ev_join)
         self.backward_finish(main.cuda_stream)
@@ -330,7 +334,7 @@ class TrainStep:
         self.backward_prepare(ss, q, q)
         self._ev_join.record(self._side)
         ms = main.cuda_stream
-        self.forward(ms, p, p)
+        self.forward(ms, p, p, share=True)
         self.expand(ms, p, p)
         self.backward_finish(ms, p, p)
         main.wait_event(self._ev_join)
