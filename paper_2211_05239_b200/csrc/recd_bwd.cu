@@ -96,6 +96,8 @@ struct BwdParams {
   int64_t* head_count;    // [nts] run heads per table segment (the heads sort's counts)
   int64_t* head_off;      // [occ cap] run lengths in sorted order -> exclusive offsets
   int32_t* fallback;      // set when some ID's runs need per-value occurrences
+  uint32_t* sc_ticket;    // k_scatter work counter (dynamic chunk order), zeroed per launch
+  int sc_dyn;             // k_scatter: warps take chunks from sc_ticket (else grid-stride)
   uint32_t* exp_keys;     // expanded occurrences (the scatter's input)
   uint32_t* exp_vals;
   const int32_t* occ_gate;              // k_occ runs only if null or *occ_gate != 0
@@ -770,7 +772,17 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
   constexpr bool HINT = RECD_SCATTER_L2 > 0 && V == 4;
   const uint64_t pol_stream = HINT ? l2_evict_first() : 0;
   const uint64_t pol_keep = (HINT && RECD_SCATTER_L2 >= 2) ? l2_evict_last() : 0;
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nwarps) {
+  // next (chunk, column block) task: grid-stride, or the next ticket (dynamic:
+  // tasks start in order however long each takes, so the warps in flight work
+  // on neighbouring chunks -- one table segment's gradients stay hot in L2)
+  auto next_task = [&](int64_t cur) -> int64_t {
+    if (!p.sc_dyn) return cur + nwarps;
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(p.sc_ticket, 1u);
+    return (int64_t)__shfl_sync(0xffffffffu, t, 0);
+  };
+  for (int64_t w = p.sc_dyn ? next_task(0) : (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+       w < total; w = next_task(w)) {
     const int64_t wc = ((ncb == 1) ? w : w / ncb) + p.sc_chunk_lo;
     // RECD_SC_REV: last table segment first -- k_grad_u_flat wrote the unique-row
     // gradients in feature order, so the last features' are still in L2
@@ -1059,6 +1071,7 @@ struct BwdScratch {
   uint32_t *head_tag, *head_len;
   int64_t *head_count, *head_off, *runs_scan_part;
   int32_t* fallback;
+  uint32_t* sc_ticket;
   uint32_t *inv_k0, *inv_v0, *inv_k1, *inv_v1, *hist;
   int32_t* csr_start;
   float* grad_u;
@@ -1091,6 +1104,7 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   s->head_off = a.take<int64_t>(rn ? occ : 1);
   s->head_count = a.take<int64_t>(RECD_MAX_FEAT);
   s->fallback = a.take<int32_t>(1);
+  s->sc_ticket = a.take<uint32_t>(1);
   {
     std::vector<ScanDesc> d;
     for (int t = 0; t < pl.nts; ++t) d.push_back({nullptr, nullptr, rn ? pl.ts_cap[t] : 1, nullptr, nullptr});
@@ -1255,6 +1269,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   p.head_off = sc.head_off;
   p.head_count = sc.head_count;
   p.fallback = sc.fallback;
+  p.sc_ticket = sc.sc_ticket;
   const bool runs = bm == BwdMode::Full && do_scatter && use_runs();
 
   const bool prep = (phase & PH_PREP) != 0, fin = (phase & PH_FINISH) != 0;
@@ -1430,9 +1445,18 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         int r3 = seg_exclusive_scan(sd.data(), (int)sd.size(), sc.scan_part, stream);
         if (r3 != RECD_OK) return r3;
       }
+      // One task per warp (the grid covers every chunk, cap 128 CTAs per SM):
+      // CTAs start in chunk order, so the warps in flight work on neighbouring
+      // chunks and each CTA's slot is refilled as soon as it drains.  cfg2:
+      // scatter 1.83-1.85 ms vs 1.95 with a 16-per-SM grid-stride loop (whose
+      // later iterations jump far ahead in the chunk order).  RECD_SC_DYN:
+      // resident grid taking tasks from a ticket counter: 1.90 ms.
+      static const int sc_dyn = getenv("RECD_SC_DYN") ? atoi(getenv("RECD_SC_DYN")) : 0;
+      p.sc_dyn = sc_dyn;
+      if (sc_dyn) RECD_CUDA_CHECK(cudaMemsetAsync(sc.sc_ticket, 0, sizeof(uint32_t), stream));
       const unsigned g2 =
           (unsigned)std::min<int64_t>(ceil_div((p.sc_chunk_hi - p.sc_chunk_lo) * ncb, 8),
-                                      (int64_t)num_sms() * 16);
+                                      grid_cap("RECD_SC_CTAS", sc_dyn ? RECD_SCATTER_MINB : 128));
       hook_before("k_scatter", stream);
       if (pl.rc == RC_BIG) {
         if (single)

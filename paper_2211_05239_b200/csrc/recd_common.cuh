@@ -8,6 +8,7 @@
 //   be enqueued (and graph-captured) without a host round trip.
 #pragma once
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -37,6 +38,12 @@ void hook_before(const char* name, cudaStream_t s);
 void hook_after(const char* name, cudaStream_t s);
 
 int num_sms();
+// grid cap of grid-stride kernels: `per_sm` CTAs per SM, or the value of the
+// environment variable `env` (tuning / A/B knob) when set
+inline int64_t grid_cap(const char* env, int per_sm) {
+  const char* e = getenv(env);
+  return (int64_t)num_sms() * (e ? (atoi(e) > 0 ? atoi(e) : 1) : per_sm);
+}
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -524,6 +524,11 @@ static unsigned grid_for(int64_t warps) {
   return (unsigned)std::min(blocks, cap);
 }
 
+static unsigned expand_grid(int64_t batch_size, int64_t tasks_per_32) {
+  return (unsigned)std::min<int64_t>(grid_for(ceil_div(batch_size, 32) * tasks_per_32),
+                                     grid_cap("RECD_EX_CTAS", 16));
+}
+
 }  // namespace recd
 
 using namespace recd;
@@ -574,7 +579,7 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
       hook_after("k_pool_fwd", stream);
       note_launch();
       if (any_expand) {
-        k_expand<C><<<grid_for(ceil_div(batch_size, 32) * p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
+        k_expand<C><<<expand_grid(batch_size, p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
         note_launch();
       }
     });
@@ -684,7 +689,7 @@ extern "C" int recd_expand(int32_t num_features, int64_t batch_size, int32_t dim
       if (!p.pooled[f] || !p.out[f]) return RECD_ERR_ARG;
     }
     int rc = RECD_DISPATCH_COL(dim, {
-      k_expand<C><<<grid_for(ceil_div(batch_size, 32) * p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
+      k_expand<C><<<expand_grid(batch_size, p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
       note_launch();
     });
     if (rc != RECD_OK) return rc;
