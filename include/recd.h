@@ -233,6 +233,26 @@ int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, int32_t dim, 
                          float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
                          size_t scratch_bytes, recd_stream_t stream);
 
+/* recd_pool_bwd in up to four stages (same arguments and scratch; enqueue the
+ * selected stages in this order, each stage after the previous ones): INVERSE
+ * (setup + inverse CSR), OCCURRENCES (occurrence pairs + their sort by ID),
+ * GRAD (unique-row gradients; reads grad_out), SCATTER (sorted scatter-add /
+ * SGD).  _prepare = INVERSE | OCCURRENCES, _finish = GRAD | SCATTER.  With
+ * OCCURRENCES on a side stream, GRAD only waits for INVERSE and runs while the
+ * sort finishes. */
+#define RECD_BWD_INVERSE 1
+#define RECD_BWD_OCCURRENCES 2
+#define RECD_BWD_GRAD 4
+#define RECD_BWD_SCATTER 8
+int recd_pool_bwd_stages(int32_t stages, int32_t num_features, int64_t batch_size, int32_t dim,
+                         int32_t mode, float* const* tables, const int64_t* table_rows,
+                         const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                         const int64_t* value_caps, const int64_t* counts,
+                         const int64_t* const* inverse, const float* const* grad_out, float lr,
+                         int32_t apply_sgd, int64_t* const* grad_ids_out,
+                         float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
+                         size_t scratch_bytes, recd_stream_t stream);
+
 /* ------------------------------------------------------- transforms --
  * <- reader.apply_transform (reader.py:69-83) as used by reader.process
  * (reader.py:178-217) on IKJT unique values: per feature f,

@@ -21,6 +21,7 @@ RECD_OK = 0
 RECD_NO_ERROR = 0x7F7F7F7F7F7F7F7F
 POOL_MODES = {"sum": 0, "avg": 1, "mean": 1, "max": 2}
 POOL_SHARE = 0x100  # recd_pool_fwd mode flag (include/recd.h)
+BWD_INVERSE, BWD_OCCURRENCES, BWD_GRAD, BWD_SCATTER = 1, 2, 4, 8  # recd_pool_bwd_stages
 _ERRORS = {1: "invalid argument", 2: "CUDA error", 3: "scratch buffer too small",
            4: "unsupported configuration"}
 
@@ -60,6 +61,8 @@ _SIGS = {
                                      _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_pool_bwd_finish": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp,
                                     _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_pool_bwd_stages": (_i32, [_i32, _i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp,
+                                    _pp, _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_wire_bound": (_i64, [_i32, C.POINTER(C.c_char_p), _i64, _i32, _p64, _p64]),
     "recd_wire_serialize": (_i32, [_i32, C.POINTER(C.c_char_p), _i64, _vp, _pp, _pp, _pp, _pp, _p64,
                                    _p64, _vp, _i64, _vp, _vp, _sz, _vp]),

@@ -1155,7 +1155,10 @@ static bool use_runs() {
   const char* e = getenv("RECD_BWD_RUNS");
   return e ? (atoi(e) != 0) : (RECD_BWD_RUNS != 0);
 }
-enum { PH_PREP = 1, PH_FINISH = 2, PH_ALL = 3 };
+// stages (include/recd.h RECD_BWD_*): inverse CSR, occurrence sort, unique-row
+// gradients, scatter; prepare = the first two, finish = the last two
+enum { PH_INV = 1, PH_OCC = 2, PH_GRAD = 4, PH_SCAT = 8,
+       PH_PREP = PH_INV | PH_OCC, PH_FINISH = PH_GRAD | PH_SCAT, PH_ALL = PH_PREP | PH_FINISH };
 
 int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* tables,
             const int64_t* table_rows, const int64_t* const* uvalues,
@@ -1175,7 +1178,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   std::vector<int64_t> dummy_rows(F, 1), dummy_caps(F, 1);
   for (int f = 0; f < F; ++f) {
     if (!uoffsets[f]) return RECD_ERR_ARG;
-    if (do_grad && (phase & PH_FINISH) && !grad_out[f]) return RECD_ERR_ARG;
+    if (do_grad && (phase & PH_GRAD) && !grad_out[f]) return RECD_ERR_ARG;
     if (bm == BwdMode::GradOnly && !gout_ext[f]) return RECD_ERR_ARG;
     if (bm == BwdMode::ScatterOnly && !grow_ext[f]) return RECD_ERR_ARG;
     if (do_scatter) {
@@ -1272,28 +1275,33 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   p.sc_ticket = sc.sc_ticket;
   const bool runs = bm == BwdMode::Full && do_scatter && use_runs();
 
-  const bool prep = (phase & PH_PREP) != 0, fin = (phase & PH_FINISH) != 0;
+  const bool fin = (phase & PH_FINISH) != 0;
+  const bool run_grad = do_grad && (phase & PH_GRAD), run_scat = do_scatter && (phase & PH_SCAT);
   // sorted buffers: a stable LSD sort of `bits` bits ends in the alternate
   // buffers after an odd number of 8-bit passes
   auto odd_passes = [](int64_t bits) { return ((bits + 7) / 8) % 2 == 1; };
   int64_t maxrows = 1;
   for (int s = 0; s < pl.nts; ++s) maxrows = std::max(maxrows, pl.table_rows[s]);
-  p.inv_keys = odd_passes(bits_for(B)) ? sc.inv_k1 : sc.inv_k0;
-  p.inv_rows = odd_passes(bits_for(B)) ? sc.inv_v1 : sc.inv_v0;
-  const bool odd = odd_passes(bits_for(maxrows));
+  const bool inv_alt = sort_lands_in_alt((int)bits_for(B), false);
+  p.inv_keys = inv_alt ? sc.inv_k1 : sc.inv_k0;
+  p.inv_rows = inv_alt ? sc.inv_v1 : sc.inv_v0;
+  const bool odd = odd_passes(bits_for(maxrows));  // the gated (plain LSD) sort
+  const bool occ_alt = sort_lands_in_alt((int)bits_for(maxrows), false);
   // the scatter's sorted occurrences: per-value sort result, or with runs the
   // expansion's output (the buffer pair the heads sort did not end in)
-  p.occ_keys = (odd != runs) ? sc.occ_k1 : sc.occ_k0;
-  p.occ_vals = (odd != runs) ? sc.occ_v1 : sc.occ_v0;
+  p.occ_keys = (occ_alt != runs) ? sc.occ_k1 : sc.occ_k0;
+  p.occ_vals = (occ_alt != runs) ? sc.occ_v1 : sc.occ_v0;
   p.exp_keys = p.occ_keys;
   p.exp_vals = p.occ_vals;
 
   // ---- prepare: everything that depends on the IKJT only (no gradient)
-  if (prep) {
+  if (phase & PH_INV) {
     k_bwd_setup<<<1, 32, 0, stream>>>(p);
     note_launch();
+  }
+  {
     // 1. inverse CSR
-    if (do_grad && pl.nis > 0) {
+    if ((phase & PH_INV) && do_grad && pl.nis > 0) {
       const int64_t n = (int64_t)pl.nis * B;
       k_inv_pairs<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p, sc.inv_k0, sc.inv_v0);
       note_launch();
@@ -1307,7 +1315,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       note_launch();
     }
     // 3-4. occurrences, sorted by ID per table segment
-    if (do_scatter) {
+    if ((phase & PH_OCC) && do_scatter) {
       int64_t ob = 0;
       p.oc_ch = pl.occ_total >= (8ll << 20) ? OC_CH : OC_CH_SMALL;
       for (int f = 0; f < F; ++f) {
@@ -1386,14 +1394,14 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     return RECD_OK;
   }
   // ---- finish: gradient-dependent work
-  if (do_scatter && !apply_sgd)
+  if (run_scat && !apply_sgd)
     RECD_CUDA_CHECK(cudaMemsetAsync(grad_counts_out, 0, sizeof(int64_t) * F, stream));
   // Fused SGD: unique-row gradients and the scatter may run in groups of
   // table segments (RECD_SC_GROUP env: segments per group), so a group's
   // gradients are still in L2 when its scatter gathers them.
   int group = 0;
   if (const char* e = getenv("RECD_SC_GROUP")) group = atoi(e);
-  if (!(do_grad && do_scatter && apply_sgd) || group <= 0 || group >= pl.nts) group = pl.nts;
+  if (!(run_grad && run_scat && apply_sgd) || group <= 0 || group >= pl.nts) group = pl.nts;
   int rc = RECD_OK;
   for (int s0 = 0; s0 < pl.nts && rc == RECD_OK; s0 += group) {
     const int s1 = std::min(pl.nts, s0 + group);
@@ -1407,7 +1415,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     rc = RECD_DISPATCH_COL_VW(dim, RECD_BWD_VW, RECD_BWD_FULLOK, {
     const int ncb = col_blocks<C>(dim);
     // 2. unique-row gradients
-    if (do_grad) {
+    if (run_grad) {
       const unsigned grid =
           (unsigned)std::min<int64_t>(ceil_div(B * F * ncb, 8), (int64_t)num_sms() * 16);
       bool any_id = !RECD_GU_FLAT, any_inv = false;
@@ -1429,7 +1437,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       }
     }
     // 5. sorted scatter-add (+ fused SGD)
-    if (do_scatter) {
+    if (run_scat) {
       if (!apply_sgd && s0 == 0) {
         if (pl.rc == RC_BIG)
           k_run_count<RC_BIG><<<(unsigned)pl.rc_chunks, RC_BIG, 0, stream>>>(p);
@@ -1545,6 +1553,22 @@ extern "C" int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, in
                  uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
                  grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
                  (cudaStream_t)stream, PH_FINISH);
+}
+
+extern "C" int recd_pool_bwd_stages(int32_t stages, int32_t num_features, int64_t batch_size,
+                                    int32_t dim, int32_t mode, float* const* tables,
+                                    const int64_t* table_rows, const int64_t* const* uvalues,
+                                    const int64_t* const* uoffsets, const int64_t* value_caps,
+                                    const int64_t* counts, const int64_t* const* inverse,
+                                    const float* const* grad_out, float lr, int32_t apply_sgd,
+                                    int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                                    int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                                    recd_stream_t stream) {
+  if (stages <= 0 || (stages & ~PH_ALL)) return RECD_ERR_ARG;
+  return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
+                 uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
+                 grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
+                 (cudaStream_t)stream, stages);
 }
 
 extern "C" size_t recd_grad_unique_scratch_bytes(int32_t num_features, int64_t batch_size) {

@@ -158,6 +158,7 @@ class TrainStep:
         self._side = torch.cuda.Stream(dev, priority=int(os.environ.get("RECD_SIDE_PRIORITY", "0")))
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
+        self._ev_inv = torch.cuda.Event()
 
     # ------------------------------------------- current stage / slot views
     def _st(self, stage=None) -> _Stage:
@@ -290,6 +291,11 @@ class TrainStep:
         _lib.check(self.lib.recd_pool_bwd_finish(*self._bwd_args(stream, stage, slot)),
                    "recd_pool_bwd_finish")
 
+    def backward_stages(self, stages: int, stream: int, stage=None, slot=None) -> None:
+        """Some of the backward's stages (_lib.BWD_*, recd_pool_bwd_stages)."""
+        _lib.check(self.lib.recd_pool_bwd_stages(stages, *self._bwd_args(stream, stage, slot)),
+                   "recd_pool_bwd_stages")
+
     def run(self, stream: int | None = None) -> None:
         """One whole step on the current slot / stage (dedup .. SGD)."""
         if stream is not None or not self.overlap:
@@ -299,16 +305,24 @@ class TrainStep:
             self.expand(s)
             self.backward(s)
             return
+        # side stream: inverse CSR, then the occurrence sort; main stream: lookup,
+        # expansion, unique-row gradients (after the CSR only, so they run while
+        # the sort finishes), then the scatter + SGD after the sort
         main = torch.cuda.current_stream(self.dev)
         self.dedup(main.cuda_stream)
         self._ev_fork.record(main)
         self._side.wait_event(self._ev_fork)
-        self.backward_prepare(self._side.cuda_stream)
+        ss = self._side.cuda_stream
+        self.backward_stages(_lib.BWD_INVERSE, ss)
+        self._ev_inv.record(self._side)
+        self.backward_stages(_lib.BWD_OCCURRENCES, ss)
         self._ev_join.record(self._side)
         self.forward(main.cuda_stream, share=True)
         self.expand(main.cuda_stream)
+        main.wait_event(self._ev_inv)
+        self.backward_stages(_lib.BWD_GRAD, main.cuda_stream)
         main.wait_event(self._ev_join)
-        self.backward_finish(main.cuda_stream)
+        self.backward_stages(_lib.BWD_SCATTER, main.cuda_stream)
 
     # ------------------------------------------------------ pipeline mode
     def prime(self, slot: int = 0) -> None:

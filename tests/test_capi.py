@@ -76,7 +76,8 @@ def test_scratch_sizes_cover_every_backward_entry_point():
         assert rc != 3, rc
     B = 1024
     nb = lib.recd_pool_bwd_scratch_bytes(F, B, D, caps)
-    for fn in (lib.recd_pool_bwd, lib.recd_pool_bwd_prepare, lib.recd_pool_bwd_finish):
+    stages = [lambda *a, st=st: lib.recd_pool_bwd_stages(st, *a) for st in (1, 2, 4, 8)]
+    for fn in (lib.recd_pool_bwd, lib.recd_pool_bwd_prepare, lib.recd_pool_bwd_finish, *stages):
         rc = fn(F, B, D, 0, P(fake[0], fake[1]), _lib.i64s([rows, rows]), P(fake[2], fake[3]),
                 P(fake[4], fake[5]), caps, fake[6].value, P(fake[6], fake[6]), P(fake[7], fake[7]),
                 C.c_float(0.1), 1, None, None, None, fake[7].value, nb, None)
