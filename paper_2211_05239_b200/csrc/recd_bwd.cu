@@ -1282,15 +1282,13 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   auto odd_passes = [](int64_t bits) { return ((bits + 7) / 8) % 2 == 1; };
   int64_t maxrows = 1;
   for (int s = 0; s < pl.nts; ++s) maxrows = std::max(maxrows, pl.table_rows[s]);
-  const bool inv_alt = sort_lands_in_alt((int)bits_for(B), false);
-  p.inv_keys = inv_alt ? sc.inv_k1 : sc.inv_k0;
-  p.inv_rows = inv_alt ? sc.inv_v1 : sc.inv_v0;
-  const bool odd = odd_passes(bits_for(maxrows));  // the gated (plain LSD) sort
-  const bool occ_alt = sort_lands_in_alt((int)bits_for(maxrows), false);
+  p.inv_keys = odd_passes(bits_for(B)) ? sc.inv_k1 : sc.inv_k0;
+  p.inv_rows = odd_passes(bits_for(B)) ? sc.inv_v1 : sc.inv_v0;
+  const bool odd = odd_passes(bits_for(maxrows));
   // the scatter's sorted occurrences: per-value sort result, or with runs the
   // expansion's output (the buffer pair the heads sort did not end in)
-  p.occ_keys = (occ_alt != runs) ? sc.occ_k1 : sc.occ_k0;
-  p.occ_vals = (occ_alt != runs) ? sc.occ_v1 : sc.occ_v0;
+  p.occ_keys = (odd != runs) ? sc.occ_k1 : sc.occ_k0;
+  p.occ_vals = (odd != runs) ? sc.occ_v1 : sc.occ_v0;
   p.exp_keys = p.occ_keys;
   p.exp_vals = p.occ_vals;
 

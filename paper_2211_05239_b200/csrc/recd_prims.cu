@@ -49,9 +49,6 @@ struct OsSeg {
 
 struct OsParams {
   int S, npass, pass, shift, nbits, bits;
-  int hrow;            // ghist row (pass) whose digit bases this launch uses
-  int top_bits;        // k_os_local: bits of the top digit (buckets = 1 << top_bits)
-  uint32_t* overflow;  // k_os_local: set when a bucket exceeds OL_CAP
   int64_t total_hchunks;
   int64_t total_tcap;
   OsSeg seg[OS_MAXSEG];
@@ -141,26 +138,6 @@ __global__ void __launch_bounds__(OS_NT) k_os_setup(const __grid_constant__ OsPa
   h[threadIdx.x] = (uint32_t)x;
 }
 
-// lanes of the warp holding the same 9-bit digit d (0x100 = invalid lane):
-// __match_any_sync, or (RECD_OS_BALLOT) one ballot per digit bit
-#ifndef RECD_OS_BALLOT
-#define RECD_OS_BALLOT 0
-#endif
-__device__ __forceinline__ unsigned digit_peers(uint32_t d) {
-#if RECD_OS_BALLOT
-  unsigned peers = 0xffffffffu;
-#pragma unroll
-  for (int b = 0; b < 9; ++b) {
-    const bool bit = (d >> b) & 1u;
-    const unsigned m = __ballot_sync(0xffffffffu, bit);
-    peers &= bit ? m : ~m;
-  }
-  return peers;
-#else
-  return __match_any_sync(0xffffffffu, d);
-#endif
-}
-
 #ifndef RECD_OS_MINB
 #define RECD_OS_MINB 3
 #endif
@@ -213,7 +190,7 @@ __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_c
       const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
       const bool valid = e < tn;
       const uint32_t d = valid ? ((key[r] >> p.shift) & mask) : 0x100u;
-      const unsigned peers = digit_peers(d);
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
       uint32_t before = 0;
       if (valid) before = s_wcnt[warp][d];
       __syncwarp();
@@ -263,7 +240,7 @@ __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_c
       st_relaxed(my, OS_PRE | (excl + cnt));
     }
     if (p.pass + 1 < p.npass) st_next[(sg.tcap0 + lt_) * 256 + tid] = 0u;
-    s_gb[tid] = (uint32_t)(sg.base + p.ghist[((int64_t)s * OS_MAXPASS + p.hrow) * 256 + tid] + excl);
+    s_gb[tid] = (uint32_t)(sg.base + p.ghist[((int64_t)s * OS_MAXPASS + p.pass) * 256 + tid] + excl);
     int64_t tot;
     const int64_t tdb = block_exclusive_scan<OS_NT>(cnt, s_scan, &tot);
     s_tdb[tid] = (uint32_t)tdb;
@@ -288,128 +265,6 @@ __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_c
     }
     __syncthreads();
   }
-}
-
-// Split sort (keys of 17..24 bits): one one-sweep pass on the top digit
-// leaves every segment in buckets of equal top digit (stable); k_os_local
-// then sorts each bucket by the low 16 bits in shared memory -- two stable
-// 8-bit passes with the same warp ranking, no look-back, one read and one
-// write of the bucket.  A bucket larger than OL_CAP sets `overflow`, and the
-// regular LSD passes (gated on it) re-sort the top pass's output.
-constexpr int OL_NT = 1024;
-constexpr int OL_WARPS = OL_NT / 32;
-constexpr int OL_ITEMS = 16;
-constexpr int OL_CAP = OL_NT * OL_ITEMS;  // 16384 elements per bucket
-constexpr int OL_SMEM = OL_CAP * (2 * (int)sizeof(uint32_t) + (int)sizeof(uint16_t));
-
-__global__ void __launch_bounds__(OL_NT, 1) k_os_local(const __grid_constant__ OsParams p) {
-  const int nb = 1 << p.top_bits;
-  const int s = blockIdx.x >> p.top_bits, d = blockIdx.x & (nb - 1);
-  const OsSeg& sg = p.seg[s];
-  const uint32_t* h = p.ghist + ((int64_t)s * OS_MAXPASS + p.hrow) * 256;
-  const int64_t lo = h[d], hi = (d + 1 < nb) ? (int64_t)h[d + 1] : *sg.count;
-  const int n = (int)(hi - lo);
-  if (n <= 0) return;
-  if (n > OL_CAP) {
-    if (threadIdx.x == 0) atomicExch(p.overflow, 1u);
-    return;
-  }
-  // values stay where they were loaded (s_vin); the passes move (key, source
-  // index) pairs, and the final write gathers the values through the index
-  extern __shared__ uint32_t ol_smem[];
-  uint32_t* s_vin = ol_smem;
-  uint32_t* s_keys = ol_smem + OL_CAP;
-  uint16_t* s_idx = reinterpret_cast<uint16_t*>(ol_smem + 2 * OL_CAP);
-  __shared__ uint32_t s_wcnt[OL_WARPS][256];
-  __shared__ uint32_t s_tdb[256];
-  __shared__ int64_t s_scan[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt = lanemask_lt();
-  // element e = warp * span + r * 32 + lane: (warp, round, lane) is input order
-  const int nr = (n + OL_NT - 1) / OL_NT, span = nr * 32;
-  const uint32_t* kin = p.kin + sg.base + lo;
-  const uint32_t* vin = p.vin + sg.base + lo;
-  for (int q = tid; q < n; q += OL_NT) s_vin[q] = __ldg(vin + q);
-  uint32_t key[OL_ITEMS], pk[OL_ITEMS];  // pk: source index << 16 | rank
-#pragma unroll
-  for (int r = 0; r < OL_ITEMS; ++r) {
-    const int e = warp * span + r * 32 + lane;
-    const bool ok = r < nr && e < n;
-    key[r] = ok ? __ldg(kin + e) : 0u;
-    pk[r] = (uint32_t)e << 16;
-  }
-#pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-    const int sh = 8 * pass;
-    for (int q = lane; q < 256; q += 32) s_wcnt[warp][q] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < OL_ITEMS; ++r) {
-      if (r < nr) {
-        const int e = warp * span + r * 32 + lane;
-        const bool valid = e < n;
-        const uint32_t dg = valid ? ((key[r] >> sh) & 0xffu) : 0x100u;
-        const unsigned peers = digit_peers(dg);
-        uint32_t before = 0;
-        if (valid) before = s_wcnt[warp][dg];
-        __syncwarp();
-        if (valid && lane == __ffs(peers) - 1) s_wcnt[warp][dg] = before + __popc(peers);
-        __syncwarp();
-        pk[r] = (pk[r] & 0xffff0000u) | (before + __popc(peers & lt));
-      }
-    }
-    __syncthreads();
-    uint32_t cnt = 0;
-    if (tid < 256) {
-#pragma unroll 8
-      for (int w = 0; w < OL_WARPS; ++w) {
-        const uint32_t c = s_wcnt[w][tid];
-        s_wcnt[w][tid] = cnt;
-        cnt += c;
-      }
-    }
-    int64_t tot;
-    const int64_t tdb = block_exclusive_scan<OL_NT>(tid < 256 ? (int64_t)cnt : 0, s_scan, &tot);
-    if (tid < 256) s_tdb[tid] = (uint32_t)tdb;
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < OL_ITEMS; ++r) {
-      const int e = warp * span + r * 32 + lane;
-      if (r < nr && e < n) {
-        const uint32_t dg = (key[r] >> sh) & 0xffu;
-        const uint32_t pos = s_tdb[dg] + s_wcnt[warp][dg] + (pk[r] & 0xffffu);
-        s_keys[pos] = key[r];
-        s_idx[pos] = (uint16_t)(pk[r] >> 16);
-      }
-    }
-    __syncthreads();
-    if (pass == 0) {
-#pragma unroll
-      for (int r = 0; r < OL_ITEMS; ++r) {
-        const int e = warp * span + r * 32 + lane;
-        if (r < nr && e < n) {
-          key[r] = s_keys[e];
-          pk[r] = (uint32_t)s_idx[e] << 16;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  uint32_t* kout = p.kout + sg.base + lo;
-  uint32_t* vout = p.vout + sg.base + lo;
-  for (int q = tid; q < n; q += OL_NT) {
-    kout[q] = s_keys[q];
-    vout[q] = s_vin[s_idx[q]];
-  }
-}
-
-// gated (fallback only): ticket counters and the first pass's status plane
-__global__ void k_os_reset(const __grid_constant__ OsParams p) {
-  if (os_gated_off(p)) return;
-  const int64_t n = p.total_tcap * 256;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p.status[i] = 0u;
-  if (blockIdx.x == 0 && threadIdx.x < OS_MAXPASS) p.counters[threadIdx.x] = 0u;
 }
 
 static void build_os_params(const SegDesc* segs, int S, OsParams* p) {
@@ -457,17 +312,6 @@ static int os_grid() {
   return g;
 }
 
-// split sort for 22..24-bit keys (a top digit of >= 6 bits: buckets of ~1/64
-// of a segment or less); RECD_SORT_SPLIT=0: plain LSD passes
-bool sort_is_split(int bits, bool gated) {
-  static const int split_env = getenv("RECD_SORT_SPLIT") ? atoi(getenv("RECD_SORT_SPLIT")) : 0;
-  return split_env && (bits + 7) / 8 == 3 && bits >= 22 && !gated;
-}
-
-bool sort_lands_in_alt(int bits, bool gated) {
-  return bits > 0 && !sort_is_split(bits, gated) && ((bits + 7) / 8) % 2 == 1;
-}
-
 int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_t* vals,
                    uint32_t* keys_alt, uint32_t* vals_alt, uint32_t* hist, bool* in_alt,
                    cudaStream_t stream, const int32_t* gate, bool hist_ready) {
@@ -477,7 +321,6 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
   if (npass > OS_MAXPASS) return RECD_ERR_UNSUPPORTED;
   for (int s = 0; s < S; ++s)
     if (segs[s].cap > (int64_t)OS_CNT) return RECD_ERR_UNSUPPORTED;
-  const bool split = sort_is_split(bits, gate != nullptr);
   for (int s0 = 0; s0 < S; s0 += OS_MAXSEG) {
     OsParams p;
     build_os_params(segs + s0, std::min(OS_MAXSEG, S - s0), &p);
@@ -503,41 +346,9 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
       k_os_setup<<<p.S * npass, OS_NT, 0, stream>>>(p);
       note_launch(2);
     }
-    if (split) {
-      // top digit: keys -> alt (ticket 0, status plane 0, no next plane)
-      OsParams t = p;
-      t.npass = 1;
-      t.pass = 0;
-      t.hrow = npass - 1;
-      t.shift = 8 * (npass - 1);
-      t.nbits = bits - 8 * (npass - 1);
-      t.kin = keys; t.vin = vals; t.kout = keys_alt; t.vout = vals_alt;
-      k_onesweep<<<(unsigned)std::min<int64_t>(os_grid(), p.total_tcap), OS_NT, 0, stream>>>(t);
-      // buckets: alt -> keys
-      uint32_t* overflow = p.counters + 8;
-      RECD_CUDA_CHECK(cudaMemsetAsync(overflow, 0, sizeof(uint32_t), stream));
-      OsParams l = t;
-      l.top_bits = t.nbits;
-      l.overflow = overflow;
-      l.kin = keys_alt; l.vin = vals_alt; l.kout = keys; l.vout = vals;
-      static bool attr[64] = {};
-      int dev = 0;
-      RECD_CUDA_CHECK(cudaGetDevice(&dev));
-      if (dev < 0 || dev >= 64 || !attr[dev]) {
-        RECD_CUDA_CHECK(cudaFuncSetAttribute(k_os_local, cudaFuncAttributeMaxDynamicSharedMemorySize, OL_SMEM));
-        if (dev >= 0 && dev < 64) attr[dev] = true;
-      }
-      k_os_local<<<(unsigned)(p.S << l.top_bits), OL_NT, OL_SMEM, stream>>>(l);
-      // fallback, gated on overflow: the full LSD sort of the top pass's output
-      p.gate = reinterpret_cast<const int32_t*>(overflow);
-      k_os_reset<<<num_sms(), 256, 0, stream>>>(p);
-      note_launch(4);
-    }
-    uint32_t *ki = split ? keys_alt : keys, *vi = split ? vals_alt : vals;
-    uint32_t *ko = split ? keys : keys_alt, *vo = split ? vals : vals_alt;
+    uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
     for (int pass = 0; pass < npass; ++pass) {
       p.pass = pass;
-      p.hrow = pass;
       p.shift = 8 * pass;
       p.nbits = std::min(8, bits - 8 * pass);
       p.kin = ki; p.vin = vi; p.kout = ko; p.vout = vo;
@@ -547,7 +358,7 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
       std::swap(vi, vo);
     }
   }
-  *in_alt = !split && (npass % 2) == 1;
+  *in_alt = (npass % 2) == 1;
   RECD_LAUNCH_CHECK();
   return RECD_OK;
 }

@@ -28,10 +28,6 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
                    uint32_t* keys_alt, uint32_t* vals_alt, uint32_t* hist, bool* in_alt,
                    cudaStream_t stream, const int32_t* gate = nullptr, bool hist_ready = false);
 int sort_hist_clear(int S, uint32_t* hist, cudaStream_t stream);
-// where seg_sort_pairs leaves the result (*in_alt) for `bits`-bit keys,
-// gated or not -- known before the sort runs
-bool sort_lands_in_alt(int bits, bool gated);
-bool sort_is_split(int bits, bool gated);
 constexpr int SORT_HIST_PASSES = 4;  // hist row stride: passes per segment
 
 struct ScanDesc {

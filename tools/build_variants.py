@@ -36,7 +36,6 @@ V = {
     "k1m4": ["RECD_RING_K=1", "RECD_RING_MINB=4"],
     "cp32": ["RECD_CP_IT=32", "RECD_OC_CH=8192"],
     "cp64": ["RECD_CP_IT=64", "RECD_OC_CH=16384"],
-    "osb": ["RECD_OS_BALLOT=1"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
