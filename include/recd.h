@@ -128,6 +128,19 @@ int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t
                   float* const* pooled_out, float* const* out, int64_t* err,
                   recd_stream_t stream);
 
+/* recd_pool_fwd with the expansion fused through the inverse CSR of
+ * recd_pool_bwd_csr (batch rows of every unique row): each pooled row is
+ * stored straight to out[f][i] for its batch rows i, so the [U x dim] pooled
+ * buffer is neither written nor re-read (pooled_out: NULL, or per feature NULL
+ * or a buffer that also receives the pooled rows).  Needs the backward's
+ * RECD_BWD_INVERSE stage to have run on the same IKJT first. */
+int recd_pool_fwd_csr(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                      const float* const* tables, const int64_t* table_rows,
+                      const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                      const int64_t* counts, const int32_t* const* csr_start,
+                      const uint32_t* const* csr_rows, float* const* pooled_out,
+                      float* const* out, int64_t* err, recd_stream_t stream);
+
 /* Owner-side pooled lookup whose output rows go straight to the sources'
  * receive buffers (the all-to-all of partial rows fused into the pooling):
  * feature f's row u is stored at seg_dst[f * num_segs + s] + (u - seg_row0[f][s]) * dim
@@ -240,6 +253,19 @@ int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, int32_t dim, 
  * SGD).  _prepare = INVERSE | OCCURRENCES, _finish = GRAD | SCATTER.  With
  * OCCURRENCES on a side stream, GRAD only waits for INVERSE and runs while the
  * sort finishes. */
+/* Where recd_pool_bwd's scratch holds the inverse CSR (valid once the
+ * RECD_BWD_INVERSE stage ran; same arguments as the stages): per feature,
+ * csr_start_out[f] -> int32[B + 1] row starts, csr_rows_out[f] -> uint32[B]
+ * batch rows grouped by unique row (NULL for identity features).  Launches
+ * nothing. */
+int recd_pool_bwd_csr(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                      float* const* tables, const int64_t* table_rows,
+                      const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                      const int64_t* value_caps, const int64_t* counts,
+                      const int64_t* const* inverse, const float* const* grad_out, float lr,
+                      int32_t apply_sgd, int64_t* const* grad_ids_out, float* const* grad_rows_out,
+                      int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
+                      const int32_t** csr_start_out, const uint32_t** csr_rows_out);
 #define RECD_BWD_INVERSE 1
 #define RECD_BWD_OCCURRENCES 2
 #define RECD_BWD_GRAD 4

@@ -61,6 +61,10 @@ _SIGS = {
                                      _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_pool_bwd_finish": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp,
                                     _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_pool_bwd_csr": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _pp,
+                                 _f32, _i32, _pp, _pp, _vp, _vp, _sz, _pp, _pp]),
+    "recd_pool_fwd_csr": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _pp, _pp, _pp,
+                                 _pp, _vp, _vp]),
     "recd_pool_bwd_stages": (_i32, [_i32, _i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp,
                                     _pp, _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_wire_bound": (_i64, [_i32, C.POINTER(C.c_char_p), _i64, _i32, _p64, _p64]),

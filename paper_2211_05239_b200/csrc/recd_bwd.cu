@@ -1168,7 +1168,8 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
             float* const* grad_rows_out, int64_t* grad_counts_out, void* scratch,
             size_t scratch_bytes, cudaStream_t stream, int phase = PH_ALL,
             int gsegs = 0, float* const* gseg_dst = nullptr,
-            const int64_t* const* gseg_row0 = nullptr) {
+            const int64_t* const* gseg_row0 = nullptr,
+            const int32_t** csr_start_out = nullptr, const uint32_t** csr_rows_out = nullptr) {
   if (F <= 0 || F > RECD_MAX_FEAT || B <= 0 || dim <= 0 || !counts) return RECD_ERR_ARG;
   if (mode != RECD_POOL_SUM && mode != RECD_POOL_AVG) return RECD_ERR_UNSUPPORTED;
   if (B >= (1ll << 24)) return RECD_ERR_UNSUPPORTED;  // occurrence tags hold u in 24 bits
@@ -1284,6 +1285,14 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   for (int s = 0; s < pl.nts; ++s) maxrows = std::max(maxrows, pl.table_rows[s]);
   p.inv_keys = odd_passes(bits_for(B)) ? sc.inv_k1 : sc.inv_k0;
   p.inv_rows = odd_passes(bits_for(B)) ? sc.inv_v1 : sc.inv_v0;
+  if (csr_start_out) {  // recd_pool_bwd_csr: where the inverse CSR lives, nothing launched
+    for (int f = 0; f < F; ++f) {
+      const int is = pl.feat_is[f];
+      csr_start_out[f] = (do_grad && is >= 0) ? sc.csr_start + (int64_t)is * (B + 1) : nullptr;
+      csr_rows_out[f] = (do_grad && is >= 0) ? p.inv_rows + (int64_t)is * B : nullptr;
+    }
+    return RECD_OK;
+  }
   const bool odd = odd_passes(bits_for(maxrows));
   // the scatter's sorted occurrences: per-value sort result, or with runs the
   // expansion's output (the buffer pair the heads sort did not end in)
@@ -1551,6 +1560,22 @@ extern "C" int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, in
                  uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
                  grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
                  (cudaStream_t)stream, PH_FINISH);
+}
+
+extern "C" int recd_pool_bwd_csr(int32_t num_features, int64_t batch_size, int32_t dim,
+                                 int32_t mode, float* const* tables, const int64_t* table_rows,
+                                 const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                                 const int64_t* value_caps, const int64_t* counts,
+                                 const int64_t* const* inverse, const float* const* grad_out,
+                                 float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
+                                 float* const* grad_rows_out, int64_t* grad_counts_out,
+                                 void* scratch, size_t scratch_bytes,
+                                 const int32_t** csr_start_out, const uint32_t** csr_rows_out) {
+  if (!csr_start_out || !csr_rows_out) return RECD_ERR_ARG;
+  return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
+                 uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
+                 grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes, nullptr,
+                 PH_INV, 0, nullptr, nullptr, csr_start_out, csr_rows_out);
 }
 
 extern "C" int recd_pool_bwd_stages(int32_t stages, int32_t num_features, int64_t batch_size,

@@ -58,7 +58,19 @@ struct PoolParams {
   int nseg;
   const int64_t* seg_row0[RECD_MAX_FEAT];   // device: nseg bases, ascending
   float* seg_dst[RECD_MAX_FEAT][RECD_PEER_MAXSEG];
+  // optional fused expansion through the inverse CSR (recd_pool_fwd_csr): the
+  // pooled row u goes straight to out[f][i] for the batch rows i of u,
+  // csr_rows[f][csr_start[f][u] .. csr_start[f][u + 1]); pooled[f] may be null
+  const int32_t* csr_start[RECD_MAX_FEAT];
+  const uint32_t* csr_rows[RECD_MAX_FEAT];
 };
+
+// pooled row u of feature f -> its destination(s): with a CSR, the batch rows
+// of u (streaming stores: written once, read by the dense model), plus the
+// pooled buffer if one is given; else the pooled buffer / peer segment
+template <class C>
+__device__ __forceinline__ void store_pooled(const PoolParams& p, int f, int64_t u,
+                                             const ColWork& cw, const float (&acc)[C::VW]);
 
 // destination row of pooled row u of feature f (peer segment or local buffer)
 __device__ __forceinline__ float* pooled_row(const PoolParams& p, int f, int64_t u) {
@@ -67,6 +79,33 @@ __device__ __forceinline__ float* pooled_row(const PoolParams& p, int f, int64_t
   const int64_t* r0 = p.seg_row0[f];
   while (s + 1 < p.nseg && __ldg(r0 + s + 1) <= u) ++s;
   return p.seg_dst[f][s] + (u - __ldg(r0 + s)) * p.D;
+}
+
+template <class C>
+__device__ __forceinline__ void store_pooled(const PoolParams& p, int f, int64_t u,
+                                             const ColWork& cw, const float (&acc)[C::VW]) {
+  const int32_t* cs = p.csr_start[f];
+  if (cs) {
+    const int32_t c0 = __ldg(cs + u), c1 = __ldg(cs + u + 1);
+    const uint32_t* R = p.csr_rows[f];
+    float* o = p.out[f] + cw.lo;
+    const int lane = threadIdx.x & 31;
+    for (int32_t j0 = c0; j0 < c1; j0 += 32) {
+      const uint32_t mine = (j0 + lane < c1) ? __ldg(R + j0 + lane) : 0u;
+      const int m = min(32, c1 - j0);
+      for (int t = 0; t < m; ++t) {
+        const uint32_t i = __shfl_sync(0xffffffffu, mine, t);
+        float* dst = o + (int64_t)i * p.D;
+        if constexpr (C::VW == 4) {
+          if (C::FULL || cw.ok) __stcs(reinterpret_cast<float4*>(dst), make_float4(acc[0], acc[1], acc[2], acc[3]));
+        } else {
+          C::st(dst, cw.ok, acc);
+        }
+      }
+    }
+    if (!p.pooled[f]) return;
+  }
+  C::st(pooled_row(p, f, u) + cw.lo, cw.ok, acc);
 }
 
 template <class C>
@@ -99,7 +138,7 @@ __global__ void __launch_bounds__(256, RECD_POOL_MINB) k_pool_fwd(const __grid_c
     row.window(a);
     float acc[C::VW];
     pool_row<C>(row, a, e - a, p.mode, cw.ok, acc);
-    C::st(pooled_row(p, f, u) + cw.lo, cw.ok, acc);
+    store_pooled<C>(p, f, u, cw, acc);
   }
 }
 
@@ -474,7 +513,7 @@ __global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_
         for (int k = 0; k < 4; ++k) acc[k] = __fdiv_rn(acc[k], fl);
       }
     }
-    C::st(pooled_row(p, f, u) + cw.lo, cw.ok, acc);
+    store_pooled<C>(p, f, u, cw, acc);
   }
   cp_async_wait<0>();
 }
@@ -533,13 +572,15 @@ static unsigned expand_grid(int64_t batch_size, int64_t tasks_per_32) {
 
 using namespace recd;
 
-extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
-                             const float* const* tables, const int64_t* table_rows,
-                             const int64_t* const* uvalues, const int64_t* const* uoffsets,
-                             const int64_t* counts, const int64_t* const* inverse,
-                             float* const* pooled_out, float* const* out, int64_t* err,
-                             recd_stream_t stream_) {
+static int pool_fwd_impl(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                         const float* const* tables, const int64_t* table_rows,
+                         const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                         const int64_t* counts, const int64_t* const* inverse,
+                         const int32_t* const* csr_start, const uint32_t* const* csr_rows,
+                         float* const* pooled_out, float* const* out, int64_t* err,
+                         recd_stream_t stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
+  const bool csr = csr_start != nullptr;
   const bool share = (mode & RECD_POOL_SHARE) != 0;
   mode &= ~RECD_POOL_SHARE;
   if (num_features <= 0 || batch_size < 0 || dim <= 0 || mode < 0 || mode > 2 || !counts || !err)
@@ -562,8 +603,15 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
       p.uvalues[f] = uvalues[f0 + f];
       p.uoffsets[f] = uoffsets[f0 + f];
       p.inverse[f] = inverse ? inverse[f0 + f] : nullptr;
-      p.pooled[f] = pooled_out[f0 + f];
+      p.pooled[f] = pooled_out ? pooled_out[f0 + f] : nullptr;
       p.out[f] = out ? out[f0 + f] : nullptr;
+      if (csr) {
+        p.csr_start[f] = csr_start[f0 + f];
+        p.csr_rows[f] = csr_rows[f0 + f];
+        if (!p.csr_start[f] || !p.csr_rows[f] || !p.out[f] || (dim % 4 == 0 && (uintptr_t)p.out[f] % 16))
+          return RECD_ERR_ARG;
+        if (!p.pooled[f]) p.pooled[f] = p.out[f];  // (alignment check below; not written)
+      }
       if (!p.tables[f] || !p.uoffsets[f] || !p.pooled[f]) return RECD_ERR_ARG;
       if (dim % 2 == 0 && ((uintptr_t)p.tables[f] % 8 || (uintptr_t)p.pooled[f] % 8 ||
                            (p.out[f] && (uintptr_t)p.out[f] % 8)))
@@ -571,6 +619,11 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
     }
     bool any_expand = false;
     for (int f = 0; f < p.F; ++f) any_expand |= (p.out[f] != nullptr && p.out[f] != p.pooled[f]);
+    if (csr) {
+      any_expand = false;
+      for (int f = 0; f < p.F; ++f)
+        if (!pooled_out || !pooled_out[f0 + f]) p.pooled[f] = nullptr;
+    }
     int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, 1, {
       const unsigned grid = grid_for(batch_size * p.F * col_blocks<C>(dim));
       hook_before("k_pool_fwd", stream);
@@ -587,6 +640,29 @@ extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t d
     RECD_LAUNCH_CHECK();
   }
   return RECD_OK;
+}
+
+extern "C" int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
+                             const float* const* tables, const int64_t* table_rows,
+                             const int64_t* const* uvalues, const int64_t* const* uoffsets,
+                             const int64_t* counts, const int64_t* const* inverse,
+                             float* const* pooled_out, float* const* out, int64_t* err,
+                             recd_stream_t stream) {
+  if (!pooled_out) return RECD_ERR_ARG;
+  return pool_fwd_impl(num_features, batch_size, dim, mode, tables, table_rows, uvalues, uoffsets,
+                       counts, inverse, nullptr, nullptr, pooled_out, out, err, stream);
+}
+
+extern "C" int recd_pool_fwd_csr(int32_t num_features, int64_t batch_size, int32_t dim,
+                                 int32_t mode, const float* const* tables,
+                                 const int64_t* table_rows, const int64_t* const* uvalues,
+                                 const int64_t* const* uoffsets, const int64_t* counts,
+                                 const int32_t* const* csr_start, const uint32_t* const* csr_rows,
+                                 float* const* pooled_out, float* const* out, int64_t* err,
+                                 recd_stream_t stream) {
+  if (!csr_start || !csr_rows || !out) return RECD_ERR_ARG;
+  return pool_fwd_impl(num_features, batch_size, dim, mode, tables, table_rows, uvalues, uoffsets,
+                       counts, nullptr, csr_start, csr_rows, pooled_out, out, err, stream);
 }
 
 // Owner-side pooling whose rows go straight to the sources' receive buffers

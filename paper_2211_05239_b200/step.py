@@ -126,6 +126,12 @@ class TrainStep:
         self.mode_id = _lib.POOL_MODES[op]
         self.lr = float(lr)
         self.overlap = bool(overlap)
+        # dedup mode, big batches: the lookup writes the batch rows itself
+        # through the backward's inverse CSR instead of a separate k_expand
+        # (cfg2 4.53-4.57 vs 4.56-4.58 ms; cfg1 0.163 vs 0.157 ms, so not for
+        # small batches).  RECD_FUSED_EXPAND=0/1 forces it off / on.
+        fx = os.environ.get("RECD_FUSED_EXPAND")
+        self.fused_expand = mode == "dedup" and (fx != "0" if fx else self.B >= 32768)
         self.pipeline = bool(pipeline)
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         self.tables = [tables[k] for k in self.keys]
@@ -264,6 +270,28 @@ class TrainStep:
                                     None, st.err.data_ptr(), stream)
         _lib.check(rc, "recd_pool_fwd")
 
+    def _csr(self, stage=None, slot=None):
+        """(csr_start, csr_rows) pointer arrays of the inverse CSR in the
+        stage's backward scratch (recd_pool_bwd_csr; dedup mode)."""
+        a = self.args(stage, slot)
+        if getattr(a, "csr", None) is None:
+            cs, cr = (C.c_void_p * self.F)(), (C.c_void_p * self.F)()
+            args = self._bwd_args(0, stage, slot)[:-1]
+            _lib.check(self.lib.recd_pool_bwd_csr(*args, cs, cr), "recd_pool_bwd_csr")
+            a.csr = (cs, cr)
+        return a.csr
+
+    def forward_expand(self, stream: int, stage=None, slot=None, share: bool = False) -> None:
+        """Pooled lookup with the expansion fused through the backward's inverse
+        CSR (recd_pool_fwd_csr: no pooled buffer; needs BWD_INVERSE first)."""
+        a, st = self.args(stage, slot), self._st(stage)
+        cs, cr = self._csr(stage, slot)
+        mode = self.mode_id | (_lib.POOL_SHARE if share else 0)
+        rc = self.lib.recd_pool_fwd_csr(self.F, self.B, self.D, mode, a.tables, a.rows, a.feat_vals,
+                                        a.feat_offs, a.counts_ptr, cs, cr, None, a.out,
+                                        st.err.data_ptr(), stream)
+        _lib.check(rc, "recd_pool_fwd_csr")
+
     def expand(self, stream: int, stage=None, slot=None) -> None:
         """out[i] = pooled[inverse[i]] (k_expand; nothing to do in kjt mode)."""
         if self.mode != "dedup":
@@ -305,10 +333,26 @@ class TrainStep:
             self.expand(s)
             self.backward(s)
             return
+        main = torch.cuda.current_stream(self.dev)
+        if self.fused_expand:
+            # main stream: dedup, inverse CSR, lookup with the expansion fused
+            # through the CSR, unique-row gradients, then the scatter + SGD
+            # after the side stream's occurrence sort
+            ms = main.cuda_stream
+            self.dedup(ms)
+            self.backward_stages(_lib.BWD_INVERSE, ms)
+            self._ev_fork.record(main)
+            self._side.wait_event(self._ev_fork)
+            self.backward_stages(_lib.BWD_OCCURRENCES, self._side.cuda_stream)
+            self._ev_join.record(self._side)
+            self.forward_expand(ms, share=True)
+            self.backward_stages(_lib.BWD_GRAD, ms)
+            main.wait_event(self._ev_join)
+            self.backward_stages(_lib.BWD_SCATTER, ms)
+            return
         # side stream: inverse CSR, then the occurrence sort; main stream: lookup,
         # expansion, unique-row gradients (after the CSR only, so they run while
         # the sort finishes), then the scatter + SGD after the sort
-        main = torch.cuda.current_stream(self.dev)
         self.dedup(main.cuda_stream)
         self._ev_fork.record(main)
         self._side.wait_event(self._ev_fork)

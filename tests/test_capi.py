@@ -82,3 +82,29 @@ def test_scratch_sizes_cover_every_backward_entry_point():
                 P(fake[4], fake[5]), caps, fake[6].value, P(fake[6], fake[6]), P(fake[7], fake[7]),
                 C.c_float(0.1), 1, None, None, None, fake[7].value, nb, None)
         assert rc != 3, rc
+
+
+def test_pool_bwd_csr_points_into_scratch():
+    """recd_pool_bwd_csr launches nothing: on the CPU it returns where the
+    inverse CSR of each feature lives inside the backward scratch (features
+    of one dedup group share one CSR)."""
+    import ctypes as C
+    from paper_2211_05239_b200 import _lib
+    lib = _lib.load()
+    F, rows, D, B = 3, 3000, 8, 1024
+    caps = _lib.i64s([500, 700, 600])
+    fake = [C.c_void_p(4096 * (i + 1)) for i in range(8)]
+    P = lambda *xs: (C.c_void_p * len(xs))(*[x.value for x in xs])  # noqa: E731
+    nb = lib.recd_pool_bwd_scratch_bytes(F, B, D, caps)
+    base = 1 << 40
+    cs, cr = (C.c_void_p * F)(), (C.c_void_p * F)()
+    inv = P(fake[6], fake[6], fake[7])   # features 0 and 1 share an inverse
+    rc = lib.recd_pool_bwd_csr(F, B, D, 0, P(fake[0], fake[1], fake[2]), _lib.i64s([rows] * F),
+                               P(fake[2], fake[3], fake[4]), P(fake[4], fake[5], fake[0]), caps,
+                               fake[6].value, inv, P(fake[7], fake[7], fake[7]), C.c_float(0.1), 1,
+                               None, None, None, base, nb, cs, cr)
+    assert rc == 0
+    for f in range(F):
+        assert base <= cs[f] < base + nb and base <= cr[f] < base + nb
+    assert cs[0] == cs[1] and cr[0] == cr[1] and cs[2] != cs[0]
+    assert cs[2] - cs[0] == 4 * (B + 1) and cr[2] - cr[0] == 4 * B

@@ -28,8 +28,9 @@ def _batches(n, b):
                                      SPECS, b) for seed in range(n)]
 
 
-@pytest.mark.parametrize("mode", ["dedup", "kjt"])
-def test_one_graph_twenty_batches(mode):
+@pytest.mark.parametrize("mode,fused", [("dedup", "0"), ("dedup", "1"), ("kjt", "0")])
+def test_one_graph_twenty_batches(mode, fused, monkeypatch):
+    monkeypatch.setenv("RECD_FUSED_EXPAND", fused)
     b, vocab, dim, lr = 1024, 4000, 32, 0.05
     batches = _batches(20, b)
     keys = [s.key for s in SPECS]

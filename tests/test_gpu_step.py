@@ -40,9 +40,13 @@ def _oracle_step(batch, w0s, grads, lr):
     return outs, w1s
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
 @pytest.mark.parametrize("overlap", [True, False])
 @pytest.mark.parametrize("graph", [True, False])
-def test_train_step_matches_oracle(overlap, graph):
+def test_train_step_matches_oracle(overlap, graph, fused, monkeypatch):
+    """fused: the lookup expands through the backward's inverse CSR
+    (recd_pool_fwd_csr) instead of k_expand."""
+    monkeypatch.setenv("RECD_FUSED_EXPAND", fused)
     b, vocab, dim, lr = 2048, 5000, 128, 0.05
     batch = _batch(b, [4, 24, 64], vocab, seed=3)
     keys = list(batch.keys)
@@ -155,3 +159,39 @@ def test_module_deferred_checks():
         ebc.check()
     np.testing.assert_array_equal(t.weights.cpu().numpy(), w0)
     ebc.check()   # errors are reported once
+
+
+def test_pool_fwd_csr_writes_batch_rows_and_pooled():
+    """recd_pool_fwd_csr with a pooled buffer as well: both outputs equal the
+    oracle's pooled rows and their expansion."""
+    import ctypes as C
+
+    from paper_2211_05239_b200 import _lib
+    b, vocab, dim = 1024, 3000, 64
+    batch = _batch(b, [6, 40], vocab, seed=11)
+    keys = list(batch.keys)
+    rng = np.random.default_rng(5)
+    w0s = {k: rng.uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32) for k in keys}
+    tables = {k: R.EmbeddingTable(k, vocab, dim, torch.as_tensor(w0s[k], device="cuda").clone())
+              for k in keys}
+    caps = {k: int(batch.values[k].size) for k in keys}
+    step = TrainStep([[k] for k in keys], b, caps, tables, "sum", 0.0, "dedup")
+    step.load_batch(batch.values, batch.offsets)
+    s = torch.cuda.current_stream().cuda_stream
+    step.dedup(s)
+    step.backward_stages(_lib.BWD_INVERSE, s)
+    a = step.args()
+    cs, cr = step._csr()
+    pooled = [torch.full((b, dim), float("nan"), device="cuda") for _ in keys]
+    out = [torch.full((b, dim), float("nan"), device="cuda") for _ in keys]
+    rc = step.lib.recd_pool_fwd_csr(step.F, b, dim, 0, a.tables, a.rows, a.feat_vals, a.feat_offs,
+                                    a.counts_ptr, cs, cr, _lib.ptrs(pooled), _lib.ptrs(out),
+                                    step._st(None).err.data_ptr(), s)
+    assert rc == 0
+    torch.cuda.synchronize()
+    for f, k in enumerate(keys):
+        inv, [(uv, uo)] = oracle.build_ikjt_arrays([(batch.values[k], batch.offsets[k])])
+        ref = oracle.pooled_lookup(uv, uo, w0s[k], "sum")
+        np.testing.assert_array_equal(pooled[f][: uo.size].cpu().numpy(), ref)
+        np.testing.assert_array_equal(out[f].cpu().numpy(), oracle.expand(ref, inv))
+    assert C.c_void_p(cs[0]).value is not None
