@@ -519,19 +519,26 @@ def run_single(args, dev):
     value = B / (ms / 1e3)
 
     # --------------------------------------- per-phase timing (roofline)
-    phases = {"dedup": [], "pool": [], "expand": [], "bwd": []}
+    # serial, one stream (the step overlaps the occurrence sort with the lookup)
+    L = R._lib
+    if args.mode == "dedup" and step.fused_expand:
+        calls = {"dedup": step.dedup,
+                 "bwd_inverse": lambda s_: step.backward_stages(L.BWD_INVERSE, s_),
+                 "pool_expand": step.forward_expand,
+                 "bwd_occurrences": lambda s_: step.backward_stages(L.BWD_OCCURRENCES, s_),
+                 "bwd_grad": lambda s_: step.backward_stages(L.BWD_GRAD, s_),
+                 "bwd_scatter": lambda s_: step.backward_stages(L.BWD_SCATTER, s_)}
+    else:
+        calls = {"dedup": step.dedup, "pool": step.forward, "expand": step.expand,
+                 "bwd": step.backward}
+    phases = {k: [] for k in calls}
     s = stream.cuda_stream
     for _ in range(max(3, min(args.steps, 20))):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)]
         ev[0].record(stream)
-        step.dedup(s)
-        ev[1].record(stream)
-        step.forward(s)
-        ev[2].record(stream)
-        step.expand(s)
-        ev[3].record(stream)
-        step.backward(s)
-        ev[4].record(stream)
+        for i, fn in enumerate(calls.values()):
+            fn(s)
+            ev[i + 1].record(stream)
         torch.cuda.synchronize()
         for i, name in enumerate(phases):
             phases[name].append(ev[i].elapsed_time(ev[i + 1]))
@@ -548,6 +555,11 @@ def run_single(args, dev):
                          8 * N_u + 8 * U_tot + 4 * D * N_u + 4 * D * U_tot),
           "k_scatter": (8 * N_u + 4 * D * U_tot + 8 * D * N_ids,
                         8 * N_u + 4 * D * N_u + 8 * D * N_ids)}
+    if args.mode == "dedup" and step.fused_expand:
+        # the lookup stores every batch row itself (recd_pool_fwd_csr): out
+        # rows instead of pooled rows, plus the CSR (int32 starts + rows)
+        kb["k_pool_fwd"] = (8 * N_u + 8 * U_tot + 4 * D * N_ids + 4 * D * B * K + 8 * B * K,
+                            8 * N_u + 8 * U_tot + 4 * D * N_u + 4 * D * B * K + 8 * B * K)
     if args.mode == "kjt":
         kb = {"k_pool_fwd": (8 * N_kjt + 4 * D * N_ids + 4 * D * B * K,
                              8 * N_kjt + 4 * D * N_kjt + 4 * D * B * K),
