@@ -90,9 +90,14 @@ struct BwdParams {
   uint32_t* occ_vals;     // tag = (f << 24) | u
   int64_t* run_part;      // [total_rc_chunks] exclusive run counts (grad-output mode)
   int32_t* bad;           // set by k_occ when an ID is outside [0, rows): no table update
-  // diagonal-run occurrences (RECD_BWD_RUNS): see k_runs_detect / k_runs_expand
+  // diagonal-run occurrences (RECD_BWD_RUNS): see k_rv*
   uint32_t* head_tag;     // [occ cap] tag of each run head (indexed by the sort's value)
+  uint32_t* head_pos;     // [occ cap] position of the head in its unique row
   uint32_t* head_len;     // [occ cap] run length k (rows tag .. tag + k - 1)
+  int64_t* rv_blk;        // [value blocks] heads per block -> exclusive head offsets
+  int32_t* fix_list;      // [RV_FIX_CAP][3] IDs whose runs overlap: (segment, first, end head)
+  uint32_t* fix_count;
+  int seg_feat[RECD_MAX_FEAT];  // the feature of each (single-feature) table segment
   int64_t* head_count;    // [nts] run heads per table segment (the heads sort's counts)
   int64_t* head_off;      // [occ cap] run lengths in sorted order -> exclusive offsets
   int32_t* fallback;      // set when some ID's runs need per-value occurrences
@@ -105,9 +110,9 @@ struct BwdParams {
   uint64_t gu_mask;                     // k_grad_u(_flat): features to reduce (bit f)
   int64_t sc_chunk_lo, sc_chunk_hi;     // k_scatter: chunk window [lo, hi) of this launch
   int occ_bits;                         //        over this many key bits
-  int64_t ex_chunk0[RECD_MAX_FEAT];     // k_runs_expand: first RC_EXP chunk of each segment
+  int64_t ex_chunk0[RECD_MAX_FEAT];     // k_rv_expand: first RV_EX_CH block of each segment
   int64_t occ_blk0[RECD_MAX_FEAT + 1];  // k_occ: first block of each feature (capacity)
-  int64_t oc_ch;                         // k_occ / k_runs: unique values per block
+  int64_t oc_ch;                         // k_occ / k_rv: unique values per block
   // optional scatter of grad_u rows to peers (fused source -> owner push): row u
   // of feature f goes to gseg_dst[f][j] + (*gseg_row0[f][j] + u) * D, j < gsegs
   int gsegs;
@@ -475,60 +480,61 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
 // Diagonal-run occurrences (RECD_BWD_RUNS=1).  In session data consecutive
 // unique rows of a history feature are windows shifted by one: the ID at
 // (u, p) is usually the ID at (u - 1, p + 1).  A diagonal of occurrences --
-// one ID in rows u .. u + k - 1 at positions p, p - 1, ... -- becomes ONE sort
-// element (ID, head index) carrying (tag of row u, k), so the occurrence sort
-// orders ~N_ids run heads instead of N_u values (3.3x fewer at cfg2), and
-// k_runs_expand writes the per-value (ID, tag) array the scatter reads.
-//
+// one ID in rows u .. u + k - 1 at positions p, p - 1, ... -- is ONE sort
+// element (ID, head index), so the occurrence sort orders the run heads
+// (~N_ids) instead of every unique value (N_u, 3.3x more at cfg2):
+//   k_rv<0>      heads per value block (a value heads a run unless it repeats
+//                its diagonal predecessor)
+//   scan         block offsets -> heads numbered in (u, p) order per segment
+//   k_rv<1>      heads written in that order (ID, index; tag, position) + the
+//                sort's digit histograms
+//   k_rv_len     run length of every head (walk down its diagonal)
+//   sort         heads by ID (stable: each ID's runs stay in (u, p) order)
+//   k_rv_lens    run lengths in sorted order (+ the IDs whose runs overlap)
+//   scan         -> expanded offsets
+//   k_rv_expand  per-value (ID, tag) array, coalesced, for the unchanged scatter
+//   k_rv_fix     the overlapping IDs' tags re-sorted in place
 // Exactness: the oracle adds, per ID, grad_u[t] over its occurrences in
 // non-decreasing tag order (equal tags add the same row, so their order does
-// not matter).  The expansion sorts each ID's runs by head tag; if no two runs
-// of the ID overlap in tags, concatenating them is exactly that order.  Runs
-// overlap only when a row holds the ID twice; such an ID (or one with more than
-// 32 runs) sets `fallback`, and the batch's occurrences are then rebuilt per
-// value (k_occ + the full sort, gated on the flag) -- slower, never different.
+// not matter).  An ID's runs come out of the sort in head order; concatenated
+// they are already non-decreasing unless a run starts before the previous one
+// ends (the ID occurs twice in one row): those IDs are listed and their
+// expanded tags sorted (k_rv_fix; > RV_FIX_MAX values or a full list set
+// `fallback`, and the gated per-value occurrences + full sort rebuild the
+// batch -- slower, never different).  Only for one feature per table segment.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int64_t urow_end(const int64_t* uo, int64_t U, int64_t NV, int64_t u) {
-  return (u + 1 < U) ? __ldg(uo + u + 1) : NV;
-}
+constexpr int RV_FIX_MAX = 4096;   // values of one overlapping ID re-sorted in shared memory
+constexpr int RV_FIX_CAP = 65536;  // overlapping IDs listed per batch
+constexpr int RV_EX_CH = 2048;     // expanded values per k_rv_expand block
 
-// 0 if the occurrence (u, p) of ID v continues the run of (u - 1, p + 1), else
-// the length k >= 1 of the run it heads
-__device__ __forceinline__ uint32_t run_head_len(const int64_t* uv, const int64_t* uo, int64_t U,
-                                                 int64_t NV, int64_t u, int64_t p, int64_t v) {
-  if (u >= 1) {
-    const int64_t b = __ldg(uo + u - 1);
-    if (b + p + 1 < __ldg(uo + u) && __ldg(uv + b + p + 1) == v) return 0u;
-  }
-  uint32_t k = 1;
-  for (int64_t j = 1; u + j < U && p - j >= 0; ++j) {
-    const int64_t a = __ldg(uo + u + j);
-    if (a + p - j >= urow_end(uo, U, NV, u + j)) break;
-    if (__ldg(uv + a + p - j) != v) break;
-    ++k;
-  }
-  return k;
-}
-
-// value-parallel (the k_occ block decomposition): run heads of a block are
-// written at a block range taken from the segment's head counter (their order
-// inside an ID is restored by the expansion's tag sort)
-__global__ void __launch_bounds__(256) k_runs_detect(const __grid_constant__ BwdParams p,
-                                                     uint32_t* keys, uint32_t* vals) {
+template <int MODE>
+__global__ void __launch_bounds__(256) k_rv(const __grid_constant__ BwdParams p, uint32_t* keys,
+                                            uint32_t* vals) {
   int f = 0;
   while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
-  const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * p.oc_ch;
+  const int64_t blk = blockIdx.x;
+  const int64_t j0 = (blk - p.occ_blk0[f]) * p.oc_ch;
   const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
-  if (j0 >= NV) return;
-  const int64_t j1 = min(NV, j0 + p.oc_ch);
   const int tid = threadIdx.x;
+  if (j0 >= NV) {
+    if (MODE == 0 && tid == 0) p.rv_blk[blk] = 0;
+    return;
+  }
+  const int64_t j1 = min(NV, j0 + p.oc_ch);
   const int64_t* uo = p.uoffsets[f];
   const int64_t* src = p.uvalues[f];
   const int ts = p.feat_ts[f];
   const uint64_t rows = (uint64_t)p.ts_rows[ts];
-  __shared__ int64_t s_u0, s_base;
-  __shared__ int64_t s_uo[OC_MAXR + 1];
+  __shared__ int64_t s_u0;
+  __shared__ int64_t s_uo[OC_MAXR + 2];  // s_uo[t] = start of row u0 - 1 + t
   __shared__ int64_t s_scan[32];
+  __shared__ uint32_t s_hist[SORT_HIST_PASSES][256];
+  uint32_t* const hist = MODE == 1 ? p.occ_hist : nullptr;
+  const int npass = hist ? (p.occ_bits + 7) / 8 : 0;
+  if (hist)
+    for (int i = tid; i < SORT_HIST_PASSES * 256; i += 256) (&s_hist[0][0])[i] = 0u;
+  const int64_t hbase = MODE == 1 ? p.ts_base[ts] + p.rv_blk[blk] : 0;
+  int64_t count = 0;  // heads of the block so far (block-uniform)
   if (tid < 32) {
     const int64_t u = warp_last_le(uo, U, j0, tid);
     if (tid == 0) s_u0 = u;
@@ -537,159 +543,223 @@ __global__ void __launch_bounds__(256) k_runs_detect(const __grid_constant__ Bwd
   int64_t u0 = s_u0;
   while (true) {
     const int nr = (int)min((int64_t)OC_MAXR, U - u0);
-    for (int t = tid; t <= nr; t += 256) {
-      const int64_t u = u0 + t;
-      s_uo[t] = (u < U) ? uo[u] : NV;
+    for (int t = tid; t <= nr + 1; t += 256) {
+      const int64_t x = u0 - 1 + t;
+      s_uo[t] = x < 0 ? 0 : (x < U ? uo[x] : NV);
     }
     __syncthreads();
-    const int64_t covered = s_uo[nr];
-    const int64_t qa = max(j0, s_uo[0]), qb = min(j1, covered);
+    const int64_t covered = s_uo[nr + 1];
+    const int64_t qa = max(j0, s_uo[1]), qb = min(j1, covered);
     int r = 0;
     for (int64_t base = qa; base < qb; base += 256) {  // block-uniform rounds
       const int64_t q = base + tid;
-      uint32_t k = 0;
-      int64_t v = 0;
+      bool head = false;
+      int64_t v = 0, pp = 0;
       if (q < qb) {
-        if (s_uo[min(r + 8, nr)] <= q) {
+        if (s_uo[min(r + 8, nr) + 1] <= q) {
           int lo = r + 8, hi = nr - 1;
           while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (s_uo[mid] <= q) lo = mid; else hi = mid - 1;
+            if (s_uo[mid + 1] <= q) lo = mid; else hi = mid - 1;
           }
           r = lo;
         } else {
-          while (s_uo[r + 1] <= q) ++r;
+          while (s_uo[r + 2] <= q) ++r;
         }
+        pp = q - s_uo[r + 1];
         v = __ldg(src + q);
-        k = run_head_len(src, uo, U, NV, u0 + r, q - s_uo[r], v);
+        bool cont = false;
+        if (u0 + r >= 1) {  // diagonal predecessor (u - 1, p + 1)
+          const int64_t ps = s_uo[r];
+          cont = pp + 1 < s_uo[r + 1] - ps && __ldg(src + ps + pp + 1) == v;
+        }
+        head = !cont;
       }
-      int64_t tot;
-      const int64_t rank = block_exclusive_scan<256>(k ? 1 : 0, s_scan, &tot);
-      if (tid == 0) s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(p.head_count + ts),
-                                             (unsigned long long)tot) : 0;
-      __syncthreads();
-      if (k) {
-        const int64_t o = p.ts_base[ts] + s_base + rank;
-        const bool in = (uint64_t)v < rows;
-        if (!in) *p.bad = 1;
-        keys[o] = in ? (uint32_t)v : 0u;
-        vals[o] = (uint32_t)o;
-        p.head_tag[o] = ((uint32_t)f << 24) | (uint32_t)(u0 + r);
-        p.head_len[o] = k;
+      if (MODE == 0) {
+        count += __syncthreads_count(head);
+      } else {
+        int64_t tot;
+        const int64_t rank = block_exclusive_scan<256>(head ? 1 : 0, s_scan, &tot);
+        if (head) {
+          const int64_t o = hbase + count + rank;
+          const bool in = (uint64_t)v < rows;
+          if (!in) *p.bad = 1;
+          const uint32_t key = in ? (uint32_t)v : 0u;
+          keys[o] = key;
+          vals[o] = (uint32_t)o;
+          p.head_tag[o] = ((uint32_t)f << 24) | (uint32_t)(u0 + r);
+          p.head_pos[o] = (uint32_t)pp;
+          for (int ps = 0; ps < npass; ++ps) atomicAdd(&s_hist[ps][(key >> (8 * ps)) & 255u], 1u);
+        }
+        count += tot;
       }
-      __syncthreads();
     }
     if (covered >= j1) break;
     __syncthreads();
     u0 += nr;
   }
+  if (MODE == 0) {
+    if (tid == 0) p.rv_blk[blk] = count;
+  } else if (hist) {
+    __syncthreads();
+    const int64_t row0 = (int64_t)ts * SORT_HIST_PASSES * 256;
+    for (int i = tid; i < npass * 256; i += 256) {
+      const uint32_t c = (&s_hist[0][0])[i];
+      if (c) atomicAdd(&hist[row0 + i], c);
+    }
+  }
+}
+
+// thread per head: run length = rows down the diagonal (u + k, p - k) that hold
+// the head's ID (row starts from global memory: the next row's start is the
+// current row's end, so one new offset + one value per step)
+__global__ void __launch_bounds__(256) k_rv_len(const __grid_constant__ BwdParams p) {
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int s = 0; s < p.nts; ++s) {
+    const int f = p.seg_feat[s];
+    const int64_t n = p.head_count[s], base = p.ts_base[s];
+    const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
+    const int64_t* uo = p.uoffsets[f];
+    const int64_t* src = p.uvalues[f];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += nthr) {
+      const int64_t o = base + j;
+      const int64_t u = p.head_tag[o] & 0xffffffu;
+      int64_t cp = p.head_pos[o];
+      const int64_t v = __ldg(src + __ldg(uo + u) + cp);
+      uint32_t len = 1;
+      int64_t cu = u;
+      int64_t ns = (cu + 1 < U) ? __ldg(uo + cu + 1) : NV;  // start of row cu + 1
+      while (cp >= 1 && cu + 1 < U) {
+        const int64_t ne = (cu + 2 < U) ? __ldg(uo + cu + 2) : NV;
+        if (cp - 1 >= ne - ns || __ldg(src + ns + cp - 1) != v) break;
+        ++len;
+        ++cu;
+        --cp;
+        ns = ne;
+      }
+      p.head_len[o] = len;
+    }
+  }
 }
 
 // sorted head j of segment blockIdx.y -> its run length (scanned into expanded
-// offsets next); grid-stride over the segment's device head count
-__global__ void k_runs_lens(const __grid_constant__ BwdParams p, const uint32_t* svals) {
+// offsets next); the first head of each ID checks whether its runs overlap
+// (a run starting before the previous one's last row) and lists the ID
+__global__ void k_rv_lens(const __grid_constant__ BwdParams p, const uint32_t* skeys,
+                          const uint32_t* svals) {
   const int s = blockIdx.y;
   const int64_t n = p.head_count[s], base = p.ts_base[s];
+  const uint32_t* K = skeys + base;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    p.head_off[base + j] = (int64_t)p.head_len[svals[base + j]];
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t hid = svals[base + j];
+    const uint32_t len = p.head_len[hid];
+    p.head_off[base + j] = (int64_t)len;
+    const uint32_t id = K[j];
+    if (j > 0 && K[j - 1] == id) continue;
+    if (j + 1 >= n || K[j + 1] != id) continue;  // one run: nothing to check
+    uint32_t last = p.head_tag[hid] + len - 1;
+    bool ovl = false;
+    int64_t e = j + 1;
+    for (; e < n && K[e] == id; ++e) {
+      const uint32_t h2 = svals[base + e];
+      const uint32_t t2 = p.head_tag[h2];
+      ovl |= t2 < last;
+      last = max(last, t2 + p.head_len[h2] - 1);
+    }
+    if (ovl) {
+      const uint32_t k = atomicAdd(p.fix_count, 1u);
+      if (k < (uint32_t)RV_FIX_CAP) {
+        p.fix_list[3 * k] = s;
+        p.fix_list[3 * k + 1] = (int32_t)j;
+        p.fix_list[3 * k + 2] = (int32_t)e;
+      } else {
+        *p.fallback = 1;
+      }
+    }
+  }
 }
 
-// warp per RC_EXP sorted heads: every ID group (run of equal sorted keys)
-// starting in the chunk is written out per value in tag order
-constexpr int RC_EXP = 256;
-__global__ void __launch_bounds__(256) k_runs_expand(const __grid_constant__ BwdParams p,
-                                                     const uint32_t* skeys, const uint32_t* svals,
-                                                     int64_t total_chunks) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total_chunks;
-       w += nwarps) {
-    int s = 0;
-    while (s + 1 < p.nts && p.ex_chunk0[s + 1] <= w) ++s;
-    const int64_t n = p.head_count[s];
-    const int64_t lo = (w - p.ex_chunk0[s]) * RC_EXP;
-    if (lo >= n) continue;
-    const int64_t hi = min(n, lo + (int64_t)RC_EXP);
-    const uint32_t* K = skeys + p.ts_base[s];
-    const uint32_t* Vs = svals;                 // head indices are absolute
-    const int64_t* off = p.head_off + p.ts_base[s];
-    uint32_t* ok_ = p.exp_keys + p.ts_base[s];
-    uint32_t* ov_ = p.exp_vals + p.ts_base[s];
-    for (int64_t j0 = lo; j0 < hi; j0 += 32) {
-      const int64_t j = j0 + lane;
-      bool st = false, single = false;
-      uint32_t id = 0;
-      if (j < hi) {
-        id = __ldg(K + j);
-        st = (j == 0) || __ldg(K + j - 1) != id;
-        single = st && (j + 1 == n || __ldg(K + j + 1) != id);
-      }
-      if (single) {  // the common case: the ID has one run -> lane writes it
-        const uint32_t hid = __ldg(Vs + p.ts_base[s] + j);
-        const uint32_t tag = __ldg(p.head_tag + hid), len = __ldg(p.head_len + hid);
-        const int64_t base = off[j];
-        for (uint32_t r = 0; r < len; ++r) {
-          ok_[base + r] = id;
-          ov_[base + r] = tag + r;
-        }
-      }
-      unsigned b = __ballot_sync(0xffffffffu, st && !single);
-      while (b) {  // IDs with several runs: sorted by head tag, checked, written
-        const int src = __ffs(b) - 1;
-        b &= b - 1;
-        const int64_t g = j0 + src;
-        const uint32_t gid = __shfl_sync(0xffffffffu, id, src);
-        const int64_t m = run_end(K, g + 1, n, gid, lane) - g;
-        if (m > 32) {
-          if (lane == 0) *p.fallback = 1;
-          continue;
-        }
-        uint32_t tag = 0xffffffffu, len = 0;
-        if (lane < m) {
-          const uint32_t hid = __ldg(Vs + p.ts_base[s] + g + lane);
-          tag = __ldg(p.head_tag + hid);
-          len = __ldg(p.head_len + hid);
-        }
-#pragma unroll
-        for (int k2 = 2; k2 <= 32; k2 <<= 1) {
-#pragma unroll
-          for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
-            const uint32_t ot = __shfl_xor_sync(0xffffffffu, tag, jj);
-            const uint32_t ol = __shfl_xor_sync(0xffffffffu, len, jj);
-            const bool up = (lane & k2) == 0, lower = (lane & jj) == 0;
-            const bool take = (lower == up) ? ot < tag : ot > tag;
-            if (take) {
-              tag = ot;
-              len = ol;
+// block per RV_EX_CH expanded values of a segment: the heads covering them
+// (two warp searches over the expanded offsets) staged in shared memory, then
+// value e -> (ID, head tag + e - head offset), coalesced stores
+__global__ void __launch_bounds__(256) k_rv_expand(const __grid_constant__ BwdParams p,
+                                                   const uint32_t* skeys, const uint32_t* svals) {
+  int s = 0;
+  while (s + 1 < p.nts && p.ex_chunk0[s + 1] <= (int64_t)blockIdx.x) ++s;
+  const int64_t E = p.seg_count[s], base = p.ts_base[s];
+  const int64_t e0 = ((int64_t)blockIdx.x - p.ex_chunk0[s]) * RV_EX_CH;
+  if (e0 >= E) return;
+  const int64_t e1 = min(E, e0 + (int64_t)RV_EX_CH);
+  const int64_t n = p.head_count[s];
+  const int64_t* off = p.head_off + base;
+  __shared__ int64_t s_j[2];
+  __shared__ int32_t s_off[RV_EX_CH];
+  __shared__ uint32_t s_key[RV_EX_CH], s_tag[RV_EX_CH];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp < 2) {
+    const int64_t j = warp_last_le(off, n, warp == 0 ? e0 : e1 - 1, lane);
+    if (lane == 0) s_j[warp] = j;
+  }
+  __syncthreads();
+  const int64_t jlo = s_j[0];
+  const int nh = (int)(s_j[1] - jlo + 1);
+  for (int i = tid; i < nh; i += 256) {
+    s_off[i] = (int32_t)(off[jlo + i] - e0);
+    s_key[i] = skeys[base + jlo + i];
+    s_tag[i] = p.head_tag[svals[base + jlo + i]];
+  }
+  __syncthreads();
+  uint32_t* ok_ = p.exp_keys + base;
+  uint32_t* ov_ = p.exp_vals + base;
+  for (int64_t e = e0 + tid; e < e1; e += 256) {
+    const int32_t x = (int32_t)(e - e0);
+    int lo = 0, hi = nh - 1;  // last head with s_off <= x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= x) lo = mid; else hi = mid - 1;
+    }
+    ok_[e] = s_key[lo];
+    ov_[e] = s_tag[lo] + (uint32_t)(x - s_off[lo]);
+  }
+}
+
+// block per listed ID: its expanded tags (all one key) sorted in shared memory
+__global__ void __launch_bounds__(256) k_rv_fix(const __grid_constant__ BwdParams p) {
+  __shared__ uint32_t s_t[RV_FIX_MAX];
+  const uint32_t cnt = min(*p.fix_count, (uint32_t)RV_FIX_CAP);
+  for (uint32_t k = blockIdx.x; k < cnt; k += gridDim.x) {
+    const int s = p.fix_list[3 * k];
+    const int64_t j = p.fix_list[3 * k + 1], e = p.fix_list[3 * k + 2];
+    const int64_t base = p.ts_base[s];
+    const int64_t lo = p.head_off[base + j];
+    const int64_t hi = e < p.head_count[s] ? p.head_off[base + e] : p.seg_count[s];
+    const int m = (int)(hi - lo);
+    if (m > RV_FIX_MAX) {
+      if (threadIdx.x == 0) *p.fallback = 1;
+      continue;
+    }
+    int m2 = 1;
+    while (m2 < m) m2 <<= 1;
+    uint32_t* v = p.exp_vals + base + lo;
+    for (int i = threadIdx.x; i < m2; i += blockDim.x) s_t[i] = i < m ? v[i] : 0xffffffffu;
+    __syncthreads();
+    for (int k2 = 2; k2 <= m2; k2 <<= 1)
+      for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
+        for (int i = threadIdx.x; i < m2; i += blockDim.x) {
+          const int x = i ^ jj;
+          if (x > i) {
+            const uint32_t a = s_t[i], b = s_t[x];
+            if (((i & k2) == 0) == (a > b)) {
+              s_t[i] = b;
+              s_t[x] = a;
             }
           }
         }
-        // runs of one ID must not share a row: tag[i + 1] >= tag[i] + len[i]
-        const uint32_t nt = __shfl_down_sync(0xffffffffu, tag, 1);
-        if (__any_sync(0xffffffffu, lane + 1 < m && nt < tag + len)) {
-          if (lane == 0) *p.fallback = 1;
-          continue;
-        }
-        uint32_t incl = len;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-          if (lane >= d) incl += y;
-        }
-        const uint32_t excl = incl - len;
-        const int64_t base = off[g];
-        for (int h = 0; h < m; ++h) {
-          const uint32_t t0 = __shfl_sync(0xffffffffu, tag, h);
-          const uint32_t l0 = __shfl_sync(0xffffffffu, len, h);
-          const uint32_t e0 = __shfl_sync(0xffffffffu, excl, h);
-          for (uint32_t r = lane; r < l0; r += 32) {
-            ok_[base + e0 + r] = gid;
-            ov_[base + e0 + r] = t0 + r;
-          }
-        }
+        __syncthreads();
       }
-    }
+    for (int i = threadIdx.x; i < m; i += blockDim.x) v[i] = s_t[i];
+    __syncthreads();
   }
 }
 
@@ -1015,6 +1085,7 @@ struct Plan {
   std::vector<float*> table;
   std::vector<int64_t> table_rows;  // max rows per table seg
   std::vector<int64_t> ts_base, ts_cap, ts_chunk0;
+  std::vector<int64_t> caps;  // value capacity per feature
   int64_t occ_total, rc_chunks;
   int rc;  // scatter chunk (RC_BIG / RC_SMALL)
 };
@@ -1023,6 +1094,7 @@ Plan make_plan(int F, const int64_t* const* inverse, float* const* tables, const
                const int64_t* caps) {
   Plan pl;
   pl.F = F;
+  pl.caps.assign(caps, caps + F);
   pl.feat_is.assign(F, -1);
   pl.feat_ts.assign(F, -1);
   std::map<const void*, int> is_map, ts_map;
@@ -1068,7 +1140,9 @@ Plan make_plan(int F, const int64_t* const* inverse, float* const* tables, const
 struct BwdScratch {
   int64_t *feat_base, *seg_count, *is_count, *run_part, *scan_part;
   int32_t* bad;
-  uint32_t *head_tag, *head_len;
+  uint32_t *head_tag, *head_pos, *head_len, *fix_count;
+  int64_t *rv_blk, *rv_scan_part;
+  int32_t* fix_list;
   int64_t *head_count, *head_off, *runs_scan_part;
   int32_t* fallback;
   uint32_t* sc_ticket;
@@ -1100,8 +1174,24 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   // expanded offsets (only the full backward uses runs)
   const bool rn = (need & NEED_OCC) && (need & NEED_GRADU);
   s->head_tag = a.take<uint32_t>(rn ? occ : 1);
+  s->head_pos = a.take<uint32_t>(rn ? occ : 1);
   s->head_len = a.take<uint32_t>(rn ? occ : 1);
   s->head_off = a.take<int64_t>(rn ? occ : 1);
+  // value blocks (k_occ's layout at its smallest chunk) and their scan partials
+  int64_t nblk = 1;
+  std::vector<ScanDesc> bd;
+  if (rn) {
+    nblk = 0;
+    for (int f = 0; f < pl.F; ++f) {
+      const int64_t nb = std::max<int64_t>(1, ceil_div(pl.caps[f], OC_CH_SMALL));
+      bd.push_back({nullptr, nullptr, nb, nullptr, nullptr});
+      nblk += nb;
+    }
+  }
+  s->rv_blk = a.take<int64_t>(nblk);
+  s->rv_scan_part = a.take<int64_t>(rn ? std::max<int64_t>(scan_part_words(bd.data(), (int)bd.size()), 1) : 1);
+  s->fix_list = a.take<int32_t>(rn ? 3 * RV_FIX_CAP : 1);
+  s->fix_count = a.take<uint32_t>(1);
   s->head_count = a.take<int64_t>(RECD_MAX_FEAT);
   s->fallback = a.take<int32_t>(1);
   s->sc_ticket = a.take<uint32_t>(1);
@@ -1143,11 +1233,9 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
 //   scatter : occurrences -> sort -> scatter, reading caller unique-row grads
 enum class BwdMode { Full, GradOnly, ScatterOnly };
 
-// Occurrences as diagonal runs (k_runs_detect / _expand) instead of one sort
-// element per unique value: exact, but slower at cfg2 (detection + expansion
-// cost more than the smaller sort saves, and rows that repeat an ID trigger the
-// per-value fallback), so it is off by default.  RECD_BWD_RUNS=1
-// in the environment (read per call) selects it.
+// Occurrences as diagonal runs (k_rv*, one sort element per run) instead of
+// one per unique value; RECD_BWD_RUNS=0/1 in the environment (read per call)
+// overrides the default.
 #ifndef RECD_BWD_RUNS
 #define RECD_BWD_RUNS 0
 #endif
@@ -1241,6 +1329,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   bool single = true;
   for (int s = 0; s < pl.nts; ++s) {
     p.seg_grow[s] = feats_of_ts[s] == 1 ? p.grow[first_feat_of_ts[s]] : nullptr;
+    p.seg_feat[s] = first_feat_of_ts[s];
     single &= feats_of_ts[s] == 1;
     p.table[s] = pl.table[s];
     p.ts_base[s] = pl.ts_base[s];
@@ -1269,12 +1358,16 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   p.run_part = sc.run_part;
   p.bad = sc.bad;
   p.head_tag = sc.head_tag;
+  p.head_pos = sc.head_pos;
   p.head_len = sc.head_len;
+  p.rv_blk = sc.rv_blk;
+  p.fix_list = sc.fix_list;
+  p.fix_count = sc.fix_count;
   p.head_off = sc.head_off;
   p.head_count = sc.head_count;
   p.fallback = sc.fallback;
   p.sc_ticket = sc.sc_ticket;
-  const bool runs = bm == BwdMode::Full && do_scatter && use_runs();
+  const bool runs = bm == BwdMode::Full && do_scatter && single && use_runs();
 
   const bool fin = (phase & PH_FINISH) != 0;
   const bool run_grad = do_grad && (phase & PH_GRAD), run_scat = do_scatter && (phase & PH_SCAT);
@@ -1331,41 +1424,68 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       }
       p.occ_blk0[F] = ob;
       if (runs) {
-        // 1. run heads (ID, head index) + (tag, k), per table segment
-        k_runs_detect<<<(unsigned)ob, 256, 0, stream>>>(p, sc.occ_k0, sc.occ_v0);
+        // 1. heads per value block -> block offsets -> heads in (u, p) order
+        //    (+ the heads sort's digit histograms) -> run lengths
+        p.oc_ch = OC_CH_SMALL;  // the block layout the scratch was sized for
+        ob = 0;
+        for (int f = 0; f < F; ++f) {
+          p.occ_blk0[f] = ob;
+          ob += std::max<int64_t>(1, ceil_div(value_caps[f], p.oc_ch));
+        }
+        p.occ_blk0[F] = ob;
+        k_rv<0><<<(unsigned)ob, 256, 0, stream>>>(p, nullptr, nullptr);
+        std::vector<ScanDesc> bd;
+        for (int f = 0; f < F; ++f)
+          bd.push_back({sc.rv_blk + p.occ_blk0[f], sc.rv_blk + p.occ_blk0[f],
+                        p.occ_blk0[f + 1] - p.occ_blk0[f], nullptr, sc.head_count + pl.feat_ts[f]});
+        int r0 = seg_exclusive_scan(bd.data(), (int)bd.size(), sc.rv_scan_part, stream);
+        if (r0 != RECD_OK) return r0;
+        int rh = sort_hist_clear(pl.nts, sc.hist, stream);
+        if (rh != RECD_OK) return rh;
+        BwdParams q1 = p;
+        q1.occ_hist = sc.hist;
+        q1.occ_bits = (int)bits_for(maxrows);
+        k_rv<1><<<(unsigned)ob, 256, 0, stream>>>(q1, sc.occ_k0, sc.occ_v0);
+        k_rv_len<<<(unsigned)num_sms() * 8, 256, 0, stream>>>(p);
+        // 2. heads sorted by ID
         std::vector<SegDesc> hs;
         for (int s = 0; s < pl.nts; ++s) hs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.head_count + s});
         bool halt = false;
         int r1 = seg_sort_pairs(hs.data(), pl.nts, (int)bits_for(maxrows), sc.occ_k0, sc.occ_v0,
-                                sc.occ_k1, sc.occ_v1, sc.hist, &halt, stream);
+                                sc.occ_k1, sc.occ_v1, sc.hist, &halt, stream, nullptr, true);
         if (r1 != RECD_OK) return r1;
         uint32_t* Hk = halt ? sc.occ_k1 : sc.occ_k0;
         uint32_t* Hv = halt ? sc.occ_v1 : sc.occ_v0;
-        // 2. run lengths in sorted order -> expanded offsets per segment
-        k_runs_lens<<<dim3((unsigned)num_sms() * 2, (unsigned)pl.nts), 256, 0, stream>>>(p, Hv);
+        // 3. run lengths in sorted order (+ overlapping IDs) -> expanded offsets
+        RECD_CUDA_CHECK(cudaMemsetAsync(sc.fix_count, 0, sizeof(uint32_t), stream));
+        k_rv_lens<<<dim3((unsigned)num_sms() * 2, (unsigned)pl.nts), 256, 0, stream>>>(p, Hk, Hv);
         std::vector<ScanDesc> sd;
         for (int s = 0; s < pl.nts; ++s)
           sd.push_back({sc.head_off + pl.ts_base[s], sc.head_off + pl.ts_base[s], pl.ts_cap[s],
                         sc.head_count + s, nullptr});
         int r2 = seg_exclusive_scan(sd.data(), (int)sd.size(), sc.runs_scan_part, stream);
         if (r2 != RECD_OK) return r2;
-        // 3. per-value occurrences in (ID, tag) order into the other buffer pair
+        // 4. per-value occurrences in (ID, tag) order into the other buffer
+        //    pair, then the overlapping IDs' tags re-sorted
         int64_t ec = 0;
         for (int s = 0; s < pl.nts; ++s) {
           p.ex_chunk0[s] = ec;
-          ec += std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RC_EXP));
+          ec += std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RV_EX_CH));
         }
-        const unsigned ge = (unsigned)std::min<int64_t>(ceil_div(ec, 8), (int64_t)num_sms() * 16);
-        k_runs_expand<<<std::max(ge, 1u), 256, 0, stream>>>(p, Hk, Hv, ec);
-        // 4. fallback (an ID whose runs share a row, or > 32 runs): per-value
-        //    occurrences + the full sort, gated on the flag; the sort is set up
-        //    so that its result lands in the expansion's buffers
+        k_rv_expand<<<(unsigned)ec, 256, 0, stream>>>(p, Hk, Hv);
+        k_rv_fix<<<(unsigned)num_sms() * 2, 256, 0, stream>>>(p);
+        note_launch(5);
+        // 5. fallback (an overlapping ID with > RV_FIX_MAX values, or a full
+        //    list): per-value occurrences + the full sort, gated on the flag;
+        //    the sort is set up so that its result lands in the expansion's
+        //    buffers
         uint32_t* Xk = odd ? Hk : p.exp_keys;
         uint32_t* Xv = odd ? Hv : p.exp_vals;
         uint32_t* Yk = odd ? p.exp_keys : Hk;
         uint32_t* Yv = odd ? p.exp_vals : Hv;
         BwdParams q = p;
         q.occ_gate = sc.fallback;
+        q.oc_ch = OC_CH_SMALL;
         k_occ<<<(unsigned)ob, 256, 0, stream>>>(q, Xk, Xv);
         std::vector<SegDesc> vs;
         for (int s = 0; s < pl.nts; ++s) vs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});

@@ -1,4 +1,4 @@
-"""The backward's diagonal-run occurrences (csrc/recd_bwd.cu k_runs_*): one
+"""The backward's diagonal-run occurrences (csrc/recd_bwd.cu k_rv*): one
 sort element per run of an ID through shifted history windows.  Bit-exact
 against the oracle's (unique row, position)-ordered scatter-add on the
 cases that stress the exactness argument: IDs repeated inside a row (dirty
