@@ -266,21 +266,18 @@ struct RingRows {
   int64_t errpos;           // (feature << 40) | absolute position of streamed value 0
   int lane;
   bool ok;
-  int32_t wb;               // IDs of positions [wb, wb + 32) in cur, the next 32 in nxt
-  uint32_t cur, nxt;
+  int32_t wb;               // IDs of positions [wb, wb + 32) in cur, the next 32 in nraw
+  uint32_t cur;
+  int64_t nraw;             // raw ID of position wb + 32 + lane: range-checked only when
+                            // it becomes cur, so its load latency is not exposed at issue
   int32_t b;                // batches consumed
 
-  __device__ __forceinline__ uint32_t load_id(int32_t q) {
-    uint32_t v = 0;
-    if (q < n) {
-      const int64_t id = __ldg(ids + q);
-      if ((uint64_t)id < (uint64_t)rows) {
-        v = (uint32_t)id;
-      } else {
-        atomicMin(reinterpret_cast<unsigned long long*>(err), (unsigned long long)(errpos + q));
-      }
-    }
-    return v;
+  __device__ __forceinline__ int64_t raw_id(int32_t q) const { return q < n ? __ldg(ids + q) : 0; }
+  __device__ __forceinline__ uint32_t check_id(int64_t id, int32_t q) const {
+    if (q >= n) return 0u;
+    if ((uint64_t)id < (uint64_t)rows) return (uint32_t)id;
+    atomicMin(reinterpret_cast<unsigned long long*>(err), (unsigned long long)(errpos + q));
+    return 0u;
   }
   // positions [8 bi, 8 bi + 8) -> slots of batch bi % NB, one commit group
   __device__ __forceinline__ void issue(int32_t bi) {
@@ -288,8 +285,8 @@ struct RingRows {
     if (p0 < n) {  // warp-uniform
       if (p0 >= wb + 32) {
         wb += 32;
-        cur = nxt;
-        nxt = load_id(wb + 32 + lane);
+        cur = check_id(nraw, wb + lane);
+        nraw = raw_id(wb + 32 + lane);
       }
       float* dst = ring + (bi % NB) * (8 * 128);
       const int sh = p0 - wb;
@@ -312,8 +309,8 @@ struct RingRows {
   }
   __device__ __forceinline__ void start() {
     wb = 0;
-    cur = load_id(lane);
-    nxt = load_id(32 + lane);
+    cur = check_id(raw_id(lane), lane);
+    nraw = raw_id(32 + lane);
     b = 0;
 #pragma unroll
     for (int i = 0; i < NB; ++i) issue(i);
