@@ -309,8 +309,9 @@ struct RingRows {
   }
   __device__ __forceinline__ void start() {
     wb = 0;
-    cur = check_id(raw_id(lane), lane);
+    const int64_t c0 = raw_id(lane);
     nraw = raw_id(32 + lane);
+    cur = check_id(c0, lane);
     b = 0;
 #pragma unroll
     for (int i = 0; i < NB; ++i) issue(i);
@@ -474,15 +475,17 @@ __global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_
     if (n <= 0) {
       C::zero(acc);
     } else {
-      // value 0 straight into registers, values 1.. through the ring
+      // value 0 straight into registers, values 1.. through the ring; value
+      // 0's ID is range-checked after the ring's first IDs were loaded, so the
+      // two loads overlap
       const int64_t id0 = __ldg(p.uvalues[f] + a);
-      uint64_t r0 = 0;
-      if ((uint64_t)id0 < (uint64_t)p.table_rows[f]) {
-        r0 = (uint64_t)id0;
-      } else if (lane == 0) {
-        atomicMin(reinterpret_cast<unsigned long long*>(p.err),
-                  (unsigned long long)(((int64_t)(p.f0 + f) << 40) + a));
-      }
+      auto row0 = [&]() -> uint64_t {
+        if ((uint64_t)id0 < (uint64_t)p.table_rows[f]) return (uint64_t)id0;
+        if (lane == 0)
+          atomicMin(reinterpret_cast<unsigned long long*>(p.err),
+                    (unsigned long long)(((int64_t)(p.f0 + f) << 40) + a));
+        return 0;
+      };
       if (n > 1) {
         RingRows<K> rr;
         rr.ring = ring;
@@ -496,13 +499,13 @@ __global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_
         rr.lane = lane;
         rr.ok = C::FULL || cw.ok;
         rr.start();
-        C::ld(p.tables[f] + cw.lo + r0 * (uint32_t)p.D, cw.ok, acc);
+        C::ld(p.tables[f] + cw.lo + row0() * (uint32_t)p.D, cw.ok, acc);
         float sv[4];
         pairwise_ring<K>(rr, (int32_t)(n - 1), sv);
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], sv[k]);
       } else {
-        C::ld(p.tables[f] + cw.lo + r0 * (uint32_t)p.D, cw.ok, acc);
+        C::ld(p.tables[f] + cw.lo + row0() * (uint32_t)p.D, cw.ok, acc);
       }
       if (p.mode == RECD_POOL_AVG) {
         const float fl = (float)n;
