@@ -867,22 +867,33 @@ __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid
     const int64_t hi = min(n, lo + (int64_t)RC);
     const uint32_t* K = p.occ_keys + p.ts_base[s];
     const uint32_t* Vv = p.occ_vals + p.ts_base[s];
-    // 1. runs starting inside [lo, hi): start offsets and IDs
+    // 1. runs starting inside [lo, hi): start offsets and IDs.  The chunk's
+    //    keys are loaded up front (RC / 32 independent loads per lane, not one
+    //    round trip per 32 positions); a position's predecessor key comes
+    //    from the next lower lane, lane 0's from the previous group's lane 31
     int nruns = 0;
-    for (int64_t j0 = lo; j0 < hi; j0 += 32) {
-      const int64_t j = j0 + lane;
-      uint32_t k = 0;
-      bool st = false;
-      if (j < hi) {
-        k = __ldg(K + j);
-        st = (j == 0) || __ldg(K + j - 1) != k;
+    {
+      uint32_t kk[RC / 32];
+#pragma unroll
+      for (int g = 0; g < RC / 32; ++g) {
+        const int64_t j = lo + g * 32 + lane;
+        kk[g] = j < hi ? __ldg(K + j) : 0u;
       }
-      const unsigned b = __ballot_sync(0xffffffffu, st);
-      if (st) {
-        starts[nruns + __popc(b & lt)] = (uint16_t)(j - lo);
-        rids[nruns + __popc(b & lt)] = k;
+      uint32_t prev_last = lo > 0 ? __ldg(K + lo - 1) : 0u;
+#pragma unroll
+      for (int g = 0; g < RC / 32; ++g) {
+        const int64_t j = lo + g * 32 + lane;
+        const uint32_t up = __shfl_up_sync(0xffffffffu, kk[g], 1);
+        const uint32_t pk = lane == 0 ? prev_last : up;
+        prev_last = __shfl_sync(0xffffffffu, kk[g], 31);
+        const bool st = j < hi && (j == 0 || pk != kk[g]);
+        const unsigned b = __ballot_sync(0xffffffffu, st);
+        if (st) {
+          starts[nruns + __popc(b & lt)] = (uint16_t)(j - lo);
+          rids[nruns + __popc(b & lt)] = kk[g];
+        }
+        nruns += __popc(b);
       }
-      nruns += __popc(b);
     }
     __syncwarp();
     if (nruns == 0) continue;
