@@ -141,6 +141,18 @@ int recd_pool_fwd_csr(int32_t num_features, int64_t batch_size, int32_t dim, int
                       const uint32_t* const* csr_rows, float* const* pooled_out,
                       float* const* out, int64_t* err, recd_stream_t stream);
 
+/* ------------------------------------------------------- row-coded H2D --
+ * Device decode of row-delta coded KJT rows (recd_host.h encodes them on the
+ * host): per feature, codes[f] uint8[B], offsets[f] int64[B] (row starts),
+ * num_values device int64[F], value_caps host int64[F] (the grid), lits[f]
+ * the literals; writes values_out[f][0 .. num_values[f]).  Exact. */
+size_t recd_rowcode_scratch_bytes(int32_t num_features, int64_t batch_size);
+int recd_rowcode_decode(int32_t num_features, int64_t batch_size, const uint8_t* const* codes,
+                        const int64_t* const* offsets, const int64_t* num_values,
+                        const int64_t* value_caps, const int64_t* const* lits,
+                        int64_t* const* values_out, void* scratch, size_t scratch_bytes,
+                        recd_stream_t stream);
+
 /* Owner-side pooled lookup whose output rows go straight to the sources'
  * receive buffers (the all-to-all of partial rows fused into the pooling):
  * feature f's row u is stored at seg_dst[f * num_segs + s] + (u - seg_row0[f][s]) * dim

@@ -61,6 +61,8 @@ _SIGS = {
                                      _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
     "recd_pool_bwd_finish": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp,
                                     _pp, _f32, _i32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "recd_rowcode_scratch_bytes": (_sz, [_i32, _i64]),
+    "recd_rowcode_decode": (_i32, [_i32, _i64, _pp, _pp, _vp, _p64, _pp, _pp, _vp, _sz, _vp]),
     "recd_pool_bwd_csr": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _p64, _vp, _pp, _pp,
                                  _f32, _i32, _pp, _pp, _vp, _vp, _sz, _pp, _pp]),
     "recd_pool_fwd_csr": (_i32, [_i32, _i64, _i32, _i32, _pp, _p64, _pp, _pp, _vp, _pp, _pp, _pp,

@@ -91,7 +91,22 @@ def build_host(force: bool = False) -> Path:
     return out
 
 
+def build_host_lib(force: bool = False) -> Path:
+    """Compile librecd_host.so (plain C ABI, g++ + threads): the row-delta
+    encoder of the H2D path (include/recd_host.h)."""
+    src = CSRC / "host" / "recd_rowcode.cpp"
+    out = PKG / "librecd_host.so"
+    if force or _stale(out, [src, ROOT / "include" / "recd_host.h"]):
+        cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-shared",
+               "-fPIC", "-pthread", str(src), "-o", str(out)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return out
+
+
 if __name__ == "__main__":
     build_host(force="--force" in sys.argv)
+    build_host_lib(force="--force" in sys.argv)
     lib = build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(lib)

@@ -1,0 +1,145 @@
+// Row-delta coding of KJT rows for the host -> device copy (librecd_host.so).
+//
+// Session-clustered batches (the reference's generator, datagen.py:210-250,
+// and RecD's premise, §3) hold each user's samples back to back, and
+// a history feature's row is usually the previous row repeated or shifted by
+// one with one new ID at the end.  The copy of the full int64 KJT is what
+// bounds the end-to-end step on PCIe, so the host sends per row one code and
+// only the IDs the device cannot rebuild:
+//   KEY    (0)  all L IDs
+//   REPEAT (1)  row == previous row                         -> no ID
+//   SHIFT  (2)  row == previous row[1:] + [x] (same length)  -> x
+// and the device decodes (recd_rowcode_decode in librecd): with the literal
+// counts' inclusive prefix c(r), row r is literals[c(r) - L_r, c(r)) --
+// a REPEAT row re-reads its predecessor's window, a SHIFT row the window one
+// further, because every run of REPEAT / SHIFT rows after a KEY row appends
+// its new IDs right behind that KEY row's literals.  Exact by construction
+// (plain integer comparisons), any input (rows that match nothing are KEY).
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "../../../include/recd_host.h"
+
+namespace {
+
+constexpr int64_t TASK_VALUES = 1 << 20;  // ~8 MB of IDs per task
+
+struct Task {
+  int f;
+  int64_t r0, r1;   // rows [r0, r1)
+  int64_t lits;     // literals of the task (pass 1)
+  int64_t lit0;     // first literal of the task in its feature (prefix)
+};
+
+inline int64_t row_end(const int64_t* off, int64_t B, int64_t nv, int64_t r) {
+  return r + 1 < B ? off[r + 1] : nv;
+}
+
+void code_rows(const int64_t* v, const int64_t* off, int64_t B, int64_t nv, Task& t,
+               uint8_t* codes) {
+  int64_t lits = 0;
+  for (int64_t r = t.r0; r < t.r1; ++r) {
+    const int64_t a = off[r], e = row_end(off, B, nv, r), L = e - a;
+    uint8_t c = RECD_ROW_KEY;
+    if (r > 0 && L > 0) {
+      const int64_t pa = off[r - 1];
+      if (a - pa == L) {  // previous row of the same length
+        if (std::memcmp(v + a, v + pa, (size_t)L * 8) == 0)
+          c = RECD_ROW_REPEAT;
+        else if (std::memcmp(v + a, v + pa + 1, (size_t)(L - 1) * 8) == 0)
+          c = RECD_ROW_SHIFT;
+      }
+    } else if (r > 0 && L == 0 && off[r - 1] == a) {
+      c = RECD_ROW_REPEAT;  // empty after empty
+    }
+    codes[r] = c;
+    lits += c == RECD_ROW_KEY ? L : (c == RECD_ROW_SHIFT ? 1 : 0);
+  }
+  t.lits = lits;
+}
+
+void write_lits(const int64_t* v, const int64_t* off, int64_t B, int64_t nv, const Task& t,
+                const uint8_t* codes, int64_t* lit) {
+  int64_t o = t.lit0;
+  for (int64_t r = t.r0; r < t.r1; ++r) {
+    const int64_t a = off[r], e = row_end(off, B, nv, r);
+    if (codes[r] == RECD_ROW_KEY) {
+      std::memcpy(lit + o, v + a, (size_t)(e - a) * 8);
+      o += e - a;
+    } else if (codes[r] == RECD_ROW_SHIFT) {
+      lit[o++] = v[e - 1];
+    }
+  }
+}
+
+template <class Fn>
+void run_parallel(int threads, size_t n, Fn fn) {
+  std::atomic<size_t> next{0};
+  auto worker = [&]() {
+    for (size_t i = next++; i < n; i = next++) fn(i);
+  };
+  std::vector<std::thread> pool;
+  for (int i = 1; i < threads; ++i) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+extern "C" int recd_rowcode_encode(int32_t num_features, int64_t batch_size,
+                                   const int64_t* const* values, const int64_t* const* offsets,
+                                   const int64_t* num_values, uint8_t* const* codes_out,
+                                   int64_t* const* lits_out, const int64_t* lit_caps,
+                                   int64_t* lit_counts_out, int32_t num_threads) {
+  if (num_features <= 0 || batch_size <= 0 || !values || !offsets || !num_values || !codes_out ||
+      !lits_out || !lit_caps || !lit_counts_out)
+    return 1;
+  const int F = num_features;
+  const int64_t B = batch_size;
+  std::vector<Task> tasks;
+  std::vector<size_t> first(F + 1);
+  for (int f = 0; f < F; ++f) {
+    first[f] = tasks.size();
+    const int64_t* off = offsets[f];
+    const int64_t nv = num_values[f];
+    if (!off || !codes_out[f] || !lits_out[f] || (nv > 0 && !values[f]) || off[0] != 0) return 1;
+    int64_t r0 = 0;
+    while (r0 < B) {  // rows in chunks of ~TASK_VALUES IDs (at least one row)
+      int64_t r1 = r0 + 1;
+      const int64_t target = off[r0] + TASK_VALUES;
+      int64_t lo = r1, hi = B;  // first row >= r1 starting at or after target
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (off[mid] < target) lo = mid + 1; else hi = mid;
+      }
+      r1 = std::max(r1, lo);
+      tasks.push_back({f, r0, r1, 0, 0});
+      r0 = r1;
+    }
+  }
+  first[F] = tasks.size();
+  int threads = num_threads > 0 ? num_threads : (int)std::thread::hardware_concurrency();
+  threads = std::max(1, std::min<int>(threads, (int)tasks.size()));
+  run_parallel(threads, tasks.size(), [&](size_t i) {
+    Task& t = tasks[i];
+    code_rows(values[t.f], offsets[t.f], B, num_values[t.f], t, codes_out[t.f]);
+  });
+  for (int f = 0; f < F; ++f) {
+    int64_t acc = 0;
+    for (size_t i = first[f]; i < first[f + 1]; ++i) {
+      tasks[i].lit0 = acc;
+      acc += tasks[i].lits;
+    }
+    if (acc > lit_caps[f]) return 2;
+    lit_counts_out[f] = acc;
+  }
+  run_parallel(threads, tasks.size(), [&](size_t i) {
+    const Task& t = tasks[i];
+    write_lits(values[t.f], offsets[t.f], B, num_values[t.f], t, codes_out[t.f], lits_out[t.f]);
+  });
+  return 0;
+}

@@ -34,6 +34,18 @@ def test_library_exports_every_declared_symbol():
     assert set(_declared()) == set(_lib.EXPORTS)
 
 
+def test_host_library_exports_its_header():
+    """librecd_host.so (the row-delta encoder of the H2D path) exports every
+    function include/recd_host.h declares."""
+    from paper_2211_05239_b200 import rowcode
+    text = (ROOT / "include" / "recd_host.h").read_text()
+    names = sorted(set(re.findall(r"\b(recd_[a-z0-9_]+)\s*\(", text)))
+    assert names == ["recd_rowcode_encode"]
+    lib = rowcode.load_host()
+    for n in names:
+        assert hasattr(lib, n), n
+
+
 def test_host_only_entry_points_without_gpu():
     from paper_2211_05239_b200 import _lib
     lib = _lib.load()

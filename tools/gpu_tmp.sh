@@ -1,7 +1,11 @@
-timeout 900 python -m pytest tests/test_gpu_runs.py -x -q > gpurun_out/pytest_rv.log 2>&1
-echo "pytest runs rc=$?"; tail -5 gpurun_out/pytest_rv.log
-RECD_BWD_RUNS=1 timeout 900 python -m pytest tests/test_gpu_bwd.py tests/test_gpu_step.py tests/test_gpu_fullsize.py -x -q > gpurun_out/pytest_rv2.log 2>&1
-echo "pytest runs=1 rc=$?"; tail -5 gpurun_out/pytest_rv2.log
-for rep in 1 2; do bash tools/ab_env.sh "" base; bash tools/ab_env.sh "RECD_BWD_RUNS=1" rv; done
-RECD_BWD_RUNS=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_" --csv --log-file gpurun_out/launches_rv.csv python bench.py --profile --steps 1 --warmup 1 --no-cpu --no-graph > gpurun_out/launches_rv.log 2>&1; echo launches rc=$?
-python profiles/launches_summary.py gpurun_out/launches_rv.csv > gpurun_out/launches_rv.txt 2>&1; head -40 gpurun_out/launches_rv.txt
+timeout 900 python -m pytest tests/test_gpu_rowcode.py tests/test_gpu_graph_batches.py -x -q > gpurun_out/pytest_rc.log 2>&1
+echo "pytest rc=$?"; tail -3 gpurun_out/pytest_rc.log
+timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_rc.json 2> gpurun_out/bench_rc.err; echo bench rc=$?
+tail -3 gpurun_out/bench_rc.err
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_rc.json').read().strip().splitlines()[-1])
+print(d['ms_per_step'], d['e2e'])"
+timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --e2e-wire raw > gpurun_out/bench_raw.json 2> gpurun_out/bench_raw.err; echo bench raw rc=$?
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_raw.json').read().strip().splitlines()[-1])
+print(d['ms_per_step'], d['e2e'])"
