@@ -48,6 +48,8 @@ def encode(values, offsets, batch_size: int, codes_out, lits_out, num_threads: i
     buffers.  Returns the literal count of every feature."""
     F = len(values)
     lib = load_host()
+    if num_threads <= 0:
+        num_threads = int(os.environ.get("RECD_ROWCODE_THREADS", "0"))
     arr = lambda xs: (C.c_void_p * F)(*[_ptr(x) for x in xs])  # noqa: E731
     nv = (C.c_int64 * F)(*[int(v.shape[0]) for v in values])
     caps = (C.c_int64 * F)(*[int(x.shape[0]) for x in lits_out])
