@@ -92,9 +92,11 @@ def parse(argv=None):
                     help="N=1: cross-step pipelining (the next batch's dedup + backward prepare "
                          "on a side stream during the current step; A/B: 4.86 vs 4.89 ms, e2e lower)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-wire", choices=["rowcode", "raw"], default="rowcode",
+    ap.add_argument("--e2e-wire", choices=["auto", "rowcode", "raw"], default="auto",
                     help="H2D format of the e2e leg: row-delta coded (host encode inside the "
-                         "timed region) or the raw int64 KJT")
+                         "timed region) or the raw int64 KJT; auto = row-coded while every rank "
+                         "has >= 8 host cores to encode with (each GPU has its own PCIe link, "
+                         "the host cores are shared)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0,
                     help="rows in the CPU sample (0 = calibrated to --cpu-seconds)")
@@ -583,14 +585,14 @@ def run_single(args, dev):
     e2e = None
     if not args.no_e2e and not args.profile:
         if pipe:
-            e2e = e2e_step_pipeline(step, batch, keys, dev, max(4, min(args.steps, 20)),
-                                    args.e2e_wire == "rowcode")
+            rc, th = e2e_wire(args, 1)
+            e2e = e2e_step_pipeline(step, batch, keys, dev, max(4, min(args.steps, 20)), rc, th)
         else:
+            rc, th = e2e_wire(args, 1)
             e2e = e2e_pipelined(step, batch, keys, step.replay, dev, max(4, min(args.steps, 20)), 1,
-                                rowcode=args.e2e_wire == "rowcode")
+                                rowcode=rc, threads=th)
             e2e["how"] = ("public TrainStep API: pinned-host KJT -> "
-                          + ("host row-delta encode (librecd_host) -> " if args.e2e_wire == "rowcode"
-                             else "") +
+                          + ("host row-delta encode (librecd_host) -> " if rc else "") +
                           "H2D on a copy stream straight "
                           "into the step's other input slot (overlaps the previous step; one CUDA "
                           "graph per slot, value counts read on the device, no device-to-device "
@@ -669,7 +671,17 @@ def roofline_entry(dom, k, peak, peaks, traffic, config):
             "avg_launch_ms": k["ms"], "achieved_requested": k["achieved_requested_gbs"]}
 
 
-def e2e_pipelined(step, batch, keys, replay, dev, n_steps, world, dist=None, rowcode=True):
+def e2e_wire(args, world):
+    """(row-coded?, encoder threads per rank) for the e2e leg."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    per_rank = max(1, (cores or 1) // max(world, 1))
+    if args.e2e_wire == "auto":
+        return per_rank >= 8, per_rank
+    return args.e2e_wire == "rowcode", per_rank
+
+
+def e2e_pipelined(step, batch, keys, replay, dev, n_steps, world, dist=None, rowcode=True,
+                  threads=0):
     """End-to-end samples/s through the public step API from pinned host
     buffers: every step's KJT goes H2D (copy stream, double-buffered, so the
     copy of batch i+1 overlaps step i), the step runs, and its dedup counts
@@ -680,7 +692,7 @@ def e2e_pipelined(step, batch, keys, replay, dev, n_steps, world, dist=None, row
 
     pin_v = {k: torch.from_numpy(batch.values[k]).pin_memory() for k in keys}
     pin_o = {k: torch.from_numpy(batch.offsets[k]).pin_memory() for k in keys}
-    pipe = H2DPipeline(step, dev, rowcode=rowcode)
+    pipe = H2DPipeline(step, dev, rowcode=rowcode, threads=threads)
     res = [torch.empty(step.counts.numel(), dtype=torch.int64).pin_memory() for _ in range(2)]
     direct = pipe.direct
     done = [torch.cuda.Event(), torch.cuda.Event()]
@@ -715,12 +727,13 @@ def e2e_pipelined(step, batch, keys, replay, dev, n_steps, world, dist=None, row
     return {"value": world * B / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d * world,
             "d2h_bytes_per_step": res[0].numel() * 8 * world, "ms_per_step": e2e_s * 1e3,
             "h2d_gbs_per_gpu": h2d / e2e_s / 1e9,
-            "wire": ("row-delta coded: host encode (C++ threads) of every step's KJT inside the "
+            "wire": (f"row-delta coded: host encode ({threads or 'all'} C++ threads per rank) of "
+                     "every step's KJT inside the "
                      f"timed region, {raw / max(h2d, 1):.1f}x fewer H2D bytes than the raw "
                      "int64 KJT, device decode on the copy stream") if rowcode else "raw int64 KJT"}
 
 
-def e2e_step_pipeline(step, batch, keys, dev, n_steps, rowcode=True):
+def e2e_step_pipeline(step, batch, keys, dev, n_steps, rowcode=True, threads=0):
     """End to end through the pipelined TrainStep: batch i+2 goes H2D (copy
     stream, pinned host) into the slot batch i came in while graph i trains
     batch i and deduplicates batch i+1 on its side stream; each step's dedup
@@ -732,7 +745,7 @@ def e2e_step_pipeline(step, batch, keys, dev, n_steps, rowcode=True):
 
     pin_v = {k: torch.from_numpy(batch.values[k]).pin_memory() for k in keys}
     pin_o = {k: torch.from_numpy(batch.offsets[k]).pin_memory() for k in keys}
-    pipe = H2DPipeline(step, dev, rowcode=rowcode)
+    pipe = H2DPipeline(step, dev, rowcode=rowcode, threads=threads)
     res = [torch.empty(step.counts.numel(), dtype=torch.int64).pin_memory() for _ in range(2)]
     done = [torch.cuda.Event(), torch.cuda.Event()]
     torch.cuda.synchronize()
@@ -900,9 +913,9 @@ def run_sharded(args, world, rank, local, dev):
 
     e2e = None
     if not args.no_e2e and not args.profile:
+        rc, th = e2e_wire(args, world)
         e2e = e2e_pipelined(step, batch, keys, step.replay if peer else step.run, dev,
-                            max(4, min(args.steps, 10)), world, dist,
-                            rowcode=args.e2e_wire == "rowcode")
+                            max(4, min(args.steps, 10)), world, dist, rowcode=rc, threads=th)
         e2e["how"] = (f"{cls.__name__} on every rank: pinned-host KJT -> H2D on a copy stream "
                       "(double-buffered) -> step -> D2H of the dedup counts; max over ranks")
     if rank == 0:

@@ -36,6 +36,12 @@ V = {
     "k1m4": ["RECD_RING_K=1", "RECD_RING_MINB=4"],
     "cp32": ["RECD_CP_IT=32", "RECD_OC_CH=8192"],
     "cp64": ["RECD_CP_IT=64", "RECD_OC_CH=16384"],
+    "b8m3": ["RECD_SC_BATCH=8", "RECD_SCATTER_MINB=3"],
+    "b8r4": ["RECD_SC_BATCH=8", "RECD_SC_RS=4"],
+    "b4": ["RECD_SC_BATCH=4"],
+    "r4": ["RECD_SC_RS=4"],
+    "r8": ["RECD_SC_RS=8"],
+    "b10m3": ["RECD_SC_BATCH=10", "RECD_SCATTER_MINB=3"],
 }
 only = sys.argv[1:] or list(V)
 for k in only:
