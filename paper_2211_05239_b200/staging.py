@@ -27,6 +27,8 @@ batches); the host encodes batch i+1 (C++ threads) while step i runs, and
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib
@@ -36,7 +38,7 @@ __all__ = ["H2DPipeline"]
 
 class H2DPipeline:
     def __init__(self, step, device=None, nslots: int = 2, rowcode: bool = False,
-                 threads: int = 0):
+                 threads: int = 0, raw_share: float | None = None):
         self.step = step
         self.direct = getattr(step, "nslots", 1) >= nslots
         self.dev = device or step.in_values[0].device
@@ -56,11 +58,14 @@ class H2DPipeline:
         self._freed = [False] * nslots
         self.rowcode = bool(rowcode)
         self.threads = int(threads)
+        if raw_share is None:
+            raw_share = float(os.environ.get("RECD_ROWCODE_RAW_SHARE", "0"))
+        self.raw_share = min(max(float(raw_share), 0.0), 1.0)
         self.h2d_bytes = [0] * nslots    # bytes the last prefetch into each slot copied
         if self.rowcode:
             B = step.B
             caps = [v.numel() for v in self.slots[0][0]]
-            self._caps = _lib.i64s(caps)
+            self._capv = caps
             self._h_codes = [torch.empty((F, B), dtype=torch.uint8).pin_memory() for _ in range(nslots)]
             self._h_lits = [[torch.empty(c, dtype=torch.int64).pin_memory() for c in caps]
                             for _ in range(nslots)]
@@ -106,23 +111,29 @@ class H2DPipeline:
     def _prefetch_rowcode(self, slot: int, values: dict, offsets: dict, n: list) -> None:
         # encoded on the calling thread with every core: on a worker thread
         # (the caller launching steps meanwhile) e2e was 11.3-11.9 vs 10.9-11.1
-        # ms per cfg2 step -- the encoder is what the host is busy with
+        # ms per cfg2 step -- the encoder is what the host is busy with.  With
+        # raw_share > 0 the largest keys (that share of the IDs) go over PCIe
+        # as raw int64 first, so the copy engine works while the cores encode
         from . import rowcode
         keys = self.step.keys
         F = len(keys)
         vals, offs = self.slots[slot]
+        total = sum(n)
+        raw = set()
+        acc = 0
+        for f in sorted(range(F), key=lambda f: -n[f]):
+            if acc >= self.raw_share * total:
+                break
+            raw.add(f)
+            acc += n[f]
+        coded = [f for f in range(F) if f not in raw]
         if self._h_done[slot] is not None:
             self._h_done[slot].synchronize()     # host staging free again
-        hc, hl = self._h_codes[slot], self._h_lits[slot]
-        host_v = [values[k] for k in keys]
-        host_o = [offsets[k] for k in keys]
-        lits = rowcode.encode(host_v, host_o, self.step.B, [hc[f] for f in range(F)], hl,
-                              self.threads)
-        dc, dl, dnv = self._d_codes[slot], self._d_lits[slot], self._d_nv[slot]
         pc = self._pin_counts[slot]
         if self._pc_done[slot] is not None:
             self._pc_done[slot].synchronize()
         pc.copy_(torch.tensor(n, dtype=torch.int64))
+        dc, dl, dnv = self._d_codes[slot], self._d_lits[slot], self._d_nv[slot]
         with torch.cuda.stream(self.copy):
             if self._freed[slot]:
                 self.copy.wait_event(self.free[slot])   # the step is done reading the slot
@@ -130,26 +141,53 @@ class H2DPipeline:
                 o = offsets[k]
                 offs[f].copy_(o if isinstance(o, torch.Tensor) else torch.from_numpy(o),
                               non_blocking=True)
-                if lits[f]:
-                    dl[f][: lits[f]].copy_(hl[f][: lits[f]], non_blocking=True)
-            dc.copy_(hc, non_blocking=True)
+            for f in sorted(raw):
+                v = values[keys[f]]
+                vals[f][: n[f]].copy_(v if isinstance(v, torch.Tensor) else torch.from_numpy(v),
+                                      non_blocking=True)
             dnv.copy_(pc, non_blocking=True)
             if self.direct:
                 self.step.in_counts[slot, F:].copy_(dnv, non_blocking=True)
-            L = _lib.load()
-            rc = L.recd_rowcode_decode(F, self.step.B, _lib.ptrs([dc[f] for f in range(F)]),
-                                       _lib.ptrs(offs), dnv.data_ptr(), self._caps, _lib.ptrs(dl),
-                                       _lib.ptrs(vals), self._rc_scratch.data_ptr(),
-                                       self._rc_scratch.numel(), self.copy.cuda_stream)
-            _lib.check(rc, "recd_rowcode_decode")
+        hc, hl = self._h_codes[slot], self._h_lits[slot]
+        lits = [0] * F
+        if coded:
+            got = rowcode.encode([values[keys[f]] for f in coded], [offsets[keys[f]] for f in coded],
+                                 self.step.B, [hc[f] for f in coded], [hl[f] for f in coded],
+                                 self.threads)
+            for f, c in zip(coded, got):
+                lits[f] = c
+        with torch.cuda.stream(self.copy):
+            for f in coded:
+                if lits[f]:
+                    dl[f][: lits[f]].copy_(hl[f][: lits[f]], non_blocking=True)
+            if coded:
+                dc.copy_(hc, non_blocking=True)
+                rc = self._decode(coded, dc, offs, dl, vals, dnv)
+                _lib.check(rc, "recd_rowcode_decode")
             ev = torch.cuda.Event()
             ev.record(self.copy)
             self._h_done[slot] = ev
             self._pc_done[slot] = ev
             self.ready[slot].record(self.copy)
         self.counts[slot] = n
-        self.h2d_bytes[slot] = sum(8 * (lits[f] + offs[f].numel() + 1) + self.step.B
-                                   for f in range(F))
+        self.h2d_bytes[slot] = sum(8 * offs[f].numel() + 8 for f in range(F)) + \
+            sum(8 * n[f] for f in raw) + sum(8 * lits[f] + self.step.B for f in coded)
+
+    def _decode(self, coded, dc, offs, dl, vals, dnv):
+        """recd_rowcode_decode over the coded keys (a subset's value counts
+        gathered into a contiguous device array first)."""
+        nv = dnv
+        if len(coded) < len(vals):
+            nv = self._nv_sub = dnv.index_select(
+                0, torch.tensor(coded, dtype=torch.int64).to(self.dev, non_blocking=True))
+        L = _lib.load()
+        return L.recd_rowcode_decode(len(coded), self.step.B, _lib.ptrs([dc[f] for f in coded]),
+                                     _lib.ptrs([offs[f] for f in coded]), nv.data_ptr(),
+                                     _lib.i64s([self._capv[f] for f in coded]),
+                                     _lib.ptrs([dl[f] for f in coded]),
+                                     _lib.ptrs([vals[f] for f in coded]),
+                                     self._rc_scratch.data_ptr(), self._rc_scratch.numel(),
+                                     self.copy.cuda_stream)
 
     def run(self, slot: int, replay) -> None:
         """Run one step on `slot` (after its copy), then hand the slot back to

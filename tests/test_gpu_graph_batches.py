@@ -30,10 +30,10 @@ def _batches(n, b):
 
 @pytest.mark.parametrize("mode,fused,wire", [("dedup", "0", "raw"), ("dedup", "1", "raw"),
                                              ("kjt", "0", "raw"), ("dedup", "1", "rowcode"),
-                                             ("kjt", "0", "rowcode")])
+                                             ("kjt", "0", "rowcode"), ("dedup", "1", "mixed")])
 def test_one_graph_twenty_batches(mode, fused, wire, monkeypatch):
-    """wire: raw int64 KJT copies, or row-delta coded batches decoded on the
-    device (H2DPipeline(rowcode=True))."""
+    """wire: raw int64 KJT copies, row-delta coded batches decoded on the
+    device (H2DPipeline(rowcode=True)), or half the IDs raw and half coded."""
     monkeypatch.setenv("RECD_FUSED_EXPAND", fused)
     b, vocab, dim, lr = 1024, 4000, 32, 0.05
     batches = _batches(20, b)
@@ -57,7 +57,7 @@ def test_one_graph_twenty_batches(mode, fused, wire, monkeypatch):
     for k in keys:
         tables[k].weights.copy_(torch.as_tensor(w[k]))
     graphs = list(step.graphs)
-    pipe = H2DPipeline(step, rowcode=wire == "rowcode")
+    pipe = H2DPipeline(step, rowcode=wire != "raw", raw_share=0.5 if wire == "mixed" else 0.0)
     pin = [({k: torch.from_numpy(x.values[k]).pin_memory() for k in keys},
             {k: torch.from_numpy(x.offsets[k]).pin_memory() for k in keys}) for x in batches]
     pipe.prefetch(0, *pin[0])
