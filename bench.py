@@ -678,7 +678,9 @@ def e2e_wire(args, world):
     measured on the B200 hosts): x / 54 = (1 - x) / (7.3 * cores)."""
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     per_rank = max(1, (cores or 1) // max(world, 1))
-    if args.e2e_wire == "raw":
+    if args.e2e_wire == "raw" or (args.e2e_wire == "auto" and per_rank < 8):
+        # < 8 cores per rank: N = 4 on the 16-core hosts here was 9.7 M samples/s
+        # row-coded vs 12.7 M raw (the ranks' copies and encoders share the host)
         return False, per_rank, 1.0
     share = 54.0 / (54.0 + 7.3 * per_rank)
     return True, per_rank, (share if args.e2e_wire == "auto" else 0.0)
