@@ -92,6 +92,8 @@ def parse(argv=None):
                     help="N=1: cross-step pipelining (the next batch's dedup + backward prepare "
                          "on a side stream during the current step; A/B: 4.86 vs 4.89 ms, e2e lower)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-raw-share", type=float, default=None,
+                    help="row-coded e2e: share of the IDs copied raw (default: the balance model)")
     ap.add_argument("--e2e-wire", choices=["auto", "rowcode", "raw"], default="auto",
                     help="H2D format of the e2e leg: row-delta coded (host encode inside the "
                          "timed region), the raw int64 KJT, or auto = row-coded with the largest "
@@ -673,16 +675,22 @@ def roofline_entry(dom, k, peak, peaks, traffic, config):
 
 def e2e_wire(args, world):
     """(row-coded?, encoder threads per rank, raw share) for the e2e leg.  The
-    share of the IDs that goes over PCIe raw balances the copy engine (~54
-    GB/s per GPU) against the rank's encoder cores (~7.3 GB/s of KJT each,
-    measured on the B200 hosts): x / 54 = (1 - x) / (7.3 * cores)."""
+    share x of the IDs that goes over PCIe raw balances the copy engine
+    against the rank's encoder cores.  The copy engine carries the raw IDs and
+    the coded rest (rho ~ 0.09 of its raw size: literals, codes, offsets) at
+    ~47 GB/s per GPU while the host encodes; the encoder reads ~6.25 GB/s of
+    KJT per core (both measured on the B200 hosts, cfg2):
+    (x + rho (1 - x)) / 47 = (1 - x) / (6.25 cores)."""
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     per_rank = max(1, (cores or 1) // max(world, 1))
     if args.e2e_wire == "raw" or (args.e2e_wire == "auto" and per_rank < 8):
         # < 8 cores per rank: N = 4 on the 16-core hosts here was 9.7 M samples/s
         # row-coded vs 12.7 M raw (the ranks' copies and encoders share the host)
         return False, per_rank, 1.0
-    share = 54.0 / (54.0 + 7.3 * per_rank)
+    c, e, rho = 47.0, 6.25 * per_rank, 0.09
+    share = (1.0 / e - rho / c) / ((1.0 - rho) / c + 1.0 / e)
+    if args.e2e_raw_share is not None:
+        share = args.e2e_raw_share
     return True, per_rank, (share if args.e2e_wire == "auto" else 0.0)
 
 

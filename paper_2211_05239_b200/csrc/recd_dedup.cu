@@ -128,7 +128,12 @@ constexpr int RS_IT = RECD_RS_IT;    // consecutive values per thread
 #ifndef RECD_RS_TMA
 #define RECD_RS_TMA 0
 #endif
-constexpr int RT_T = 2048;                                    // values per stage (16 KB)
+// uniform chunks: warp-coalesced 16-byte value pairs (RECD_RS_COAL=1) instead
+// of 8 thread-contiguous values per thread
+#ifndef RECD_RS_COAL
+#define RECD_RS_COAL 1
+#endif
+constexpr int RT_T = 2048;                                  // values per stage (16 KB)
 constexpr int RT_SMEM = RECD_RS_TMA ? 3 * RT_T * 8 : 0;       // dynamic shared memory
 
 #ifndef RECD_RS_MINB
@@ -276,6 +281,53 @@ __global__ void __launch_bounds__(RS_NT, RECD_RS_MINB) k_rowscan(const __grid_co
           if (tid == 0 && t + 2 < ntiles) issue(t + 2);
         }
         tiles_seen += (uint32_t)ntiles;
+        continue;
+      }
+#endif
+#if RECD_RS_COAL
+      if (a16) {
+        // warp-coalesced: value pair (q, q + 1) of thread tid at q = base + 2 tid
+        // + k 512 (consecutive threads, consecutive 16 bytes: 4 L1 lines per
+        // warp load instead of 16 for thread-contiguous runs); the predecessor
+        // pair at q - L is 16-byte aligned when L is even
+        constexpr int PK = RS_IT / 2;                  // pairs per thread per trip
+        constexpr int64_t STEP = 2 * RS_NT;            // values per pair slot
+        const int64_t tbe = vbeg & ~(int64_t)1;
+        const bool Leven = (L & 1u) == 0;
+        for (int64_t ob = tbe; ob < vend; ob += STEP * PK) {
+          longlong2 cv[PK], pv[PK];
+#pragma unroll
+          for (int k = 0; k < PK; ++k) {
+            const int64_t q = ob + k * STEP + 2 * tid;
+            cv[k] = make_longlong2(0, 0);
+            if (q + 1 < nv) cv[k] = __ldg(reinterpret_cast<const longlong2*>(val + q));
+            else if (q < nv) cv[k].x = __ldg(val + q);
+          }
+#pragma unroll
+          for (int k = 0; k < PK; ++k) {
+            const int64_t pq = ob + k * STEP + 2 * tid - L0;
+            if (Leven && pq >= 0) {
+              pv[k] = __ldg(reinterpret_cast<const longlong2*>(val + pq));
+            } else {
+              pv[k].x = __ldg(val + max(pq, (int64_t)0));
+              pv[k].y = __ldg(val + max(pq + 1, (int64_t)0));
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < PK; ++k) {
+            const int64_t q = ob + k * STEP + 2 * tid;
+            if (q >= vend) continue;
+            if (q >= vbeg) {
+              const uint32_t rel = (uint32_t)(q - vbeg);
+              const uint32_t j = rel / L;
+              if (cv[k].x != pv[k].x) s_mism[j] = 1u;
+              if (q + 1 < vend && cv[k].y != pv[k].y) s_mism[j + (rel - j * L + 1 == L ? 1u : 0u)] = 1u;
+            } else if (cv[k].y != pv[k].y) {  // q = vbeg - 1: only q + 1 (row 0)
+              s_mism[0] = 1u;
+            }
+          }
+        }
+        __syncthreads();
         continue;
       }
 #endif

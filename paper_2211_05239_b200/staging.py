@@ -118,14 +118,7 @@ class H2DPipeline:
         keys = self.step.keys
         F = len(keys)
         vals, offs = self.slots[slot]
-        total = sum(n)
-        raw = set()
-        acc = 0
-        for f in sorted(range(F), key=lambda f: -n[f]):
-            if acc >= self.raw_share * total:
-                break
-            raw.add(f)
-            acc += n[f]
+        raw = self._raw_keys(n)
         coded = [f for f in range(F) if f not in raw]
         if self._h_done[slot] is not None:
             self._h_done[slot].synchronize()     # host staging free again
@@ -172,6 +165,18 @@ class H2DPipeline:
         self.counts[slot] = n
         self.h2d_bytes[slot] = sum(8 * offs[f].numel() + 8 for f in range(F)) + \
             sum(8 * n[f] for f in raw) + sum(8 * lits[f] + self.step.B for f in coded)
+
+    def _raw_keys(self, n: list) -> set:
+        """Keys copied raw: largest first, skipping any that would take the
+        raw IDs past raw_share of the batch (so the share is met from below
+        to within the smallest key, not overshot by a whole long key)."""
+        target = self.raw_share * sum(n)
+        raw, acc = set(), 0
+        for f in sorted(range(len(n)), key=lambda f: -n[f]):
+            if n[f] and acc + n[f] <= target:
+                raw.add(f)
+                acc += n[f]
+        return raw
 
     def _decode(self, coded, dc, offs, dl, vals, dnv):
         """recd_rowcode_decode over the coded keys (a subset's value counts

@@ -59,3 +59,24 @@ def test_random_rows_and_capacity():
     offs = np.array([0, 5], dtype=np.int64)
     with pytest.raises(ValueError, match="capacity"):
         rowcode.encode([vals], [offs], 2, [np.empty(2, np.uint8)], [np.empty(4, np.int64)])
+
+
+def test_raw_key_share_met_from_below():
+    """H2DPipeline copies the largest keys raw up to raw_share of the IDs,
+    skipping a key that would overshoot (cfg2: 4 keys of 256 IDs per row are
+    12.6% each, so 0.28 takes two of them plus shorter keys, not three)."""
+    import types
+
+    from paper_2211_05239_b200.staging import H2DPipeline
+
+    n = [L * 1000 for L in ([8, 16, 32, 64, 128, 256] * 5)[:26]]
+    pick = lambda share: H2DPipeline._raw_keys(types.SimpleNamespace(raw_share=share), n)
+    tot = sum(n)
+    for share in (0.0, 0.1, 0.2, 0.28, 0.5, 1.0):
+        raw = pick(share)
+        got = sum(n[f] for f in raw)
+        assert got <= share * tot
+        # nothing left out that would still fit
+        assert all(n[f] == 0 or got + n[f] > share * tot for f in range(len(n)) if f not in raw)
+    assert sorted(n[f] for f in pick(0.28)).count(256000) == 2
+    assert pick(1.0) == set(range(len(n)))

@@ -6,6 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
+    "nocoal": ["RECD_RS_COAL=0"],
     "noflat": ["RECD_GU_FLAT=0"],
     "fm4": ["RECD_GUF_MINB=4"],
     "rs8": ["RECD_SC_RS=8"],
