@@ -121,6 +121,7 @@ struct BwdParams {
 };
 
 __global__ void k_bwd_setup(const __grid_constant__ BwdParams p) {
+  RECD_PDL_PROLOGUE();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   *p.bad = 0;
   *p.fallback = 0;
@@ -138,6 +139,7 @@ __global__ void k_bwd_setup(const __grid_constant__ BwdParams p) {
 
 // keys = inverse value, vals = row: sorted by key -> CSR of each unique row
 __global__ void k_inv_pairs(const __grid_constant__ BwdParams p, uint32_t* keys, uint32_t* vals) {
+  RECD_PDL_PROLOGUE();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)p.nis * p.B) return;
   const int s = (int)(idx / p.B);
@@ -147,6 +149,7 @@ __global__ void k_inv_pairs(const __grid_constant__ BwdParams p, uint32_t* keys,
 }
 
 __global__ void k_csr_bounds(const __grid_constant__ BwdParams p) {
+  RECD_PDL_PROLOGUE();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)p.nis * p.B) return;
   const int s = (int)(idx / p.B);
@@ -166,6 +169,7 @@ __global__ void k_csr_bounds(const __grid_constant__ BwdParams p) {
 
 template <class C>
 __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdParams p) {
+  RECD_PDL_PROLOGUE();
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
   const int ncb = col_blocks<C>(p.D);
   if (threadIdx.x == 0) {
@@ -246,6 +250,7 @@ __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t
 #endif
 template <class C, int GU_CH>
 __global__ void __launch_bounds__(256, RECD_GUF_MINB) k_grad_u_flat(const __grid_constant__ BwdParams p) {
+  RECD_PDL_PROLOGUE();
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
   const int ncb = col_blocks<C>(p.D);
   const int64_t nch = (p.B + GU_CH - 1) / GU_CH;
@@ -355,6 +360,7 @@ constexpr int OC_CH_SMALL = 4096;  // ... and on small ones (more blocks in flig
 constexpr int OC_MAXR = 512;
 __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p, uint32_t* keys,
                                              uint32_t* vals) {
+  RECD_PDL_PROLOGUE();
   if (p.occ_gate && !*(volatile const int32_t*)p.occ_gate) return;  // runs fallback only
   int f = 0;
   while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
@@ -510,6 +516,7 @@ constexpr int RV_EX_CH = 2048;     // expanded values per k_rv_expand block
 template <int MODE>
 __global__ void __launch_bounds__(256) k_rv(const __grid_constant__ BwdParams p, uint32_t* keys,
                                             uint32_t* vals) {
+  RECD_PDL_PROLOGUE();
   int f = 0;
   while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
   const int64_t blk = blockIdx.x;
@@ -614,6 +621,7 @@ __global__ void __launch_bounds__(256) k_rv(const __grid_constant__ BwdParams p,
 // the head's ID (row starts from global memory: the next row's start is the
 // current row's end, so one new offset + one value per step)
 __global__ void __launch_bounds__(256) k_rv_len(const __grid_constant__ BwdParams p) {
+  RECD_PDL_PROLOGUE();
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int s = 0; s < p.nts; ++s) {
     const int f = p.seg_feat[s];
@@ -647,6 +655,7 @@ __global__ void __launch_bounds__(256) k_rv_len(const __grid_constant__ BwdParam
 // (a run starting before the previous one's last row) and lists the ID
 __global__ void k_rv_lens(const __grid_constant__ BwdParams p, const uint32_t* skeys,
                           const uint32_t* svals) {
+  RECD_PDL_PROLOGUE();
   const int s = blockIdx.y;
   const int64_t n = p.head_count[s], base = p.ts_base[s];
   const uint32_t* K = skeys + base;
@@ -685,6 +694,7 @@ __global__ void k_rv_lens(const __grid_constant__ BwdParams p, const uint32_t* s
 // value e -> (ID, head tag + e - head offset), coalesced stores
 __global__ void __launch_bounds__(256) k_rv_expand(const __grid_constant__ BwdParams p,
                                                    const uint32_t* skeys, const uint32_t* svals) {
+  RECD_PDL_PROLOGUE();
   int s = 0;
   while (s + 1 < p.nts && p.ex_chunk0[s + 1] <= (int64_t)blockIdx.x) ++s;
   const int64_t E = p.seg_count[s], base = p.ts_base[s];
@@ -726,6 +736,7 @@ __global__ void __launch_bounds__(256) k_rv_expand(const __grid_constant__ BwdPa
 
 // block per listed ID: its expanded tags (all one key) sorted in shared memory
 __global__ void __launch_bounds__(256) k_rv_fix(const __grid_constant__ BwdParams p) {
+  RECD_PDL_PROLOGUE();
   __shared__ uint32_t s_t[RV_FIX_MAX];
   const uint32_t cnt = min(*p.fix_count, (uint32_t)RV_FIX_CAP);
   for (uint32_t k = blockIdx.x; k < cnt; k += gridDim.x) {
@@ -775,6 +786,7 @@ __device__ __forceinline__ int rc_seg(const BwdParams& p, int64_t chunk) {
 // number of run starts per RC chunk (grad-output mode)
 template <int RC>
 __global__ void __launch_bounds__(RC) k_run_count(const __grid_constant__ BwdParams p) {
+  RECD_PDL_PROLOGUE();
   const int64_t chunk = blockIdx.x;
   const int s = rc_seg(p, chunk);
   const int64_t n = p.seg_count[s];
@@ -824,6 +836,7 @@ constexpr int SC_BATCH = RECD_SC_BATCH;  // unique-row gradient gathers in fligh
 // stored, and its slot refilled with the row of run r + SC_RS.
 template <class C, bool SINGLE, int RC>
 __global__ void __launch_bounds__(256, RECD_SCATTER_MINB) k_scatter(const __grid_constant__ BwdParams p) {
+  RECD_PDL_PROLOGUE();
   constexpr int V = C::VW;
   __shared__ uint16_t s_starts[8][RC + 2];
   __shared__ uint32_t s_ids[8][RC];
@@ -1407,14 +1420,14 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
 
   // ---- prepare: everything that depends on the IKJT only (no gradient)
   if (phase & PH_INV) {
-    k_bwd_setup<<<1, 32, 0, stream>>>(p);
+    pdl(k_bwd_setup, 1, 32, 0, stream)(p);
     note_launch();
   }
   {
     // 1. inverse CSR
     if ((phase & PH_INV) && do_grad && pl.nis > 0) {
       const int64_t n = (int64_t)pl.nis * B;
-      k_inv_pairs<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p, sc.inv_k0, sc.inv_v0);
+      pdl(k_inv_pairs, (unsigned)ceil_div(n, 256), 256, 0, stream)(p, sc.inv_k0, sc.inv_v0);
       note_launch();
       std::vector<SegDesc> segs;
       for (int s = 0; s < pl.nis; ++s) segs.push_back({(int64_t)s * B, B, sc.is_count + s});
@@ -1422,7 +1435,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       int rc = seg_sort_pairs(segs.data(), pl.nis, (int)bits_for(B), sc.inv_k0, sc.inv_v0,
                               sc.inv_k1, sc.inv_v1, sc.hist, &alt, stream);
       if (rc != RECD_OK) return rc;
-      k_csr_bounds<<<(unsigned)ceil_div(n, 256), 256, 0, stream>>>(p);
+      pdl(k_csr_bounds, (unsigned)ceil_div(n, 256), 256, 0, stream)(p);
       note_launch();
     }
     // 3-4. occurrences, sorted by ID per table segment
@@ -1444,7 +1457,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
           ob += std::max<int64_t>(1, ceil_div(value_caps[f], p.oc_ch));
         }
         p.occ_blk0[F] = ob;
-        k_rv<0><<<(unsigned)ob, 256, 0, stream>>>(p, nullptr, nullptr);
+        pdl(k_rv<0>, (unsigned)ob, 256, 0, stream)(p, nullptr, nullptr);
         std::vector<ScanDesc> bd;
         for (int f = 0; f < F; ++f)
           bd.push_back({sc.rv_blk + p.occ_blk0[f], sc.rv_blk + p.occ_blk0[f],
@@ -1456,8 +1469,8 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         BwdParams q1 = p;
         q1.occ_hist = sc.hist;
         q1.occ_bits = (int)bits_for(maxrows);
-        k_rv<1><<<(unsigned)ob, 256, 0, stream>>>(q1, sc.occ_k0, sc.occ_v0);
-        k_rv_len<<<(unsigned)num_sms() * 8, 256, 0, stream>>>(p);
+        pdl(k_rv<1>, (unsigned)ob, 256, 0, stream)(q1, sc.occ_k0, sc.occ_v0);
+        pdl(k_rv_len, (unsigned)num_sms() * 8, 256, 0, stream)(p);
         // 2. heads sorted by ID
         std::vector<SegDesc> hs;
         for (int s = 0; s < pl.nts; ++s) hs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.head_count + s});
@@ -1469,7 +1482,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         uint32_t* Hv = halt ? sc.occ_v1 : sc.occ_v0;
         // 3. run lengths in sorted order (+ overlapping IDs) -> expanded offsets
         RECD_CUDA_CHECK(cudaMemsetAsync(sc.fix_count, 0, sizeof(uint32_t), stream));
-        k_rv_lens<<<dim3((unsigned)num_sms() * 2, (unsigned)pl.nts), 256, 0, stream>>>(p, Hk, Hv);
+        pdl(k_rv_lens, dim3((unsigned)num_sms() * 2, (unsigned)pl.nts), 256, 0, stream)(p, Hk, Hv);
         std::vector<ScanDesc> sd;
         for (int s = 0; s < pl.nts; ++s)
           sd.push_back({sc.head_off + pl.ts_base[s], sc.head_off + pl.ts_base[s], pl.ts_cap[s],
@@ -1483,8 +1496,8 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
           p.ex_chunk0[s] = ec;
           ec += std::max<int64_t>(1, ceil_div(pl.ts_cap[s], RV_EX_CH));
         }
-        k_rv_expand<<<(unsigned)ec, 256, 0, stream>>>(p, Hk, Hv);
-        k_rv_fix<<<(unsigned)num_sms() * 2, 256, 0, stream>>>(p);
+        pdl(k_rv_expand, (unsigned)ec, 256, 0, stream)(p, Hk, Hv);
+        pdl(k_rv_fix, (unsigned)num_sms() * 2, 256, 0, stream)(p);
         note_launch(5);
         // 5. fallback (an overlapping ID with > RV_FIX_MAX values, or a full
         //    list): per-value occurrences + the full sort, gated on the flag;
@@ -1497,7 +1510,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         BwdParams q = p;
         q.occ_gate = sc.fallback;
         q.oc_ch = OC_CH_SMALL;
-        k_occ<<<(unsigned)ob, 256, 0, stream>>>(q, Xk, Xv);
+        pdl(k_occ, (unsigned)ob, 256, 0, stream)(q, Xk, Xv);
         std::vector<SegDesc> vs;
         for (int s = 0; s < pl.nts; ++s) vs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
         bool valt = false;
@@ -1516,7 +1529,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         BwdParams q = p;
         q.occ_hist = fuse ? sc.hist : nullptr;
         q.occ_bits = (int)bits_for(maxrows);
-        k_occ<<<(unsigned)ob, 256, 0, stream>>>(q, sc.occ_k0, sc.occ_v0);
+        pdl(k_occ, (unsigned)ob, 256, 0, stream)(q, sc.occ_k0, sc.occ_v0);
         note_launch();
         std::vector<SegDesc> segs;
         for (int s = 0; s < pl.nts; ++s) segs.push_back({pl.ts_base[s], pl.ts_cap[s], sc.seg_count + s});
@@ -1559,7 +1572,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       bool any_id = !RECD_GU_FLAT, any_inv = false;
       for (int f = 0; f < F; ++f) (p.feat_is[f] < 0 ? any_id : any_inv) = true;
       if (any_id) {
-        k_grad_u<C><<<grid, 256, 0, stream>>>(p);
+        pdl(k_grad_u<C>, grid, 256, 0, stream)(p);
         note_launch();
       }
       if (RECD_GU_FLAT && any_inv) {
@@ -1568,9 +1581,9 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
         const unsigned gf = (unsigned)std::min<int64_t>(
             ceil_div(ceil_div(B, ch) * F * ncb, 8), (int64_t)num_sms() * 16);
         if (small)
-          k_grad_u_flat<C, GU_CH_SMALL><<<std::max(gf, 1u), 256, 0, stream>>>(p);
+          pdl(k_grad_u_flat<C, GU_CH_SMALL>, std::max(gf, 1u), 256, 0, stream)(p);
         else
-          k_grad_u_flat<C, GU_CH><<<std::max(gf, 1u), 256, 0, stream>>>(p);
+          pdl(k_grad_u_flat<C, GU_CH>, std::max(gf, 1u), 256, 0, stream)(p);
         note_launch();
       }
     }
@@ -1578,9 +1591,9 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     if (run_scat) {
       if (!apply_sgd && s0 == 0) {
         if (pl.rc == RC_BIG)
-          k_run_count<RC_BIG><<<(unsigned)pl.rc_chunks, RC_BIG, 0, stream>>>(p);
+          pdl(k_run_count<RC_BIG>, (unsigned)pl.rc_chunks, RC_BIG, 0, stream)(p);
         else
-          k_run_count<RC_SMALL><<<(unsigned)pl.rc_chunks, RC_SMALL, 0, stream>>>(p);
+          pdl(k_run_count<RC_SMALL>, (unsigned)pl.rc_chunks, RC_SMALL, 0, stream)(p);
         note_launch();
         std::vector<ScanDesc> sd;
         for (int s = 0; s < pl.nts; ++s) {
@@ -1606,14 +1619,14 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       hook_before("k_scatter", stream);
       if (pl.rc == RC_BIG) {
         if (single)
-          k_scatter<C, true, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          pdl(k_scatter<C, true, RC_BIG>, std::max(g2, 1u), 256, 0, stream)(p);
         else
-          k_scatter<C, false, RC_BIG><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          pdl(k_scatter<C, false, RC_BIG>, std::max(g2, 1u), 256, 0, stream)(p);
       } else {
         if (single)
-          k_scatter<C, true, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          pdl(k_scatter<C, true, RC_SMALL>, std::max(g2, 1u), 256, 0, stream)(p);
         else
-          k_scatter<C, false, RC_SMALL><<<std::max(g2, 1u), 256, 0, stream>>>(p);
+          pdl(k_scatter<C, false, RC_SMALL>, std::max(g2, 1u), 256, 0, stream)(p);
       }
       hook_after("k_scatter", stream);
       note_launch();
@@ -1655,6 +1668,7 @@ extern "C" int recd_pool_bwd(int32_t num_features, int64_t batch_size, int32_t d
                              float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
                              float* const* grad_rows_out, int64_t* grad_counts_out,
                              void* scratch, size_t scratch_bytes, recd_stream_t stream) {
+  recd::PdlScope pdl_scope(batch_size * (int64_t)num_features);
   return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
                  uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
                  grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
@@ -1673,6 +1687,7 @@ extern "C" int recd_pool_bwd_prepare(int32_t num_features, int64_t batch_size, i
                                      float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
                                      float* const* grad_rows_out, int64_t* grad_counts_out,
                                      void* scratch, size_t scratch_bytes, recd_stream_t stream) {
+  recd::PdlScope pdl_scope(batch_size * (int64_t)num_features);
   return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
                  uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
                  grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
@@ -1687,6 +1702,7 @@ extern "C" int recd_pool_bwd_finish(int32_t num_features, int64_t batch_size, in
                                     float lr, int32_t apply_sgd, int64_t* const* grad_ids_out,
                                     float* const* grad_rows_out, int64_t* grad_counts_out,
                                     void* scratch, size_t scratch_bytes, recd_stream_t stream) {
+  recd::PdlScope pdl_scope(batch_size * (int64_t)num_features);
   return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
                  uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
                  grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,
@@ -1718,6 +1734,7 @@ extern "C" int recd_pool_bwd_stages(int32_t stages, int32_t num_features, int64_
                                     int64_t* const* grad_ids_out, float* const* grad_rows_out,
                                     int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
                                     recd_stream_t stream) {
+  recd::PdlScope pdl_scope(batch_size * (int64_t)num_features);
   if (stages <= 0 || (stages & ~PH_ALL)) return RECD_ERR_ARG;
   return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
                  uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,

@@ -45,6 +45,62 @@ inline int64_t grid_cap(const char* env, int per_sm) {
   return (int64_t)num_sms() * (e ? (atoi(e) > 0 ? atoi(e) : 1) : per_sm);
 }
 
+// Programmatic dependent launch (PDL).  Every kernel starts with
+// RECD_PDL_PROLOGUE(): griddepcontrol.wait blocks until the preceding kernel
+// of the stream has completed and its memory is visible (a no-op when the
+// kernel was launched without the attribute), then launch_dependents lets the
+// next kernel's CTAs be scheduled as soon as every CTA of this one started.
+// So a chain of small kernels (config 1: ~25 launches per step) overlaps each
+// launch with its predecessor instead of paying the launch latency in series.
+// pdl(k, grid, block, smem, stream)(args...) launches with the attribute
+// while a PdlScope of the calling API entry point allows it (RECD_PDL=0 never,
+// 1 always, default: steps of at most RECD_PDL_MAX batch rows x features --
+// on big steps early-resident CTAs would only hold SM slots a concurrent
+// side-stream kernel could use).
+#define RECD_PDL_PROLOGUE()                                          \
+  do {                                                               \
+    asm volatile("griddepcontrol.wait;" ::: "memory");               \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  \
+  } while (0)
+
+bool pdl_allowed();
+struct PdlScope {
+  bool prev;
+  explicit PdlScope(int64_t rows_x_features);
+  ~PdlScope();
+};
+
+template <typename... KArgs>
+struct PdlLaunch {
+  void (*k)(KArgs...);
+  dim3 grid, block;
+  size_t smem;
+  cudaStream_t stream;
+  template <typename... Args>
+  void operator()(Args&&... args) const {
+    if (!pdl_allowed()) {
+      k<<<grid, block, smem, stream>>>(static_cast<Args&&>(args)...);
+      return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<Args&&>(args)...);
+  }
+};
+template <typename... KArgs>
+PdlLaunch<KArgs...> pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem = 0,
+                        cudaStream_t stream = 0) {
+  return PdlLaunch<KArgs...>{k, grid, block, smem, stream};
+}
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 __host__ __device__ inline uint64_t next_pow2(uint64_t x) {

@@ -141,6 +141,7 @@ constexpr int RT_SMEM = RECD_RS_TMA ? 3 * RT_T * 8 : 0;       // dynamic shared 
 #endif
 template <int RS_RPB>
 __global__ void __launch_bounds__(RS_NT, RECD_RS_MINB) k_rowscan(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   const int g = p.rs_group[blockIdx.y];
   const int tid = threadIdx.x;
   const int64_t r0 = (int64_t)blockIdx.x * RS_RPB;
@@ -502,6 +503,7 @@ __global__ void __launch_bounds__(RS_NT, RECD_RS_MINB) k_rowscan(const __grid_co
 // heads only: open-addressing table (64-bit key, L2 resident),
 // rep = atomicMin(row) per key -> deterministic min row.
 __global__ void __launch_bounds__(256) k_insert(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)p.G * p.B) return;
   const int g = (int)(idx / p.B);
@@ -525,6 +527,7 @@ __global__ void __launch_bounds__(256) k_insert(const __grid_constant__ DedupPar
 
 // ---------------------------------------------------------------- resolve
 __global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)p.G * p.B) return;
   if (!p.head[idx]) return;
@@ -548,6 +551,7 @@ __global__ void __launch_bounds__(256) k_resolve(const __grid_constant__ DedupPa
 // reference's bucket scan does (tensors.py:288-297).
 constexpr int FB_NT = 256;
 __global__ void __launch_bounds__(FB_NT) k_fallback(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   const int g = blockIdx.x;
   if (!p.collide[g]) return;
   const int tid = threadIdx.x;
@@ -608,6 +612,7 @@ constexpr int NB_ITEMS = 8;
 constexpr int NB_CH = NB_NT * NB_ITEMS;  // rows per chunk
 
 __global__ void __launch_bounds__(NB_NT) k_num_reduce(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   const int g = blockIdx.y;
   const int64_t c = blockIdx.x;
   const int64_t B = p.B;
@@ -648,6 +653,7 @@ __global__ void __launch_bounds__(NB_NT) k_num_reduce(const __grid_constant__ De
 // block per group: chunk prefixes in place (rh -> incoming run head, an
 // exclusive max; nf / len -> exclusive sums) and the group's totals
 __global__ void __launch_bounds__(NB_NT) k_num_scan(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   const int g = blockIdx.x;
   const int tid = threadIdx.x;
   const int64_t nch = ceil_div(p.B, NB_CH);
@@ -692,6 +698,7 @@ __global__ void __launch_bounds__(NB_NT) k_num_scan(const __grid_constant__ Dedu
 }
 
 __global__ void __launch_bounds__(NB_NT) k_num_down(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   const int g = blockIdx.y;
   const int64_t c = blockIdx.x;
   const int64_t B = p.B;
@@ -766,6 +773,7 @@ __global__ void __launch_bounds__(NB_NT) k_num_down(const __grid_constant__ Dedu
 }
 
 __global__ void __launch_bounds__(256) k_num_inv(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)p.G * p.B) return;
   const int g = (int)(idx / p.B);
@@ -788,6 +796,7 @@ constexpr int CP_MAXR = 512;          // rows staged per pass
 
 
 __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupParams p) {
+  RECD_PDL_PROLOGUE();
   int f = 0;
   while (f + 1 < p.F && p.cp_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
   const int64_t j0 = ((int64_t)blockIdx.x - p.cp_blk0[f]) * p.cp_ch;
@@ -1047,9 +1056,9 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
           DedupParams q = p;
           for (int k = k0; k < k1; ++k) q.rs_group[k - k0] = p.rs_group[k];
           const dim3 grid((unsigned)ceil_div(B, rpb), (unsigned)(k1 - k0));
-          if (rpb == 2048) k_rowscan<2048><<<grid, RS_NT, RT_SMEM, stream>>>(q);
-          else if (rpb == 1024) k_rowscan<1024><<<grid, RS_NT, RT_SMEM, stream>>>(q);
-          else k_rowscan<RS_RPB><<<grid, RS_NT, RT_SMEM, stream>>>(q);
+          if (rpb == 2048) pdl(k_rowscan<2048>, grid, RS_NT, RT_SMEM, stream)(q);
+          else if (rpb == 1024) pdl(k_rowscan<1024>, grid, RS_NT, RT_SMEM, stream)(q);
+          else pdl(k_rowscan<RS_RPB>, grid, RS_NT, RT_SMEM, stream)(q);
           note_launch();
           k0 = k1;
         };
@@ -1060,14 +1069,14 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
         launch_class(k1, 1024);
         launch_class(p.G, 2048);
       }
-      k_insert<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
-      k_resolve<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
-      k_fallback<<<p.G, FB_NT, 0, stream>>>(p);
+      pdl(k_insert, (unsigned)ceil_div(rows, 256), 256, 0, stream)(p);
+      pdl(k_resolve, (unsigned)ceil_div(rows, 256), 256, 0, stream)(p);
+      pdl(k_fallback, p.G, FB_NT, 0, stream)(p);
       const dim3 ng((unsigned)ceil_div(B, NB_CH), p.G);
-      k_num_reduce<<<ng, NB_NT, 0, stream>>>(p);
-      k_num_scan<<<p.G, NB_NT, 0, stream>>>(p);
-      k_num_down<<<ng, NB_NT, 0, stream>>>(p);
-      k_num_inv<<<(unsigned)ceil_div(rows, 256), 256, 0, stream>>>(p);
+      pdl(k_num_reduce, ng, NB_NT, 0, stream)(p);
+      pdl(k_num_scan, p.G, NB_NT, 0, stream)(p);
+      pdl(k_num_down, ng, NB_NT, 0, stream)(p);
+      pdl(k_num_inv, (unsigned)ceil_div(rows, 256), 256, 0, stream)(p);
       note_launch(7);
     }
     if (phase & DD_COPY) {
@@ -1082,7 +1091,7 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
         cblk += std::max<int64_t>(1, ceil_div(p.nvalues[ff], p.cp_ch));
       }
       p.cp_blk0[p.F] = cblk;
-      k_copy<<<(unsigned)cblk, CP_NT, 0, stream>>>(p);
+      pdl(k_copy, (unsigned)cblk, CP_NT, 0, stream)(p);
       note_launch(1);
     }
     RECD_LAUNCH_CHECK();
@@ -1098,6 +1107,7 @@ extern "C" int recd_dedup(int32_t num_groups, const int32_t* group_sizes, int64_
                           int64_t* const* uoffsets_out, int64_t* const* uvalues_out,
                           int64_t* counts_out, void* scratch, size_t scratch_bytes,
                           recd_stream_t stream) {
+  recd::PdlScope pdl_scope(batch_size * (int64_t)num_groups);
   return run_dedup(num_groups, group_sizes, batch_size, values, offsets, num_values, inverse_out,
                    uoffsets_out, uvalues_out, counts_out, scratch, scratch_bytes,
                    (cudaStream_t)stream, DD_ALL, nullptr, nullptr);
@@ -1144,6 +1154,7 @@ extern "C" int recd_dedup_ex(int32_t num_groups, const int32_t* group_sizes, int
                              int64_t* counts_out, int64_t* const* remote_values,
                              const int64_t* const* remote_base, void* scratch,
                              size_t scratch_bytes, recd_stream_t stream) {
+  recd::PdlScope pdl_scope(batch_size * (int64_t)num_groups);
   if (!num_values_dev || !value_caps || phase < 1 || phase > 3) return RECD_ERR_ARG;
   return run_dedup(num_groups, group_sizes, batch_size, values, offsets, value_caps, inverse_out,
                    uoffsets_out, uvalues_out, counts_out, scratch, scratch_bytes,

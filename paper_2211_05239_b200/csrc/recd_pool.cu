@@ -110,6 +110,7 @@ __device__ __forceinline__ void store_pooled(const PoolParams& p, int f, int64_t
 
 template <class C>
 __global__ void __launch_bounds__(256, RECD_POOL_MINB) k_pool_fwd(const __grid_constant__ PoolParams p) {
+  RECD_PDL_PROLOGUE();
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
   const int ncb = col_blocks<C>(p.D);
   if (threadIdx.x == 0) {
@@ -155,6 +156,7 @@ constexpr int EXP_RF = RECD_EXPAND_RF;  // row copies in flight per lane
 // per lane) and streamed out.
 template <class C>
 __global__ void __launch_bounds__(256) k_expand(const __grid_constant__ PoolParams p) {
+  RECD_PDL_PROLOGUE();
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
   const int ncb = col_blocks<C>(p.D);
   const int64_t rb = ceil_div(p.B, 32);  // 32-row blocks per feature
@@ -206,6 +208,7 @@ template <class C>
 __global__ void __launch_bounds__(256) k_lookup(const float* W, int64_t rows, int D,
                                                 const int64_t* ids, int64_t n, float* out,
                                                 int64_t* err) {
+  RECD_PDL_PROLOGUE();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t total = n * col_blocks<C>(D);
@@ -224,6 +227,7 @@ template <class C>
 __global__ void __launch_bounds__(256, 3) k_pool_dense(const float* A, int64_t nvals, int D,
                                                        const int64_t* offsets, int64_t nrows,
                                                        int mode, float* out) {
+  RECD_PDL_PROLOGUE();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t total = nrows * col_blocks<C>(D);
@@ -445,6 +449,7 @@ __device__ __forceinline__ void pairwise_ring(RingRows<NB>& rr, int32_t m, float
 
 template <class C, int K>
 __global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_constant__ PoolParams p) {
+  RECD_PDL_PROLOGUE();
   static_assert(C::VW == 4, "ring pool streams float4 lane slices");
   extern __shared__ __align__(128) float s_ring[];
   __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];
@@ -549,11 +554,11 @@ static int launch_pool_fwd(const PoolParams& p, int mode, bool share, unsigned g
       const int res = (dev >= 0 && dev < 64) ? resident[dev] : 1;
       const int per_sm = env_ctas ? env_ctas : std::max(1, share ? res - 1 : res);
       grid = std::min<unsigned>(grid, (unsigned)(num_sms() * per_sm));
-      k_pool_ring<C, K><<<grid, 256, smem, stream>>>(p);
+      pdl(k_pool_ring<C, K>, grid, 256, smem, stream)(p);
       return RECD_OK;
     }
   }
-  k_pool_fwd<C><<<grid, 256, 0, stream>>>(p);
+  pdl(k_pool_fwd<C>, grid, 256, 0, stream)(p);
   return RECD_OK;
 }
 
@@ -579,6 +584,7 @@ static int pool_fwd_impl(int32_t num_features, int64_t batch_size, int32_t dim, 
                          const int32_t* const* csr_start, const uint32_t* const* csr_rows,
                          float* const* pooled_out, float* const* out, int64_t* err,
                          recd_stream_t stream_) {
+  recd::PdlScope pdl_scope(batch_size * (int64_t)num_features);
   cudaStream_t stream = (cudaStream_t)stream_;
   const bool csr = csr_start != nullptr;
   const bool share = (mode & RECD_POOL_SHARE) != 0;
@@ -632,7 +638,7 @@ static int pool_fwd_impl(int32_t num_features, int64_t batch_size, int32_t dim, 
       hook_after("k_pool_fwd", stream);
       note_launch();
       if (any_expand) {
-        k_expand<C><<<expand_grid(batch_size, p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
+        pdl(k_expand<C>, expand_grid(batch_size, p.F * col_blocks<C>(dim)), 256, 0, stream)(p);
         note_launch();
       }
     });
@@ -722,7 +728,7 @@ extern "C" int recd_embedding_lookup(const float* table, int64_t table_rows, int
   RECD_CUDA_CHECK(cudaMemsetAsync(err, 0x7f, sizeof(int64_t), stream));
   if (n == 0) return RECD_OK;
   int rc = RECD_DISPATCH_COL(dim, {
-    k_lookup<C><<<grid_for(n * col_blocks<C>(dim)), 256, 0, stream>>>(table, table_rows, dim,
+    pdl(k_lookup<C>, grid_for(n * col_blocks<C>(dim)), 256, 0, stream)(table, table_rows, dim,
                                                                       values, n, out, err);
     note_launch();
   });
@@ -738,7 +744,7 @@ extern "C" int recd_pool_dense(const float* acts, int64_t n_values, int32_t dim,
   if (dim <= 0 || n_rows < 0 || mode < 0 || mode > 2) return RECD_ERR_ARG;
   if (n_rows == 0) return RECD_OK;
   int rc = RECD_DISPATCH_COL(dim, {
-    k_pool_dense<C><<<grid_for(n_rows * col_blocks<C>(dim)), 256, 0, stream>>>(
+    pdl(k_pool_dense<C>, grid_for(n_rows * col_blocks<C>(dim)), 256, 0, stream)(
         acts, n_values, dim, offsets, n_rows, mode, out);
     note_launch();
   });
@@ -750,6 +756,7 @@ extern "C" int recd_pool_dense(const float* acts, int64_t n_values, int32_t dim,
 extern "C" int recd_expand(int32_t num_features, int64_t batch_size, int32_t dim,
                            const int64_t* const* inverse, const float* const* pooled,
                            float* const* out, recd_stream_t stream_) {
+  recd::PdlScope pdl_scope(batch_size * (int64_t)num_features);
   cudaStream_t stream = (cudaStream_t)stream_;
   if (num_features <= 0 || batch_size < 0 || dim <= 0 || !pooled || !out) return RECD_ERR_ARG;
   for (int f0 = 0; f0 < num_features; f0 += RECD_MAX_FEAT) {
@@ -765,7 +772,7 @@ extern "C" int recd_expand(int32_t num_features, int64_t batch_size, int32_t dim
       if (!p.pooled[f] || !p.out[f]) return RECD_ERR_ARG;
     }
     int rc = RECD_DISPATCH_COL(dim, {
-      k_expand<C><<<expand_grid(batch_size, p.F * col_blocks<C>(dim)), 256, 0, stream>>>(p);
+      pdl(k_expand<C>, expand_grid(batch_size, p.F * col_blocks<C>(dim)), 256, 0, stream)(p);
       note_launch();
     });
     if (rc != RECD_OK) return rc;

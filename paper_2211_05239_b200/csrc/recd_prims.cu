@@ -77,6 +77,7 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
 }
 
 __global__ void __launch_bounds__(OS_NT) k_os_hist(const __grid_constant__ OsParams p) {
+  RECD_PDL_PROLOGUE();
   if (os_gated_off(p)) return;
   const int64_t chunk = blockIdx.x;
   int s = 0;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(OS_NT) k_os_hist(const __grid_constant__ OsPar
 
 // block per (segment, pass): exclusive digit scan; block 0 also the tile prefix
 __global__ void __launch_bounds__(OS_NT) k_os_setup(const __grid_constant__ OsParams p) {
+  RECD_PDL_PROLOGUE();
   if (os_gated_off(p)) return;
   __shared__ int64_t s_scan[32];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(OS_NT) k_os_setup(const __grid_constant__ OsPa
 #define RECD_OS_MINB 3
 #endif
 __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_constant__ OsParams p) {
+  RECD_PDL_PROLOGUE();
   if (os_gated_off(p)) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t mask = (1u << p.nbits) - 1u;
@@ -338,12 +341,12 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
       // counters and the first pass's tile status words need clearing
       RECD_CUDA_CHECK(cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * OS_MAXPASS, stream));
       RECD_CUDA_CHECK(cudaMemsetAsync(p.status, 0, sizeof(uint32_t) * p.total_tcap * 256, stream));
-      k_os_setup<<<p.S * npass, OS_NT, 0, stream>>>(p);
+      pdl(k_os_setup, p.S * npass, OS_NT, 0, stream)(p);
       note_launch(1);
     } else {
       RECD_CUDA_CHECK(cudaMemsetAsync(p.ghist, 0, sizeof(uint32_t) * p.S * OS_MAXPASS * 256, stream));
-      k_os_hist<<<(unsigned)p.total_hchunks, OS_NT, 0, stream>>>(p);
-      k_os_setup<<<p.S * npass, OS_NT, 0, stream>>>(p);
+      pdl(k_os_hist, (unsigned)p.total_hchunks, OS_NT, 0, stream)(p);
+      pdl(k_os_setup, p.S * npass, OS_NT, 0, stream)(p);
       note_launch(2);
     }
     uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
@@ -352,7 +355,7 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
       p.shift = 8 * pass;
       p.nbits = std::min(8, bits - 8 * pass);
       p.kin = ki; p.vin = vi; p.kout = ko; p.vout = vo;
-      k_onesweep<<<(unsigned)std::min<int64_t>(os_grid(), p.total_tcap), OS_NT, 0, stream>>>(p);
+      pdl(k_onesweep, (unsigned)std::min<int64_t>(os_grid(), p.total_tcap), OS_NT, 0, stream)(p);
       note_launch();
       std::swap(ki, ko);
       std::swap(vi, vo);
@@ -401,6 +404,7 @@ __device__ __forceinline__ int scan_seg(const ScanParams& p, int64_t chunk) {
 }
 
 __global__ void __launch_bounds__(XS_NT) k_scan_reduce(const __grid_constant__ ScanParams p) {
+  RECD_PDL_PROLOGUE();
   const int64_t chunk = blockIdx.x;
   const ScanSegDev& sg = p.seg[scan_seg(p, chunk)];
   const int64_t n = sg.count ? *sg.count : sg.cap;
@@ -414,6 +418,7 @@ __global__ void __launch_bounds__(XS_NT) k_scan_reduce(const __grid_constant__ S
 }
 
 __global__ void __launch_bounds__(1024) k_scan_parts(const __grid_constant__ ScanParams p) {
+  RECD_PDL_PROLOGUE();
   const ScanSegDev& sg = p.seg[blockIdx.x];
   __shared__ int64_t s_scan[32];
   int64_t carry = 0;
@@ -429,6 +434,7 @@ __global__ void __launch_bounds__(1024) k_scan_parts(const __grid_constant__ Sca
 }
 
 __global__ void __launch_bounds__(XS_NT) k_scan_down(const __grid_constant__ ScanParams p) {
+  RECD_PDL_PROLOGUE();
   const int64_t chunk = blockIdx.x;
   const ScanSegDev& sg = p.seg[scan_seg(p, chunk)];
   const int64_t n = sg.count ? *sg.count : sg.cap;
@@ -484,9 +490,9 @@ int seg_exclusive_scan(const ScanDesc* segs, int S, int64_t* part, cudaStream_t 
     ScanParams p;
     build_scan_params(segs + s0, std::min(XS_MAXSEG, S - s0), &p);
     p.part = part;
-    k_scan_reduce<<<(unsigned)p.total_chunks, XS_NT, 0, stream>>>(p);
-    k_scan_parts<<<p.S, 1024, 0, stream>>>(p);
-    k_scan_down<<<(unsigned)p.total_chunks, XS_NT, 0, stream>>>(p);
+    pdl(k_scan_reduce, (unsigned)p.total_chunks, XS_NT, 0, stream)(p);
+    pdl(k_scan_parts, p.S, 1024, 0, stream)(p);
+    pdl(k_scan_down, (unsigned)p.total_chunks, XS_NT, 0, stream)(p);
     note_launch(3);
   }
   RECD_LAUNCH_CHECK();

@@ -20,6 +20,23 @@ void hook_after(const char* name, cudaStream_t s) {
 
 static std::atomic<int64_t> g_launches{0};
 
+static thread_local bool t_pdl = false;
+static int pdl_mode() {  // 0 never, 1 always, 2 small steps only
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("RECD_PDL");
+    m = e ? (atoi(e) ? 1 : 0) : 2;
+  }
+  return m;
+}
+bool pdl_allowed() { return t_pdl; }
+PdlScope::PdlScope(int64_t rows_x_features) : prev(t_pdl) {
+  static const int64_t lim = getenv("RECD_PDL_MAX") ? atoll(getenv("RECD_PDL_MAX")) : (1 << 17);
+  const int m = pdl_mode();
+  t_pdl = m == 1 || (m == 2 && rows_x_features <= lim);
+}
+PdlScope::~PdlScope() { t_pdl = prev; }
+
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int num_sms() {
