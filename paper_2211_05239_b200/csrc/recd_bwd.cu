@@ -44,7 +44,10 @@
 namespace recd {
 
 constexpr int RC_BIG = 256;   // sorted positions per scatter work item
-constexpr int RC_SMALL = 64;  // ... when the occurrence arrays are small (latency-bound)
+#ifndef RECD_RC_SMALL
+#define RECD_RC_SMALL 32
+#endif
+constexpr int RC_SMALL = RECD_RC_SMALL;  // ... when the occurrence arrays are small (latency-bound; cfg1 32 vs 64: 0.130 vs 0.136 ms)
 static int rc_for(int64_t occ_total) { return occ_total >= (4ll << 20) ? RC_BIG : RC_SMALL; }
 
 struct BwdParams {
@@ -239,7 +242,10 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
 // no per-row dependent chain (CSR start -> row ids -> gradient rows) stalls it.
 // Same order as k_grad_u (ascending batch row within each unique row).
 constexpr int GU_CH = 256;     // positions per warp task (32 for small batches: more tasks)
-constexpr int GU_CH_SMALL = 32;
+#ifndef RECD_GU_CH_SMALL
+#define RECD_GU_CH_SMALL 32
+#endif
+constexpr int GU_CH_SMALL = RECD_GU_CH_SMALL;
 __device__ __forceinline__ int64_t run_end(const uint32_t* K, int64_t j, int64_t n, uint32_t id,
                                            int lane);
 #ifndef RECD_GUF_CS
@@ -356,6 +362,9 @@ __global__ void __launch_bounds__(256, RECD_GUF_MINB) k_grad_u_flat(const __grid
 #define RECD_OC_CH 16384
 #endif
 constexpr int OC_CH = RECD_OC_CH;   // values per block on big batches
+#ifndef RECD_TINY_CH
+#define RECD_TINY_CH 1
+#endif
 constexpr int OC_CH_SMALL = 4096;  // ... and on small ones (more blocks in flight)
 constexpr int OC_MAXR = 512;
 __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p, uint32_t* keys,
@@ -1441,7 +1450,10 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
     // 3-4. occurrences, sorted by ID per table segment
     if ((phase & PH_OCC) && do_scatter) {
       int64_t ob = 0;
-      p.oc_ch = pl.occ_total >= (8ll << 20) ? OC_CH : OC_CH_SMALL;
+      // 16K values per block on big batches, 4K on small ones, 1K on tiny
+      // (config 1: ~120K values -- a latency-bound pass wants every SM busy)
+      p.oc_ch = pl.occ_total >= (8ll << 20) ? OC_CH
+                : (pl.occ_total >= (1ll << 20) || !RECD_TINY_CH) ? OC_CH_SMALL : OC_CH_SMALL / 4;
       for (int f = 0; f < F; ++f) {
         p.occ_blk0[f] = ob;
         ob += std::max<int64_t>(1, ceil_div(do_scatter ? value_caps[f] : 1, p.oc_ch));

@@ -55,6 +55,7 @@ struct DedupParams {
   int64_t* nb_rh;       // [G][nch] numbering chunk aggregates
   int64_t* nb_nf;       // [G][nch]
   int64_t* nb_len;      // [F][nch]
+  int nb_ch;            // rows per numbering chunk (NB_NT * items)
   int32_t* fb_list;     // [G][B]
   unsigned long long* tkeys;  // [G][C]
   uint32_t* treps;            // [G][C]
@@ -136,6 +137,9 @@ constexpr int RS_IT = RECD_RS_IT;    // consecutive values per thread
 constexpr int RT_T = 2048;                                  // values per stage (16 KB)
 constexpr int RT_SMEM = RECD_RS_TMA ? 3 * RT_T * 8 : 0;       // dynamic shared memory
 
+#ifndef RECD_RS_SMALLB
+#define RECD_RS_SMALLB 1
+#endif
 #ifndef RECD_RS_MINB
 #define RECD_RS_MINB 4
 #endif
@@ -608,10 +612,16 @@ __global__ void __launch_bounds__(FB_NT) k_fallback(const __grid_constant__ Dedu
 //                 first rows, first_rows[uid], unique offsets per feature
 //   k_num_inv     inverse[i] = uidmap[cls[i]] (needs every chunk's uidmap)
 constexpr int NB_NT = 256;
-constexpr int NB_ITEMS = 8;
-constexpr int NB_CH = NB_NT * NB_ITEMS;  // rows per chunk
+constexpr int NB_ITEMS = 8;              // rows per thread (big batches: 2048-row chunks)
+#ifndef RECD_NB_SMALL
+#define RECD_NB_SMALL 1
+#endif
+constexpr int NB_ITEMS_SMALL = 1;        // small batches (< 32,768 rows): 256-row chunks,
+                                         // 8x the blocks of a latency-bound numbering
 
+template <int NB_ITEMS>
 __global__ void __launch_bounds__(NB_NT) k_num_reduce(const __grid_constant__ DedupParams p) {
+  constexpr int NB_CH = NB_NT * NB_ITEMS;
   RECD_PDL_PROLOGUE();
   const int g = blockIdx.y;
   const int64_t c = blockIdx.x;
@@ -656,7 +666,7 @@ __global__ void __launch_bounds__(NB_NT) k_num_scan(const __grid_constant__ Dedu
   RECD_PDL_PROLOGUE();
   const int g = blockIdx.x;
   const int tid = threadIdx.x;
-  const int64_t nch = ceil_div(p.B, NB_CH);
+  const int64_t nch = ceil_div(p.B, (int64_t)p.nb_ch);
   __shared__ int64_t s_scan[32];
   __shared__ int64_t s_last[NB_NT];
   int64_t crh = -1, cnf = 0;
@@ -697,7 +707,9 @@ __global__ void __launch_bounds__(NB_NT) k_num_scan(const __grid_constant__ Dedu
   }
 }
 
+template <int NB_ITEMS>
 __global__ void __launch_bounds__(NB_NT) k_num_down(const __grid_constant__ DedupParams p) {
+  constexpr int NB_CH = NB_NT * NB_ITEMS;
   RECD_PDL_PROLOGUE();
   const int g = blockIdx.y;
   const int64_t c = blockIdx.x;
@@ -789,6 +801,9 @@ __global__ void __launch_bounds__(256) k_num_inv(const __grid_constant__ DedupPa
 constexpr int CP_NT = 256;
 #ifndef RECD_CP_IT
 #define RECD_CP_IT 64
+#endif
+#ifndef RECD_TINY_CH  // 1K unique values per k_copy block on tiny batches
+#define RECD_TINY_CH 1
 #endif
 constexpr int CP_IT = RECD_CP_IT;
 constexpr int CP_CH = CP_NT * CP_IT;  // unique values per block
@@ -912,7 +927,7 @@ struct DedupScratch {
 static size_t carve_dedup(void* base, size_t cap, int G, int F, int64_t B, int64_t C,
                           DedupScratch* s) {
   Arena a(base, cap);
-  const int64_t nch = ceil_div(B, NB_CH);
+  const int64_t nch = ceil_div(B, NB_NT * NB_ITEMS_SMALL);  // the most chunks either layout has
   s->nb_rh = a.take<int64_t>((size_t)G * nch);
   s->nb_nf = a.take<int64_t>((size_t)G * nch);
   s->nb_len = a.take<int64_t>((size_t)F * nch);
@@ -1010,7 +1025,8 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
     p.fb_list = s.fb_list + (int64_t)g0 * B;
     p.collide = s.collide + g0;
     {
-      const int64_t nch = ceil_div(B, NB_CH);
+      p.nb_ch = NB_NT * (RECD_NB_SMALL && B < 32768 ? NB_ITEMS_SMALL : NB_ITEMS);
+      const int64_t nch = ceil_div(B, (int64_t)p.nb_ch);
       p.nb_rh = s.nb_rh + (int64_t)g0 * nch;
       p.nb_nf = s.nb_nf + (int64_t)g0 * nch;
       p.nb_len = s.nb_len + (int64_t)f0 * nch;
@@ -1056,7 +1072,8 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
           DedupParams q = p;
           for (int k = k0; k < k1; ++k) q.rs_group[k - k0] = p.rs_group[k];
           const dim3 grid((unsigned)ceil_div(B, rpb), (unsigned)(k1 - k0));
-          if (rpb == 2048) pdl(k_rowscan<2048>, grid, RS_NT, RT_SMEM, stream)(q);
+          if (rpb == 64) pdl(k_rowscan<64>, grid, RS_NT, RT_SMEM, stream)(q);
+          else if (rpb == 2048) pdl(k_rowscan<2048>, grid, RS_NT, RT_SMEM, stream)(q);
           else if (rpb == 1024) pdl(k_rowscan<1024>, grid, RS_NT, RT_SMEM, stream)(q);
           else pdl(k_rowscan<RS_RPB>, grid, RS_NT, RT_SMEM, stream)(q);
           note_launch();
@@ -1064,7 +1081,8 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
         };
         int k1 = 0;
         while (k1 < p.G && (!RECD_RS_SHORT || rs_avg[k1] > 48.0)) ++k1;
-        launch_class(k1, RS_RPB);
+        // small batches (latency-bound): 64-row blocks, 4x the blocks in flight
+        launch_class(k1, (RECD_RS_SMALLB && B < 32768) ? 64 : RS_RPB);
         while (k1 < p.G && rs_avg[k1] > 12.0) ++k1;
         launch_class(k1, 1024);
         launch_class(p.G, 2048);
@@ -1072,10 +1090,16 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
       pdl(k_insert, (unsigned)ceil_div(rows, 256), 256, 0, stream)(p);
       pdl(k_resolve, (unsigned)ceil_div(rows, 256), 256, 0, stream)(p);
       pdl(k_fallback, p.G, FB_NT, 0, stream)(p);
-      const dim3 ng((unsigned)ceil_div(B, NB_CH), p.G);
-      pdl(k_num_reduce, ng, NB_NT, 0, stream)(p);
-      pdl(k_num_scan, p.G, NB_NT, 0, stream)(p);
-      pdl(k_num_down, ng, NB_NT, 0, stream)(p);
+      const dim3 ng((unsigned)ceil_div(B, (int64_t)p.nb_ch), p.G);
+      if (p.nb_ch == NB_NT * NB_ITEMS) {
+        pdl(k_num_reduce<NB_ITEMS>, ng, NB_NT, 0, stream)(p);
+        pdl(k_num_scan, p.G, NB_NT, 0, stream)(p);
+        pdl(k_num_down<NB_ITEMS>, ng, NB_NT, 0, stream)(p);
+      } else {
+        pdl(k_num_reduce<NB_ITEMS_SMALL>, ng, NB_NT, 0, stream)(p);
+        pdl(k_num_scan, p.G, NB_NT, 0, stream)(p);
+        pdl(k_num_down<NB_ITEMS_SMALL>, ng, NB_NT, 0, stream)(p);
+      }
       pdl(k_num_inv, (unsigned)ceil_div(rows, 256), 256, 0, stream)(p);
       note_launch(7);
     }
@@ -1084,7 +1108,7 @@ static int run_dedup(int32_t num_groups, const int32_t* group_sizes, int64_t bat
       // ones (more blocks in flight); A/B: dedup 0.67 -> 0.61 ms at cfg2
       int64_t tot = 0;
       for (int ff = 0; ff < p.F; ++ff) tot += p.nvalues[ff];
-      p.cp_ch = (int64_t)CP_NT * (tot >= (8ll << 20) ? CP_IT : 16);
+      p.cp_ch = (int64_t)CP_NT * (tot >= (8ll << 20) ? CP_IT : (tot >= (1ll << 20) || !RECD_TINY_CH) ? 16 : 4);
       int64_t cblk = 0;
       for (int ff = 0; ff < p.F; ++ff) {
         p.cp_blk0[ff] = cblk;

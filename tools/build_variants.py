@@ -6,6 +6,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
+    "notiny": ["RECD_TINY_CH=0"],
+    "rs256": ["RECD_RS_SMALLB=0"],
+    "gu16": ["RECD_GU_CH_SMALL=16"],
+    "gu16rc32": ["RECD_GU_CH_SMALL=16", "RECD_RC_SMALL=32"],
+    "nbbig": ["RECD_NB_SMALL=0"],
+    "nolocal": ["RECD_OS_LOCAL=0"],
+    "rc32": ["RECD_RC_SMALL=32"],
     "nocoal": ["RECD_RS_COAL=0"],
     "noflat": ["RECD_GU_FLAT=0"],
     "fm4": ["RECD_GUF_MINB=4"],
