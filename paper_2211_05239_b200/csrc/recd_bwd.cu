@@ -1434,6 +1434,10 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   }
   {
     // 1. inverse CSR
+    // (a one-CTA-per-segment kernel building the pairs, sorting them and
+    // writing the run starts in one launch was slower at config 1 -- 0.119
+    // vs 0.114 ms: the CSR then runs on 8 SMs on the side stream's critical
+    // path; the sort alone takes the one-CTA path, k_local_sort)
     if ((phase & PH_INV) && do_grad && pl.nis > 0) {
       const int64_t n = (int64_t)pl.nis * B;
       pdl(k_inv_pairs, (unsigned)ceil_div(n, 256), 256, 0, stream)(p, sc.inv_k0, sc.inv_v0);

@@ -279,78 +279,25 @@ __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_c
 // look-back, no global round trip between passes, one launch instead of
 // memset + k_os_hist + k_os_setup + one k_onesweep per pass.  The result goes
 // where the multi-pass sort would leave it (alt buffers for an odd pass count).
-__global__ void __launch_bounds__(OS_NT) k_local_sort(const __grid_constant__ OsParams p) {
+__global__ void __launch_bounds__(LS_NT) k_local_sort(const __grid_constant__ OsParams p) {
   RECD_PDL_PROLOGUE();
   if (os_gated_off(p)) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt = lanemask_lt();
-  __shared__ uint32_t s_wcnt[OS_WARPS][256];
-  __shared__ uint32_t s_tdb[256];
-  __shared__ uint32_t s_keys[OS_TILE];
-  __shared__ uint32_t s_vals[OS_TILE];
-  __shared__ int64_t s_scan[32];
+  __shared__ LocalSortSmem sm;
   const OsSeg& sg = p.seg[blockIdx.x];
-  const int tn = (int)min((int64_t)OS_TILE, *sg.count);
-  uint32_t key[OS_ITEMS], val[OS_ITEMS], rank[OS_ITEMS];
+  const int tn = (int)min((int64_t)LS_TILE, *sg.count);
+  uint32_t key[LS_ITEMS], val[LS_ITEMS];
 #pragma unroll
-  for (int r = 0; r < OS_ITEMS; ++r) {
-    const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
+  for (int r = 0; r < LS_ITEMS; ++r) {
+    const int e = ls_elem(r);
     key[r] = e < tn ? __ldg(p.kin + sg.base + e) : 0u;
     val[r] = e < tn ? __ldg(p.vin + sg.base + e) : 0u;
   }
-  for (int pass = 0; pass < p.npass; ++pass) {
-    const int shift = 8 * pass;
-    const uint32_t mask = (1u << min(8, p.bits - shift)) - 1u;
-    for (int d = lane; d < 256; d += 32) s_wcnt[warp][d] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < OS_ITEMS; ++r) {
-      const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
-      const bool valid = e < tn;
-      const uint32_t d = valid ? ((key[r] >> shift) & mask) : 0x100u;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      uint32_t before = 0;
-      if (valid) before = s_wcnt[warp][d];
-      __syncwarp();
-      if (valid && lane == __ffs(peers) - 1) s_wcnt[warp][d] = before + __popc(peers);
-      __syncwarp();
-      rank[r] = before + __popc(peers & lt);
-    }
-    __syncthreads();
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int w = 0; w < OS_WARPS; ++w) {
-      const uint32_t c = s_wcnt[w][tid];
-      s_wcnt[w][tid] = cnt;
-      cnt += c;
-    }
-    int64_t tot;
-    s_tdb[tid] = (uint32_t)block_exclusive_scan<OS_NT>(cnt, s_scan, &tot);
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < OS_ITEMS; ++r) {
-      const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
-      if (e < tn) {
-        const uint32_t d = (key[r] >> shift) & mask;
-        const uint32_t lp = s_tdb[d] + s_wcnt[warp][d] + rank[r];
-        s_keys[lp] = key[r];
-        s_vals[lp] = val[r];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < OS_ITEMS; ++r) {
-      const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
-      key[r] = e < tn ? s_keys[e] : 0u;
-      val[r] = e < tn ? s_vals[e] : 0u;
-    }
-    __syncthreads();
-  }
+  local_sort_tile(key, val, tn, p.bits, sm);
   uint32_t* ko = (p.npass & 1) ? p.kout : const_cast<uint32_t*>(p.kin);
   uint32_t* vo = (p.npass & 1) ? p.vout : const_cast<uint32_t*>(p.vin);
-  for (int e = tid; e < tn; e += OS_NT) {
-    ko[sg.base + e] = s_keys[e];
-    vo[sg.base + e] = s_vals[e];
+  for (int e = threadIdx.x; e < tn; e += LS_NT) {
+    ko[sg.base + e] = sm.keys[e];
+    vo[sg.base + e] = sm.vals[e];
   }
 }
 
@@ -409,7 +356,7 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
   for (int s = 0; s < S; ++s)
     if (segs[s].cap > (int64_t)OS_CNT) return RECD_ERR_UNSUPPORTED;
   bool local = RECD_OS_LOCAL != 0;
-  for (int s = 0; s < S; ++s) local &= segs[s].cap <= OS_TILE;
+  for (int s = 0; s < S; ++s) local &= segs[s].cap <= LS_TILE;
   for (int s0 = 0; s0 < S; s0 += OS_MAXSEG) {
     OsParams p;
     build_os_params(segs + s0, std::min(OS_MAXSEG, S - s0), &p);
@@ -418,7 +365,7 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
       p.bits = bits;
       p.gate = gate;
       p.kin = keys; p.vin = vals; p.kout = keys_alt; p.vout = vals_alt;
-      pdl(k_local_sort, p.S, OS_NT, 0, stream)(p);
+      pdl(k_local_sort, p.S, LS_NT, 0, stream)(p);
       note_launch();
       continue;
     }
