@@ -105,3 +105,51 @@ def test_long_rows_pairwise_tree():
     for op in ("sum", "avg", "max"):
         [out] = R.pooled_lookup([R.JaggedTensor(vals, offs)], [t], op)
         np.testing.assert_array_equal(out.cpu().numpy(), oracle.pooled_lookup(vals, offs, w, op))
+
+
+def _chains(rng, L, nrows, vocab, brk_p):
+    """Unique rows of one length L built as chains of one-position shifts
+    (row u+1 = row u [1:] + [x]) broken with probability brk_p."""
+    rows, cur = [], list(rng.integers(0, vocab, L))
+    for _ in range(nrows):
+        rows.append(cur)
+        if rng.random() < brk_p:
+            cur = list(rng.integers(0, vocab, L))
+        else:
+            cur = cur[1:] + [int(rng.integers(0, vocab))]
+    return rows
+
+
+@pytest.mark.parametrize("L", [2, 3, 8, 9, 128, 129, 256, 300, 512, 513])
+@pytest.mark.parametrize("brk_p", [0.0, 0.3, 0.9])
+def test_shifted_window_sharing_bit_exact(L, brk_p):
+    """k_pool_win (D = 128, sum / avg): groups of 8 unique rows whose chains
+    share one staged window -- long chains, several chains per group, chains
+    of one, a partial last group, rows longer than the shared path takes (513)
+    -- bit-exact against the oracle's reduceat order."""
+    rng = np.random.default_rng(L * 10 + int(brk_p * 10))
+    nrows = 8 * 5 + 3
+    rows = _chains(rng, L, nrows, 5000, brk_p)
+    vals = np.array([v for r in rows for v in r], np.int64)
+    offs = np.arange(nrows, dtype=np.int64) * L
+    w = (rng.standard_normal((5000, 128)) * 10.0 ** rng.integers(-3, 3, (5000, 1))).astype(np.float32)
+    t = _table(w)
+    for op in ("sum", "avg"):
+        [out] = R.pooled_lookup([R.JaggedTensor(vals, offs)], [t], op)
+        np.testing.assert_array_equal(out.cpu().numpy(), oracle.pooled_lookup(vals, offs, w, op))
+
+
+def test_shifted_window_out_of_range_id():
+    """An out-of-range ID inside a shared window (the last ID of a chained
+    row) raises the reference's ValueError for its position."""
+    rng = np.random.default_rng(5)
+    L = 16
+    rows = _chains(rng, L, 16, 100, 0.0)
+    vals = np.array([v for r in rows for v in r], np.int64)
+    bad = 5 * L + L - 1          # last ID of row 5 (window position L + 4 of its chain)
+    vals[bad] = 100
+    offs = np.arange(16, dtype=np.int64) * L
+    t = _table(np.ones((100, 128), np.float32))
+    with pytest.raises(ValueError) as e:
+        R.pooled_lookup([R.JaggedTensor(vals, offs)], [t], "sum")
+    assert "100" in str(e.value)
