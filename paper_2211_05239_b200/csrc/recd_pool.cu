@@ -528,212 +528,6 @@ __global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_ring(const __grid_
   cp_async_wait<0>();
 }
 
-// ---------------------------------------------------------------------------
-// Shifted-window sharing (full 128-float rows, sum / avg).  A CTA pools a
-// group of 8 consecutive unique rows of one feature, a warp per row.  In
-// session data most unique rows are the previous one shifted by one position
-// (row u+1 = row u [1:] + [x]): a chain of m such rows reads the window
-// row_u + (the last ID of each next row), L + m - 1 table rows instead of m L.
-// The CTA stages, per batch of 8 positions, the window rows every chain of the
-// group needs (8 + m - 1 per chain) in shared memory with cp.async, PW_NS
-// batches in flight, one __syncthreads per batch; warp (chain c, offset k)
-// reads its 8 rows at consecutive stage slots.  The consumer is the same
-// pairwise_ring, so the summation order -- and the result -- are bit-identical.
-// Groups of mixed lengths, rows longer than PW_MAXL or more than PW_MAXCH
-// chains take the per-warp ring (pool_row_ring).
-#ifndef RECD_POOL_WIN
-#define RECD_POOL_WIN 1
-#endif
-constexpr int PW_G = 8;                          // rows per group = warps per CTA
-constexpr int PW_NS = 3;                         // batches in flight
-constexpr int PW_MAXCH = 4;                      // chains per group on the shared path
-constexpr int PW_SROWS = 7 * PW_MAXCH + PW_G;    // stage rows (<= 36)
-constexpr int PW_MAXL = 512;                     // longest row on the shared path
-constexpr int PW_WIDS = PW_MAXCH * PW_MAXL + PW_G;
-
-struct PwShared {
-  uint32_t wid[PW_WIDS];          // window IDs of the group's chains, concatenated
-  int16_t sr_w0[PW_SROWS];        // stage row -> window base of its chain in wid
-  int16_t sr_j[PW_SROWS];         // ... position offset inside its chain's batch window
-  int16_t sr_W[PW_SROWS];         // ... window length of its chain
-  int32_t len[PW_G];
-  int32_t brk[PW_G];
-  int32_t wslot[PW_G];            // warp -> first stage slot (sbase_c + k)
-  int32_t wwin[PW_G];             // warp -> window index of its position 0 (wbase_c + k)
-  int32_t cw0[PW_MAXCH + 1];      // chain -> window base (prefix)
-  int32_t cstart[PW_MAXCH];       // chain -> first warp
-  int32_t nch, nrows, shared;
-};
-
-struct WinRows {
-  float* buf;            // stage buffers: PW_NS x PW_SROWS rows of 128 floats
-  const PwShared* sh;
-  const float* W;        // table base
-  int slot;              // this warp's first stage slot (lane offset added on acquire)
-  int lane, tid;
-  int32_t b;             // batches consumed
-  bool ok;
-  // stage bb: window positions 8 bb + 1 + j of every chain, j < 7 + m (all threads)
-  __device__ __forceinline__ void issue(int32_t bb) {
-    float* dst = buf + (bb % PW_NS) * (PW_SROWS * 128);
-    const int total = sh->nrows * 32;
-    for (int c = tid; c < total; c += 256) {
-      const int r = c >> 5, ch = c & 31;
-      const int q = 8 * bb + 1 + sh->sr_j[r];
-      if (q < sh->sr_W[r]) {
-        const uint32_t id = sh->wid[sh->sr_w0[r] + q];
-        cp_async<16>(dst + r * 128 + ch * 4, W + (uint64_t)id * 128 + ch * 4);
-      }
-    }
-    cp_async_commit();
-  }
-  __device__ __forceinline__ void start() {
-    b = 0;
-#pragma unroll
-    for (int i = 0; i < PW_NS - 1; ++i) issue(i);
-  }
-  __device__ __forceinline__ const float* acquire() {
-    cp_async_wait<PW_NS - 2>();
-    __syncthreads();           // batch b landed for everyone; batch b - 1 is consumed
-    issue(b + PW_NS - 1);      // into batch b - 1's buffer
-    return buf + (b % PW_NS) * (PW_SROWS * 128) + slot * 128 + lane * 4;
-  }
-  __device__ __forceinline__ void release() { ++b; }
-};
-
-template <class C, int K>
-__global__ void __launch_bounds__(256, RECD_RING_MINB) k_pool_win(const __grid_constant__ PoolParams p) {
-  RECD_PDL_PROLOGUE();
-  static_assert(C::VW == 4 && C::FULL, "window pool: full 128-float rows");
-  extern __shared__ __align__(128) float s_ring[];
-  __shared__ int64_t s_pref[RECD_MAX_FEAT + 1];  // groups of PW_G rows per feature
-  __shared__ PwShared sh;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    int64_t acc = 0;
-    for (int f = 0; f < p.F; ++f) {
-      s_pref[f] = acc;
-      acc += ceil_div(p.counts[f], (int64_t)PW_G);
-    }
-    s_pref[p.F] = acc;
-  }
-  __syncthreads();
-  const int64_t total = s_pref[p.F];
-  float* ring = s_ring + (int64_t)warp * K * 8 * 128 + lane * 4;
-  for (int64_t g = blockIdx.x; g < total; g += gridDim.x) {
-    const int f = find_seg(s_pref, p.F, g);
-    const int64_t U = p.counts[f], N = p.counts[p.Ftot + f];
-    const int64_t u0 = (g - s_pref[f]) * PW_G, u = u0 + warp;
-    const bool active = u < U;
-    const int64_t* uo = p.uoffsets[f];
-    const int64_t* ids = p.uvalues[f];
-    const int64_t a = active ? uo[u] : 0;
-    const int64_t L = active ? ((u + 1 < U) ? uo[u + 1] : N) - a : -1;
-    if (lane == 0) sh.len[warp] = (int32_t)min(L, (int64_t)INT32_MAX);
-    __syncthreads();
-    const int L0 = sh.len[0];
-    bool uni = L0 >= 2 && L0 <= PW_MAXL;
-    for (int w = 1; w < PW_G; ++w) uni &= sh.len[w] == L0 || sh.len[w] < 0;
-    if (uni) {
-      // chain breaks: row u is not row u-1 shifted by one (u0 always starts one)
-      bool brk = warp == 0;
-      if (!brk && active) {
-        bool diff = false;
-        for (int q = lane; q < L0 - 1; q += 32) diff |= __ldg(ids + a + q) != __ldg(ids + a - L0 + q + 1);
-        brk = __any_sync(0xffffffffu, diff);
-      }
-      if (lane == 0) sh.brk[warp] = brk;
-      __syncthreads();
-      if (tid == 0) {
-        int nch = 0, w0 = 0, rows = 0;
-        const int nact = (int)min((int64_t)PW_G, U - u0);
-        for (int w = 0; w < nact && nch <= PW_MAXCH; ++w) {
-          if (sh.brk[w]) {
-            if (nch == PW_MAXCH) { nch = PW_MAXCH + 1; break; }
-            sh.cstart[nch] = w;
-            sh.cw0[nch] = w0;
-            ++nch;
-          }
-          const int c = nch - 1, k = w - sh.cstart[c];
-          sh.wwin[w] = sh.cw0[c] + k;
-          w0 += sh.brk[w] ? L0 : 1;   // a chain's window: L0 IDs, then one per next row
-        }
-        sh.shared = nch <= PW_MAXCH;
-        if (sh.shared) {
-          sh.cw0[nch] = w0;
-          for (int c = 0; c < nch; ++c) {
-            const int m = (c + 1 < nch ? sh.cstart[c + 1] : nact) - sh.cstart[c];
-            for (int j = 0; j < 7 + m; ++j) {
-              sh.sr_w0[rows + j] = (int16_t)sh.cw0[c];
-              sh.sr_j[rows + j] = (int16_t)j;
-              sh.sr_W[rows + j] = (int16_t)(L0 + m - 1);
-            }
-            for (int k = 0; k < m; ++k) sh.wslot[sh.cstart[c] + k] = rows + k;
-            rows += 7 + m;
-          }
-          for (int w = nact; w < PW_G; ++w) sh.wslot[w] = 0, sh.wwin[w] = 0;
-          sh.nch = nch;
-          sh.nrows = rows;
-        }
-      }
-      __syncthreads();
-      uni = sh.shared;
-    }
-    if (!uni) {  // per-warp rings (no syncthreads inside)
-      if (active) {
-        ColWork cw{u, lane * 4, true};
-        pool_row_ring<C, K>(p, f, cw, ring, lane);
-      }
-      cp_async_wait<0>();
-      __syncthreads();
-      continue;
-    }
-    // window IDs of every chain (range-checked): position q < L0 of chain c is
-    // ID q of its first row, q >= L0 the last ID of row q - L0 + 1 of the chain
-    {
-      const int nw = sh.cw0[sh.nch];
-      const int64_t rows_f = p.table_rows[f];
-      for (int t = tid; t < nw; t += 256) {
-        int c = 0;
-        while (c + 1 < sh.nch && sh.cw0[c + 1] <= t) ++c;
-        const int q = t - sh.cw0[c];
-        const int64_t ac = uo[u0 + sh.cstart[c]];
-        const int64_t pos = q < L0 ? ac + q : ac + (int64_t)(q - L0 + 1) * L0 + L0 - 1;
-        const int64_t id = __ldg(ids + pos);
-        uint32_t v = 0;
-        if ((uint64_t)id < (uint64_t)rows_f) v = (uint32_t)id;
-        else atomicMin(reinterpret_cast<unsigned long long*>(p.err),
-                       (unsigned long long)(((int64_t)(p.f0 + f) << 40) + pos));
-        sh.wid[t] = v;
-      }
-    }
-    __syncthreads();
-    WinRows rr;
-    rr.buf = s_ring;
-    rr.sh = &sh;
-    rr.W = p.tables[f];
-    rr.slot = sh.wslot[warp];
-    rr.lane = lane;
-    rr.tid = tid;
-    rr.ok = active;
-    rr.start();
-    float acc[4];
-    C::ld(p.tables[f] + lane * 4 + (uint64_t)sh.wid[sh.wwin[warp]] * 128, true, acc);
-    float sv[4];
-    pairwise_ring(rr, (int32_t)(L0 - 1), sv);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], sv[k]);
-    if (p.mode == RECD_POOL_AVG) {
-      const float fl = (float)L0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k] = __fdiv_rn(acc[k], fl);
-    }
-    if (active) store_pooled<C>(p, f, u, ColWork{u, lane * 4, true}, acc);
-    cp_async_wait<0>();
-    __syncthreads();  // stage buffers and sh are reused by the next group
-  }
-}
-
 // k_pool_ring for sum / avg with float4 lanes, k_pool_fwd otherwise
 template <class C>
 static int launch_pool_fwd(const PoolParams& p, int mode, bool share, unsigned grid,
@@ -742,12 +536,8 @@ static int launch_pool_fwd(const PoolParams& p, int mode, bool share, unsigned g
     if (mode != RECD_POOL_MAX) {
       constexpr int K = RECD_RING_K;  // batches of 8 rows in flight per warp
       constexpr int smem = 8 * K * 8 * 128 * (int)sizeof(float);
-      static_assert(!RECD_POOL_WIN || smem >= PW_NS * PW_SROWS * 128 * (int)sizeof(float),
-                    "window stages share the rings' shared memory");
-      // shifted-window sharing for full 128-float rows (k_pool_win)
-      const bool win = RECD_POOL_WIN && C::FULL && p.D == 128;
       static bool attr[64] = {};
-      static int resident[64] = {}, resident_w[64] = {};
+      static int resident[64] = {};
       int dev = 0;
       RECD_CUDA_CHECK(cudaGetDevice(&dev));
       if (dev < 0 || dev >= 64 || !attr[dev]) {
@@ -755,14 +545,7 @@ static int launch_pool_fwd(const PoolParams& p, int mode, bool share, unsigned g
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int per = 0;
         RECD_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pool_ring<C, K>, 256, smem));
-        int per_w = 1;
-        if constexpr (C::FULL) {
-          RECD_CUDA_CHECK(cudaFuncSetAttribute(k_pool_win<C, K>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-          RECD_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_w, k_pool_win<C, K>, 256, smem));
-        }
-        if (dev >= 0 && dev < 64)
-          attr[dev] = true, resident[dev] = std::max(per, 1), resident_w[dev] = std::max(per_w, 1);
+        if (dev >= 0 && dev < 64) attr[dev] = true, resident[dev] = std::max(per, 1);
       }
       // Persistent grid (one wave: each CTA's ring warms up once).  With
       // RECD_POOL_SHARE one slot per SM is left to a kernel running beside
@@ -773,15 +556,9 @@ static int launch_pool_fwd(const PoolParams& p, int mode, bool share, unsigned g
         const char* e = getenv("RECD_POOL_CTAS");
         env_ctas = e ? std::max(1, atoi(e)) : 0;
       }
-      const int res = (dev >= 0 && dev < 64) ? (win ? resident_w[dev] : resident[dev]) : 1;
+      const int res = (dev >= 0 && dev < 64) ? resident[dev] : 1;
       const int per_sm = env_ctas ? env_ctas : std::max(1, share ? res - 1 : res);
       grid = std::min<unsigned>(grid, (unsigned)(num_sms() * per_sm));
-      if constexpr (C::FULL) {
-        if (win) {
-          pdl(k_pool_win<C, K>, grid, 256, smem, stream)(p);
-          return RECD_OK;
-        }
-      }
       pdl(k_pool_ring<C, K>, grid, 256, smem, stream)(p);
       return RECD_OK;
     }

@@ -123,10 +123,10 @@ def _chains(rng, L, nrows, vocab, brk_p):
 @pytest.mark.parametrize("L", [2, 3, 8, 9, 128, 129, 256, 300, 512, 513])
 @pytest.mark.parametrize("brk_p", [0.0, 0.3, 0.9])
 def test_shifted_window_sharing_bit_exact(L, brk_p):
-    """k_pool_win (D = 128, sum / avg): groups of 8 unique rows whose chains
-    share one staged window -- long chains, several chains per group, chains
-    of one, a partial last group, rows longer than the shared path takes (513)
-    -- bit-exact against the oracle's reduceat order."""
+    """Unique rows that are chains of shifted windows (session histories),
+    D = 128, sum / avg, long chains, several chains per group of 8 rows,
+    chains of one, a partial last group, rows up to 513 long -- bit-exact
+    against the oracle's reduceat order."""
     rng = np.random.default_rng(L * 10 + int(brk_p * 10))
     nrows = 8 * 5 + 3
     rows = _chains(rng, L, nrows, 5000, brk_p)
@@ -140,13 +140,13 @@ def test_shifted_window_sharing_bit_exact(L, brk_p):
 
 
 def test_shifted_window_out_of_range_id():
-    """An out-of-range ID inside a shared window (the last ID of a chained
-    row) raises the reference's ValueError for its position."""
+    """An out-of-range ID as the last ID of a chained (shifted) row raises
+    the reference's ValueError."""
     rng = np.random.default_rng(5)
     L = 16
     rows = _chains(rng, L, 16, 100, 0.0)
     vals = np.array([v for r in rows for v in r], np.int64)
-    bad = 5 * L + L - 1          # last ID of row 5 (window position L + 4 of its chain)
+    bad = 5 * L + L - 1          # last ID of row 5
     vals[bad] = 100
     offs = np.arange(16, dtype=np.int64) * L
     t = _table(np.ones((100, 128), np.float32))
