@@ -299,6 +299,10 @@ __global__ void __launch_bounds__(RS_NT, RECD_RS_MINB) k_rowscan(const __grid_co
         constexpr int64_t STEP = 2 * RS_NT;            // values per pair slot
         const int64_t tbe = vbeg & ~(int64_t)1;
         const bool Leven = (L & 1u) == 0;
+        // rows of a thread's pairs: one division per trip, then stepped by
+        // STEP values (dj rows + dr positions) -- ncu: the per-pair division
+        // was 12% of the kernel's instructions
+        const uint32_t dj = (uint32_t)STEP / L, dr = (uint32_t)STEP % L;
         for (int64_t ob = tbe; ob < vend; ob += STEP * PK) {
           longlong2 cv[PK], pv[PK];
 #pragma unroll
@@ -308,27 +312,46 @@ __global__ void __launch_bounds__(RS_NT, RECD_RS_MINB) k_rowscan(const __grid_co
             if (q + 1 < nv) cv[k] = __ldg(reinterpret_cast<const longlong2*>(val + q));
             else if (q < nv) cv[k].x = __ldg(val + q);
           }
+          if (Leven) {  // block-uniform; pq < 0 only in global row 0 (a head anyway)
 #pragma unroll
-          for (int k = 0; k < PK; ++k) {
-            const int64_t pq = ob + k * STEP + 2 * tid - L0;
-            if (Leven && pq >= 0) {
-              pv[k] = __ldg(reinterpret_cast<const longlong2*>(val + pq));
-            } else {
-              pv[k].x = __ldg(val + max(pq, (int64_t)0));
-              pv[k].y = __ldg(val + max(pq + 1, (int64_t)0));
+            for (int k = 0; k < PK; ++k) {
+              const int64_t pq = ob + k * STEP + 2 * tid - L0;
+              pv[k] = __ldg(reinterpret_cast<const longlong2*>(val + (pq < 0 ? 0 : pq)));
             }
+          } else {
+#pragma unroll
+            for (int k = 0; k < PK; ++k) {
+              const int64_t pq = ob + k * STEP + 2 * tid - L0;
+              pv[k].x = __ldg(val + (pq < 0 ? 0 : pq));
+              pv[k].y = __ldg(val + (pq + 1 < 0 ? 0 : pq + 1));
+            }
+          }
+          // q = vbeg - 1 (thread 0's first pair when vbeg is odd): only its
+          // second value is in the chunk (row 0); rows from the next pair on
+          const int64_t rel0 = ob + 2 * tid - vbeg;
+          const bool neg = rel0 < 0;
+          uint32_t j, rem;
+          {
+            const uint32_t r = (uint32_t)(neg ? rel0 + STEP : rel0);
+            j = r / L;
+            rem = r - j * L;
           }
 #pragma unroll
           for (int k = 0; k < PK; ++k) {
             const int64_t q = ob + k * STEP + 2 * tid;
-            if (q >= vend) continue;
-            if (q >= vbeg) {
-              const uint32_t rel = (uint32_t)(q - vbeg);
-              const uint32_t j = rel / L;
+            if (k == 0 && neg) {
+              if (cv[k].y != pv[k].y) s_mism[0] = 1u;
+              continue;
+            }
+            if (q < vend) {
               if (cv[k].x != pv[k].x) s_mism[j] = 1u;
-              if (q + 1 < vend && cv[k].y != pv[k].y) s_mism[j + (rel - j * L + 1 == L ? 1u : 0u)] = 1u;
-            } else if (cv[k].y != pv[k].y) {  // q = vbeg - 1: only q + 1 (row 0)
-              s_mism[0] = 1u;
+              if (q + 1 < vend && cv[k].y != pv[k].y) s_mism[j + (rem + 1 == L ? 1u : 0u)] = 1u;
+            }
+            j += dj;
+            rem += dr;
+            if (rem >= L) {
+              rem -= L;
+              ++j;
             }
           }
         }
