@@ -39,6 +39,9 @@ constexpr uint32_t OS_AGG = 1u << 30, OS_PRE = 2u << 30, OS_CNT = (1u << 30) - 1
 #define RECD_OS_LB 8
 #endif
 constexpr int OS_LB = RECD_OS_LB;
+#ifndef RECD_OS_EARLY  // publish a tile's digit counts before its ranking
+#define RECD_OS_EARLY 1
+#endif
 #ifndef RECD_OS_LOCAL  // one-CTA-per-segment sort when every segment fits a tile
 #define RECD_OS_LOCAL 1
 #endif              // look-back tiles per round trip
@@ -143,6 +146,36 @@ __global__ void __launch_bounds__(OS_NT) k_os_setup(const __grid_constant__ OsPa
   h[threadIdx.x] = (uint32_t)x;
 }
 
+// decoupled look-back, OS_LB predecessors per round trip: the loads of tiles
+// k, k-1, ..., k-OS_LB+1 are independent, so a walk over many in-flight tiles
+// costs one L2 latency per OS_LB tiles instead of per tile; the words are
+// consumed in order up to the first unpublished one (retried) or the first
+// inclusive prefix (done); tile 0 always publishes a prefix.  col = this
+// thread's digit column of the segment's status rows; returns the exclusive
+// count of tile lt_ (> 0).
+__device__ __forceinline__ uint32_t os_look_back(const uint32_t* col, int64_t lt_) {
+  uint32_t excl = 0;
+  for (int64_t k = lt_ - 1;;) {
+    uint32_t v[OS_LB];
+#pragma unroll
+    for (int j = 0; j < OS_LB; ++j) v[j] = (k - j >= 0) ? ld_relaxed(col + (k - j) * 256) : OS_PRE;
+    int j = 0;
+    bool done = false;
+#pragma unroll
+    for (int q = 0; q < OS_LB; ++q) {
+      if (done || j < q) continue;                  // stopped earlier in this batch
+      const uint32_t w = v[q];
+      if ((w & ~OS_CNT) == 0u) continue;            // not published yet: retry from here
+      excl += w & OS_CNT;
+      if (w & OS_PRE) done = true;
+      j = q + 1;
+    }
+    if (done) break;
+    k -= j;
+  }
+  return excl;
+}
+
 #ifndef RECD_OS_MINB
 #define RECD_OS_MINB 3
 #endif
@@ -191,6 +224,21 @@ __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_c
       key[r] = e < tn ? __ldg(kin + e) : 0u;
       val[r] = e < tn ? __ldg(vin + e) : 0u;
     }
+    uint32_t* my = st_cur + (sg.tcap0 + lt_) * 256 + tid;
+#if RECD_OS_EARLY
+    // publish the tile's digit counts before ranking it (shared-atomic
+    // histogram): the tiles behind it in the look-back stop waiting for this
+    // tile's ranking (ncu: 27% of a pass's stall samples sat in the look-back)
+    s_tdb[tid] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < OS_ITEMS; ++r) {
+      const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
+      if (e < tn) atomicAdd(&s_tdb[(key[r] >> p.shift) & mask], 1u);
+    }
+    __syncthreads();
+    st_relaxed(my, (lt_ == 0 ? OS_PRE : OS_AGG) | s_tdb[tid]);
+#endif
 #pragma unroll
     for (int r = 0; r < OS_ITEMS; ++r) {
       const int e = warp * (OS_TILE / OS_WARPS) + r * 32 + lane;
@@ -213,36 +261,12 @@ __global__ void __launch_bounds__(OS_NT, RECD_OS_MINB) k_onesweep(const __grid_c
       s_wcnt[w][tid] = cnt;
       cnt += c;
     }
-    uint32_t* my = st_cur + (sg.tcap0 + lt_) * 256 + tid;
     uint32_t excl = 0;
     if (lt_ == 0) {
-      st_relaxed(my, OS_PRE | cnt);
+      if (!RECD_OS_EARLY) st_relaxed(my, OS_PRE | cnt);
     } else {
-      st_relaxed(my, OS_AGG | cnt);
-      // decoupled look-back, OS_LB predecessors per round trip: the loads of
-      // tiles k, k-1, ..., k-OS_LB+1 are independent, so a walk over many
-      // in-flight tiles costs one L2 latency per OS_LB tiles instead of per tile;
-      // the words are consumed in order up to the first unpublished one (retried)
-      // or the first inclusive prefix (done); tile 0 always publishes a prefix
-      const uint32_t* col = st_cur + sg.tcap0 * 256 + tid;
-      for (int64_t k = lt_ - 1;;) {
-        uint32_t v[OS_LB];
-#pragma unroll
-        for (int j = 0; j < OS_LB; ++j) v[j] = (k - j >= 0) ? ld_relaxed(col + (k - j) * 256) : OS_PRE;
-        int j = 0;
-        bool done = false;
-#pragma unroll
-        for (int q = 0; q < OS_LB; ++q) {
-          if (done || j < q) continue;                  // stopped earlier in this batch
-          const uint32_t w = v[q];
-          if ((w & ~OS_CNT) == 0u) continue;            // not published yet: retry from here
-          excl += w & OS_CNT;
-          if (w & OS_PRE) done = true;
-          j = q + 1;
-        }
-        if (done) break;
-        k -= j;
-      }
+      if (!RECD_OS_EARLY) st_relaxed(my, OS_AGG | cnt);
+      excl = os_look_back(st_cur + sg.tcap0 * 256 + tid, lt_);
       st_relaxed(my, OS_PRE | (excl + cnt));
     }
     if (p.pass + 1 < p.npass) st_next[(sg.tcap0 + lt_) * 256 + tid] = 0u;

@@ -6,6 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
+    "noearly": ["RECD_OS_EARLY=0"],
     "notiny": ["RECD_TINY_CH=0"],
     "rs256": ["RECD_RS_SMALLB=0"],
     "gu16": ["RECD_GU_CH_SMALL=16"],

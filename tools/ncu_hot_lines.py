@@ -7,7 +7,7 @@ import sys
 rep, kern = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
-                      "--launch-count", "1", "--print-source", "cuda,sass"],
+                      "--launch-skip", str(int(sys.argv[4]) if len(sys.argv) > 4 else 0), "--launch-count", "1", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 fname, hdr, recs = "", None, []
 for r in csv.reader(out.splitlines()):
