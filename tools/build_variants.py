@@ -6,6 +6,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
+    "noil": ["RECD_OS_IL=0"],
+    "lb16": ["RECD_OS_LB=16"],
+    "lb4": ["RECD_OS_LB=4"],
     "noearly": ["RECD_OS_EARLY=0"],
     "notiny": ["RECD_TINY_CH=0"],
     "rs256": ["RECD_RS_SMALLB=0"],
