@@ -461,7 +461,9 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
     p.counters = reinterpret_cast<uint32_t*>(p.tile0 + OS_MAXSEG + 1);
     p.status = p.counters + 64;
     p.tmap = p.status + 2 * p.total_tcap * 256;
-    p.il = RECD_OS_IL && p.S > 1;
+    // (sorts of short segments -- the inverse CSR: 16 tiles each at cfg2 --
+    // gain nothing and would pay the map's setup on the critical path)
+    p.il = RECD_OS_IL && p.S > 1 && p.total_tcap >= 64 * (int64_t)p.S;
     p.kin = keys;
     if (hist_ready && S <= OS_MAXSEG) {
       // the producer of the keys already counted every pass's digits into
