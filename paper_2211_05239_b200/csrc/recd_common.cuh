@@ -79,7 +79,7 @@ struct PdlLaunch {
   template <typename... Args>
   void operator()(Args&&... args) const {
     if (!pdl_allowed()) {
-      k<<<grid, block, smem, stream>>>(static_cast<Args&&>(args)...);
+      k<<<grid, block, smem, stream>>>(args...);
       return;
     }
     cudaLaunchConfig_t cfg = {};
@@ -92,7 +92,12 @@ struct PdlLaunch {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k, static_cast<Args&&>(args)...);
+    if (cudaLaunchKernelEx(&cfg, k, args...) != cudaSuccess) {
+      // attribute refused: launch plainly (a real launch error then shows in
+      // the caller's RECD_LAUNCH_CHECK)
+      (void)cudaGetLastError();
+      k<<<grid, block, smem, stream>>>(args...);
+    }
   }
 };
 template <typename... KArgs>
