@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <cstring>
 #include <thread>
+#include <unistd.h>
 #include <vector>
 
 #include "../../../include/recd_host.h"
@@ -144,9 +145,20 @@ class Pool {
   bool stop_ = false;
 };
 
+// one pool per process, never destroyed: a forked child (the bench's CPU
+// baseline forks after the encoder ran) gets a fresh pool instead of the
+// parent's, whose worker threads do not exist in the child; at exit the
+// sleeping workers simply end with the process
 Pool& pool() {
-  static Pool p;
-  return p;
+  static std::mutex m;
+  static Pool* p = nullptr;
+  static pid_t owner = 0;
+  std::lock_guard<std::mutex> lk(m);
+  if (!p || owner != getpid()) {
+    p = new Pool;
+    owner = getpid();
+  }
+  return *p;
 }
 
 template <class Fn>
