@@ -61,3 +61,45 @@ def test_sort_pairs_stable(bits, nseg, maxn, dist):
         order = np.argsort(seg_k & mask, kind="stable")
         np.testing.assert_array_equal(rv[a:a + n], vals[a:a + n][order])
         np.testing.assert_array_equal(rk[a:a + n], seg_k[order])
+
+
+def _sort_and_check(keys, caps, counts, bits):
+    dev = torch.device("cuda")
+    nseg = len(caps)
+    caps = np.asarray(caps, np.int64)
+    bases = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.int64)
+    vals = np.arange(keys.size, dtype=np.uint32)
+    k = torch.as_tensor(keys.view(np.int32), device=dev)
+    v = torch.as_tensor(vals.view(np.int32), device=dev)
+    ka, va = torch.empty_like(k), torch.empty_like(v)
+    cnt = [torch.tensor([c], dtype=torch.int64, device=dev) for c in counts]
+    lib = _lib.load()
+    nb = lib.recd_sort_pairs_scratch_bytes(nseg, _lib.i64s(bases.tolist()), _lib.i64s(caps.tolist()))
+    scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
+    alt = C.c_int32(-1)
+    rc = lib.recd_sort_pairs(nseg, _lib.i64s(bases.tolist()), _lib.i64s(caps.tolist()), _lib.ptrs(cnt),
+                             bits, k.data_ptr(), v.data_ptr(), ka.data_ptr(), va.data_ptr(),
+                             C.byref(alt), scratch.data_ptr(), nb, _lib.stream_ptr(dev))
+    assert rc == 0
+    torch.cuda.synchronize()
+    rk, rv = (ka, va) if alt.value else (k, v)
+    rk = rk.cpu().numpy().view(np.uint32)
+    rv = rv.cpu().numpy().view(np.uint32)
+    for s in range(nseg):
+        a, n = int(bases[s]), counts[s]
+        order = np.argsort(keys[a:a + n] & np.uint32((1 << bits) - 1), kind="stable")
+        np.testing.assert_array_equal(rv[a:a + n], vals[a:a + n][order])
+
+
+def test_sort_interleaved_tickets_skewed_segments():
+    """Tickets interleaved over the segments in proportion to their tile
+    counts (>= 64 tiles per segment on average): segments of very different
+    sizes, empty ones, a one-element one, partial last tiles, clustered
+    (history-like) and random keys -- every segment stable-sorted."""
+    rng = np.random.default_rng(11)
+    caps = [2_000_000, 1, 0, 4097, 700_000, 1_500_000, 3, 260_000]
+    counts = [2_000_000, 1, 0, 4097, 699_999, 1_234_567, 0, 260_000]
+    caps = [max(c, 1) for c in caps]
+    keys = rng.integers(0, 10_000_000, size=sum(caps), dtype=np.uint64).astype(np.uint32)
+    keys[: 2_000_000] = np.repeat(rng.integers(0, 10_000_000, 2_000_000 // 8), 8)  # clustered equal keys
+    _sort_and_check(keys, caps, counts, 24)
