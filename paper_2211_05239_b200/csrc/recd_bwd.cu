@@ -241,7 +241,11 @@ __global__ void __launch_bounds__(256, 4) k_grad_u(const __grid_constant__ BwdPa
 // end), gathering grad_out rows 8 positions at a time across run boundaries, so
 // no per-row dependent chain (CSR start -> row ids -> gradient rows) stalls it.
 // Same order as k_grad_u (ascending batch row within each unique row).
-constexpr int GU_CH = 256;     // positions per warp task (32 for small batches: more tasks)
+#ifndef RECD_GU_CH
+#define RECD_GU_CH 512
+#endif
+constexpr int GU_CH = RECD_GU_CH;  // positions per warp task (32 for small batches: more tasks;
+                                   // 512 vs 256: grads 0.238 vs 0.243 ms, 64 / 128: 0.263 / 0.255)
 #ifndef RECD_GU_CH_SMALL
 #define RECD_GU_CH_SMALL 32
 #endif
