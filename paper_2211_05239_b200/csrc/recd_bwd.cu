@@ -43,7 +43,10 @@
 
 namespace recd {
 
-constexpr int RC_BIG = 256;   // sorted positions per scatter work item
+#ifndef RECD_RC_BIG
+#define RECD_RC_BIG 256
+#endif
+constexpr int RC_BIG = RECD_RC_BIG;  // sorted positions per scatter work item
 #ifndef RECD_RC_SMALL
 #define RECD_RC_SMALL 32
 #endif
