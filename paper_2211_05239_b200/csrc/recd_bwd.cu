@@ -378,8 +378,7 @@ __global__ void __launch_bounds__(256) k_occ(const __grid_constant__ BwdParams p
                                              uint32_t* vals) {
   RECD_PDL_PROLOGUE();
   if (p.occ_gate && !*(volatile const int32_t*)p.occ_gate) return;  // runs fallback only
-  int f = 0;
-  while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
+  const int f = block_feature(p.occ_blk0, p.F, (int64_t)blockIdx.x);
   const int64_t j0 = ((int64_t)blockIdx.x - p.occ_blk0[f]) * p.oc_ch;
   const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];
   if (j0 >= NV) return;
@@ -533,8 +532,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_rv(const __grid_constant__ BwdParams p, uint32_t* keys,
                                             uint32_t* vals) {
   RECD_PDL_PROLOGUE();
-  int f = 0;
-  while (f + 1 < p.F && p.occ_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
+  const int f = block_feature(p.occ_blk0, p.F, (int64_t)blockIdx.x);
   const int64_t blk = blockIdx.x;
   const int64_t j0 = (blk - p.occ_blk0[f]) * p.oc_ch;
   const int64_t U = p.counts[f], NV = p.counts[p.Ftot + f];

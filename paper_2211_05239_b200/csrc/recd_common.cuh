@@ -289,6 +289,17 @@ __device__ __forceinline__ int64_t block_inclusive_max(int64_t v, int64_t* smem,
   return r;
 }
 
+// last f in [0, F) with first[f] <= b for non-decreasing block offsets
+// first[0..F) (kernel parameter arrays: block -> feature)
+__device__ __forceinline__ int block_feature(const int64_t* first, int F, int64_t b) {
+  int lo = 0, hi = F - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (first[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 // Last index k in [0, n) with a[k] <= x for a non-decreasing a with a[0] <= x,
 // found by the whole warp with 32-ary probing (every lane returns it).
 __device__ __forceinline__ int64_t warp_last_le(const int64_t* a, int64_t n, int64_t x, int lane) {

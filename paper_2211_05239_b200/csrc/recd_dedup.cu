@@ -829,14 +829,17 @@ constexpr int CP_NT = 256;
 #define RECD_TINY_CH 1
 #endif
 constexpr int CP_IT = RECD_CP_IT;
+#ifndef RECD_CP_ILP  // gathers in flight per thread in the uniform-row copy
+#define RECD_CP_ILP 4
+#endif
+constexpr int CP_ILP = RECD_CP_ILP;
 constexpr int CP_CH = CP_NT * CP_IT;  // unique values per block
 constexpr int CP_MAXR = 512;          // rows staged per pass
 
 
 __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupParams p) {
   RECD_PDL_PROLOGUE();
-  int f = 0;
-  while (f + 1 < p.F && p.cp_blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
+  const int f = block_feature(p.cp_blk0, p.F, (int64_t)blockIdx.x);
   const int64_t j0 = ((int64_t)blockIdx.x - p.cp_blk0[f]) * p.cp_ch;
   const int64_t U = p.count_rows[f], NV = p.count_vals[f];
   if (j0 >= NV) return;
@@ -882,10 +885,10 @@ __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupPar
         r = rel / L;
         rem = rel - r * L;
       }
-      for (int64_t qq = q_first; qq < qb; qq += 4 * CP_NT) {
-        int64_t a[4], v[4];
+      for (int64_t qq = q_first; qq < qb; qq += CP_ILP * CP_NT) {
+        int64_t a[CP_ILP], v[CP_ILP];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < CP_ILP; ++k) {
           a[k] = s_so[min(r, (uint32_t)(nr - 1))] + rem;
           r += dj;
           rem += dr;
@@ -895,10 +898,10 @@ __global__ void __launch_bounds__(CP_NT) k_copy(const __grid_constant__ DedupPar
           }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < CP_ILP; ++k)
           if (qq + k * CP_NT < qb) v[k] = __ldg(src + a[k]);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < CP_ILP; ++k) {
           const int64_t q = qq + k * CP_NT;
           if (q < qb) {
             dst[q] = v[k];

@@ -53,8 +53,7 @@ __global__ void k_rc_count(const __grid_constant__ RcParams p) {
 }
 
 __global__ void __launch_bounds__(RC_NT) k_rc_copy(const __grid_constant__ RcParams p) {
-  int f = 0;
-  while (f + 1 < p.F && p.blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
+  const int f = block_feature(p.blk0, p.F, (int64_t)blockIdx.x);
   const int64_t NV = p.nv[f];
   const int64_t j0 = ((int64_t)blockIdx.x - p.blk0[f]) * RC_CH;
   if (j0 >= NV) return;

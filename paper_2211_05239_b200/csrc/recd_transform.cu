@@ -32,8 +32,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
 constexpr int XF_NT = 256, XF_IT = 8;
 
 __global__ void __launch_bounds__(XF_NT) k_transform(const __grid_constant__ XformParams p) {
-  int f = 0;
-  while (f + 1 < p.F && p.blk0[f + 1] <= (int64_t)blockIdx.x) ++f;
+  const int f = block_feature(p.blk0, p.F, (int64_t)blockIdx.x);
   const int64_t n = p.count[f] ? min(*p.count[f], p.n[f]) : p.n[f];
   const int64_t base = ((int64_t)blockIdx.x - p.blk0[f]) * (XF_NT * XF_IT);
   const int op = p.op[f];
