@@ -133,7 +133,9 @@ int recd_pool_fwd(int32_t num_features, int64_t batch_size, int32_t dim, int32_t
  * stored straight to out[f][i] for its batch rows i, so the [U x dim] pooled
  * buffer is neither written nor re-read (pooled_out: NULL, or per feature NULL
  * or a buffer that also receives the pooled rows).  Needs the backward's
- * RECD_BWD_INVERSE stage to have run on the same IKJT first. */
+ * RECD_BWD_INVERSE stage to have run on the same IKJT first.  A feature whose
+ * csr_start and csr_rows are both NULL is an identity (plain KJT) feature --
+ * recd_pool_bwd_csr reports it so -- pooled straight into out[f]. */
 int recd_pool_fwd_csr(int32_t num_features, int64_t batch_size, int32_t dim, int32_t mode,
                       const float* const* tables, const int64_t* table_rows,
                       const int64_t* const* uvalues, const int64_t* const* uoffsets,

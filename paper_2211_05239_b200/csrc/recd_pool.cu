@@ -617,11 +617,15 @@ static int pool_fwd_impl(int32_t num_features, int64_t batch_size, int32_t dim, 
       p.pooled[f] = pooled_out ? pooled_out[f0 + f] : nullptr;
       p.out[f] = out ? out[f0 + f] : nullptr;
       if (csr) {
+        // a feature with neither CSR array is an identity (plain KJT) feature:
+        // its unique rows are the batch rows, pooled straight into out
+        const bool ident = !csr_start[f0 + f] && !csr_rows[f0 + f];
         p.csr_start[f] = csr_start[f0 + f];
         p.csr_rows[f] = csr_rows[f0 + f];
-        if (!p.csr_start[f] || !p.csr_rows[f] || !p.out[f] || (dim % 4 == 0 && (uintptr_t)p.out[f] % 16))
+        if ((!ident && (!p.csr_start[f] || !p.csr_rows[f])) || !p.out[f] ||
+            (dim % 4 == 0 && (uintptr_t)p.out[f] % 16))
           return RECD_ERR_ARG;
-        if (!p.pooled[f]) p.pooled[f] = p.out[f];  // (alignment check below; not written)
+        if (!p.pooled[f]) p.pooled[f] = p.out[f];  // (alignment check below; written only if ident)
       }
       if (!p.tables[f] || !p.uoffsets[f] || !p.pooled[f]) return RECD_ERR_ARG;
       if (dim % 2 == 0 && ((uintptr_t)p.tables[f] % 8 || (uintptr_t)p.pooled[f] % 8 ||
@@ -633,7 +637,7 @@ static int pool_fwd_impl(int32_t num_features, int64_t batch_size, int32_t dim, 
     if (csr) {
       any_expand = false;
       for (int f = 0; f < p.F; ++f)
-        if (!pooled_out || !pooled_out[f0 + f]) p.pooled[f] = nullptr;
+        if ((!pooled_out || !pooled_out[f0 + f]) && p.csr_start[f]) p.pooled[f] = nullptr;
     }
     int rc = RECD_DISPATCH_COL_VW(dim, RECD_POOL_VW, 1, {
       const unsigned grid = grid_for(batch_size * p.F * col_blocks<C>(dim));

@@ -26,6 +26,10 @@ slot = step parity) and each parity is one captured CUDA graph.
 
 This is the device-side equivalent of one `forward_iteration`'s sparse part
 (trainer_sim.py:484-574) plus the backward the reference does not have.
+Like the reference's iteration, a step may mix deduplicated groups with
+plain KJT keys (`plain=`, trainer_sim.py:562-574): the plain keys skip the
+dedup, are pooled per batch row and take the backward's identity path, in
+the same calls (and graph) as the deduplicated features.
 """
 
 from __future__ import annotations
@@ -57,14 +61,20 @@ class _Stage:
     def __init__(self, step: "TrainStep"):
         dev, B, F, i64 = step.dev, step.B, step.F, torch.int64
         lib = step.lib
+        Fd = step.Fd
         self.inverse = [torch.empty(B, dtype=i64, device=dev) for _ in step.groups]
-        self.uoffsets = [torch.empty(B, dtype=i64, device=dev) for _ in step.keys]
-        self.uvalues = [torch.empty(c, dtype=i64, device=dev) for c in step.caps]
+        self.uoffsets = [torch.empty(B, dtype=i64, device=dev) for _ in step.keys[:Fd]]
+        self.uvalues = [torch.empty(c, dtype=i64, device=dev) for c in step.caps[:Fd]]
+        # counts of the step's features [U per feature, N_u per feature]; with
+        # plain keys the dedup writes its own [2 Fd] (dc_sub) and the plain
+        # keys' entries are B and the slot's value counts
         self.dcounts = torch.zeros(2 * F, dtype=i64, device=dev)
+        self.dcounts[Fd:F] = B
+        self.dc_sub = torch.zeros(2 * Fd, dtype=i64, device=dev) if Fd < F else self.dcounts
         self.err = torch.full((2,), _lib.RECD_NO_ERROR, dtype=i64, device=dev)
         self.dedup_scratch = torch.empty(
-            max(lib.recd_dedup_scratch_bytes(len(step.groups), F, B), 256), dtype=torch.uint8,
-            device=dev)
+            max(lib.recd_dedup_scratch_bytes(max(len(step.groups), 1), max(Fd, 1), B), 256),
+            dtype=torch.uint8, device=dev)
         self.bwd_scratch = torch.empty(
             max(lib.recd_pool_bwd_scratch_bytes(F, B, step.D, _lib.i64s(step.caps)), 256),
             dtype=torch.uint8, device=dev)
@@ -86,13 +96,19 @@ class _Args:
         self.caps = L.i64s(step.caps)
         self.grad, self.out = L.ptrs(step.grad_out), L.ptrs(step.out)
         if step.mode == "dedup":
+            Fd = step.Fd
             inv_f = []
             for gi, g in enumerate(step.groups):
                 inv_f += [st.inverse[gi]] * len(g)
-            self.inverse_f = L.ptrs(inv_f)
-            self.pooled = L.ptrs(step.pooled)
-            self.feat_vals, self.feat_offs, self.feat_vals_t = self.uvalues, self.uoffsets, st.uvalues
+            # plain keys (after the deduplicated ones): identity inverse, the
+            # KJT rows themselves, pooled straight into the batch rows
+            self.inverse_f = L.ptrs(inv_f + [None] * (step.F - Fd))
+            self.pooled = L.ptrs(step.pooled[:Fd] + step.out[Fd:])
+            self.feat_vals_t = list(st.uvalues) + list(vals[Fd:])
+            self.feat_vals = L.ptrs(self.feat_vals_t)
+            self.feat_offs = L.ptrs(list(st.uoffsets) + list(offs[Fd:]))
             self.counts_ptr = st.dcounts.data_ptr()
+            self.dc_out = st.dc_sub.data_ptr()
         else:
             self.inverse_f = L.ptrs([None] * step.F)
             self.pooled = self.out  # no expansion: pooled rows are the batch rows
@@ -111,15 +127,22 @@ class TrainStep:
     def __init__(self, groups: Sequence[Sequence[str]], batch_size: int,
                  value_caps: dict[str, int], tables: dict[str, EmbeddingTable], op: str = "sum",
                  lr: float = 0.01, mode: str = "dedup", device=None, overlap: bool = True,
-                 slots: int = 1, pipeline: bool = False):
+                 slots: int = 1, pipeline: bool = False, plain: Sequence[str] = ()):
         if mode not in ("dedup", "kjt"):
             raise ValueError(f"unknown mode {mode!r}")
+        plain = tuple(plain)
+        if set(plain) & {k for g in groups for k in g}:
+            raise ValueError("a key is both in a dedup group and plain")
+        if plain and mode != "dedup":
+            raise ValueError("plain keys are for dedup mode (kjt mode has no dedup at all)")
         if op not in ("sum", "avg", "mean"):
             raise ValueError(f"the training step needs sum/avg pooling (max has no backward), got {op!r}")
         self.lib = _lib.load()
         self.groups = [tuple(g) for g in groups]
-        self.keys = [k for g in self.groups for k in g]
+        self.plain = plain
+        self.keys = [k for g in self.groups for k in g] + list(plain)
         self.F = len(self.keys)
+        self.Fd = self.F - len(plain)  # deduplicated features come first
         self.B = int(batch_size)
         self.mode = mode
         self.op = op
@@ -254,11 +277,21 @@ class TrainStep:
         if self.mode != "dedup":
             return
         a, st = self.args(stage, slot), self._st(stage)
-        rc = self.lib.recd_dedup_ex(len(self.groups), a.gsizes, self.B, a.in_values, a.in_offsets,
-                                    a.caps, a.in_counts_ptr, 3, a.inverse_g, a.uoffsets,
-                                    a.uvalues, st.dcounts.data_ptr(), None, None,
-                                    st.dedup_scratch.data_ptr(), st.dedup_scratch.numel(), stream)
-        _lib.check(rc, "recd_dedup_ex")
+        Fd, F = self.Fd, self.F
+        if Fd:
+            rc = self.lib.recd_dedup_ex(len(self.groups), a.gsizes, self.B, a.in_values, a.in_offsets,
+                                        a.caps, a.in_counts_ptr, 3, a.inverse_g, a.uoffsets,
+                                        a.uvalues, a.dc_out, None, None,
+                                        st.dedup_scratch.data_ptr(), st.dedup_scratch.numel(), stream)
+            _lib.check(rc, "recd_dedup_ex")
+        if Fd < F:  # assemble [U, N_u] of all features (plain keys: B, their value counts)
+            s = torch.cuda.ExternalStream(stream, device=self.dev)
+            with torch.cuda.stream(s):
+                if Fd:
+                    st.dcounts[:Fd].copy_(st.dc_sub[:Fd], non_blocking=True)
+                    st.dcounts[F:F + Fd].copy_(st.dc_sub[Fd:], non_blocking=True)
+                st.dcounts[F + Fd:].copy_(self.in_counts[self.slot if slot is None else slot, F + Fd:],
+                                          non_blocking=True)
 
     def forward(self, stream: int, stage=None, slot=None, share: bool = False) -> None:
         """Pooled lookup over the unique rows (k_pool_fwd only).  share: the
@@ -293,11 +326,12 @@ class TrainStep:
         _lib.check(rc, "recd_pool_fwd_csr")
 
     def expand(self, stream: int, stage=None, slot=None) -> None:
-        """out[i] = pooled[inverse[i]] (k_expand; nothing to do in kjt mode)."""
-        if self.mode != "dedup":
+        """out[i] = pooled[inverse[i]] (k_expand; nothing to do in kjt mode or
+        for plain keys, whose lookup wrote the batch rows)."""
+        if self.mode != "dedup" or self.Fd == 0:
             return
         a = self.args(stage, slot)
-        rc = self.lib.recd_expand(self.F, self.B, self.D, a.inverse_f, a.pooled, a.out, stream)
+        rc = self.lib.recd_expand(self.Fd, self.B, self.D, a.inverse_f, a.pooled, a.out, stream)
         _lib.check(rc, "recd_expand")
 
     def _bwd_args(self, stream: int, stage=None, slot=None):

@@ -195,3 +195,52 @@ def test_pool_fwd_csr_writes_batch_rows_and_pooled():
         np.testing.assert_array_equal(pooled[f][: uo.size].cpu().numpy(), ref)
         np.testing.assert_array_equal(out[f].cpu().numpy(), oracle.expand(ref, inv))
     assert C.c_void_p(cs[0]).value is not None
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("graph", [True, False])
+def test_mixed_dedup_and_plain_keys(graph, fused, monkeypatch):
+    """One step over deduplicated groups and plain KJT keys together
+    (trainer_sim.py:562-574): the dedup'd keys match the oracle's IKJT path,
+    the plain key the oracle with an identity inverse (one unique row per
+    batch row, gradients reduced per batch row), tables and outputs
+    bit-exact, eager and as one CUDA graph."""
+    monkeypatch.setenv("RECD_FUSED_EXPAND", fused)
+    b, vocab, dim, lr = 2048, 5000, 128, 0.05
+    batch = _batch(b, [8, 24, 16], vocab, seed=5)
+    keys = list(batch.keys)
+    plain = [keys[2]]
+    rng = np.random.default_rng(1)
+    w0s = {k: rng.uniform(-0.1, 0.1, size=(vocab, dim)).astype(np.float32) for k in keys}
+    tables = {k: R.EmbeddingTable(k, vocab, dim, torch.as_tensor(w0s[k], device="cuda").clone())
+              for k in keys}
+    caps = {k: int(batch.values[k].size) for k in keys}
+    step = TrainStep([[keys[0]], [keys[1]]], b, caps, tables, "sum", lr, "dedup", plain=plain)
+    assert step.keys == keys
+    step.load_batch(batch.values, batch.offsets)
+    grads = {k: rng.standard_normal((b, dim)).astype(np.float32) for k in keys}
+    for f, k in enumerate(step.keys):
+        step.grad_out[f].copy_(torch.as_tensor(grads[k]))
+    if graph:
+        step.capture()
+        for k in keys:
+            tables[k].weights.copy_(torch.as_tensor(w0s[k]))
+        step.replay()
+    else:
+        step.run()
+    torch.cuda.synchronize()
+    outs, w1s = _oracle_step(batch, w0s, grads, lr)
+    for k in plain:  # identity inverse: no dedup
+        v, o = batch.values[k], batch.offsets[k]
+        outs[k] = oracle.pooled_lookup(v, o, w0s[k], "sum")
+        ids, g = oracle.sparse_table_grad(grads[k], v, o, "sum")
+        w1 = w0s[k].copy()
+        w1[ids] = w0s[k][ids] - (np.float32(lr) * g).astype(np.float32)
+        w1s[k] = w1
+    for f, k in enumerate(step.keys):
+        np.testing.assert_array_equal(step.out[f].cpu().numpy(), outs[k])
+        np.testing.assert_array_equal(tables[k].weights.cpu().numpy(), w1s[k])
+    c = step.host_counts()
+    assert c.U[2] == b and c.N_u[2] == batch.values[keys[2]].size
+    with pytest.raises(ValueError):
+        TrainStep([[keys[0]]], b, caps, tables, "sum", lr, "dedup", plain=[keys[0]])
