@@ -284,6 +284,13 @@ int recd_pool_bwd_csr(int32_t num_features, int64_t batch_size, int32_t dim, int
 #define RECD_BWD_OCCURRENCES 2
 #define RECD_BWD_GRAD 4
 #define RECD_BWD_SCATTER 8
+/* The step's backward bookkeeping (bad-ID flag, per-table segment counts)
+ * runs with RECD_BWD_INVERSE; RECD_BWD_SETUP runs it alone, and
+ * RECD_BWD_SETUP_DONE makes RECD_BWD_INVERSE skip it -- so after a SETUP call
+ * the INVERSE and OCCURRENCES stages may run concurrently on two streams
+ * (they use separate scratch). */
+#define RECD_BWD_SETUP 16
+#define RECD_BWD_SETUP_DONE 32
 int recd_pool_bwd_stages(int32_t stages, int32_t num_features, int64_t batch_size, int32_t dim,
                          int32_t mode, float* const* tables, const int64_t* table_rows,
                          const int64_t* const* uvalues, const int64_t* const* uoffsets,

@@ -22,6 +22,7 @@ RECD_NO_ERROR = 0x7F7F7F7F7F7F7F7F
 POOL_MODES = {"sum": 0, "avg": 1, "mean": 1, "max": 2}
 POOL_SHARE = 0x100  # recd_pool_fwd mode flag (include/recd.h)
 BWD_INVERSE, BWD_OCCURRENCES, BWD_GRAD, BWD_SCATTER = 1, 2, 4, 8  # recd_pool_bwd_stages
+BWD_SETUP, BWD_SETUP_DONE = 16, 32  # bookkeeping alone / INVERSE without it
 _ERRORS = {1: "invalid argument", 2: "CUDA error", 3: "scratch buffer too small",
            4: "unsupported configuration"}
 

@@ -1184,7 +1184,7 @@ struct BwdScratch {
   int64_t *head_count, *head_off, *runs_scan_part;
   int32_t* fallback;
   uint32_t* sc_ticket;
-  uint32_t *inv_k0, *inv_v0, *inv_k1, *inv_v1, *hist;
+  uint32_t *inv_k0, *inv_v0, *inv_k1, *inv_v1, *hist, *hist_inv;
   int32_t* csr_start;
   float* grad_u;
   uint32_t *occ_k0, *occ_v0, *occ_k1, *occ_v1;
@@ -1244,17 +1244,20 @@ size_t carve_bwd(void* base, size_t cap, const Plan& pl, int64_t B, int D, BwdSc
   s->occ_v1 = a.take<uint32_t>(occ);
   // sort histograms: max of the inverse sort and the table sort
   std::vector<SegDesc> segs;
-  int64_t hw = 0;
+  // the inverse-CSR sort and the occurrence sort get separate sort state, so
+  // the two stages may run concurrently (RECD_BWD_SETUP, TrainStep)
+  int64_t hw_inv = 0, hw = 0;
   if (need & NEED_INV) {
     for (int i = 0; i < pl.nis; ++i) segs.push_back({(int64_t)i * B, B, nullptr});
-    if (!segs.empty()) hw = sort_hist_words(segs.data(), (int)segs.size());
+    if (!segs.empty()) hw_inv = sort_hist_words(segs.data(), (int)segs.size());
   }
   segs.clear();
   if (need & NEED_OCC) {
     for (int t = 0; t < pl.nts; ++t) segs.push_back({pl.ts_base[t], pl.ts_cap[t], nullptr});
-    hw = std::max(hw, sort_hist_words(segs.data(), (int)segs.size()));
+    hw = sort_hist_words(segs.data(), (int)segs.size());
   }
   s->hist = a.take<uint32_t>(std::max<int64_t>(hw, 256));
+  s->hist_inv = a.take<uint32_t>(std::max<int64_t>(hw_inv, 256));
   // run-count scan partials (one scan segment per table)
   std::vector<ScanDesc> sd;
   for (int t = 0; t < pl.nts; ++t) {
@@ -1284,7 +1287,8 @@ static bool use_runs() {
 // stages (include/recd.h RECD_BWD_*): inverse CSR, occurrence sort, unique-row
 // gradients, scatter; prepare = the first two, finish = the last two
 enum { PH_INV = 1, PH_OCC = 2, PH_GRAD = 4, PH_SCAT = 8,
-       PH_PREP = PH_INV | PH_OCC, PH_FINISH = PH_GRAD | PH_SCAT, PH_ALL = PH_PREP | PH_FINISH };
+       PH_PREP = PH_INV | PH_OCC, PH_FINISH = PH_GRAD | PH_SCAT, PH_ALL = PH_PREP | PH_FINISH,
+       PH_SETUP = RECD_BWD_SETUP, PH_SETUP_DONE = RECD_BWD_SETUP_DONE };
 
 int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* tables,
             const int64_t* table_rows, const int64_t* const* uvalues,
@@ -1433,7 +1437,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
   p.exp_vals = p.occ_vals;
 
   // ---- prepare: everything that depends on the IKJT only (no gradient)
-  if (phase & PH_INV) {
+  if ((phase & PH_SETUP) || ((phase & PH_INV) && !(phase & PH_SETUP_DONE))) {
     pdl(k_bwd_setup, 1, 32, 0, stream)(p);
     note_launch();
   }
@@ -1451,7 +1455,7 @@ int run_bwd(BwdMode bm, int F, int64_t B, int dim, int mode, float* const* table
       for (int s = 0; s < pl.nis; ++s) segs.push_back({(int64_t)s * B, B, sc.is_count + s});
       bool alt = false;
       int rc = seg_sort_pairs(segs.data(), pl.nis, (int)bits_for(B), sc.inv_k0, sc.inv_v0,
-                              sc.inv_k1, sc.inv_v1, sc.hist, &alt, stream);
+                              sc.inv_k1, sc.inv_v1, sc.hist_inv, &alt, stream);
       if (rc != RECD_OK) return rc;
       pdl(k_csr_bounds, (unsigned)ceil_div(n, 256), 256, 0, stream)(p);
       note_launch();
@@ -1756,7 +1760,7 @@ extern "C" int recd_pool_bwd_stages(int32_t stages, int32_t num_features, int64_
                                     int64_t* grad_counts_out, void* scratch, size_t scratch_bytes,
                                     recd_stream_t stream) {
   recd::PdlScope pdl_scope(batch_size * (int64_t)num_features);
-  if (stages <= 0 || (stages & ~PH_ALL)) return RECD_ERR_ARG;
+  if (stages <= 0 || (stages & ~(PH_ALL | PH_SETUP | PH_SETUP_DONE))) return RECD_ERR_ARG;
   return run_bwd(BwdMode::Full, num_features, batch_size, dim, mode, tables, table_rows, uvalues,
                  uoffsets, value_caps, counts, inverse, grad_out, nullptr, nullptr, lr, apply_sgd,
                  grad_ids_out, grad_rows_out, grad_counts_out, scratch, scratch_bytes,

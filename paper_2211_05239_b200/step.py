@@ -188,6 +188,14 @@ class TrainStep:
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
         self._ev_inv = torch.cuda.Event()
+        # small batches: the occurrence sort on a stream of its own, beside the
+        # inverse CSR (RECD_BWD_SETUP first) -- both are latency-bound chains
+        # there (cfg1 0.111 vs 0.117 ms); on big ones starting the sort early
+        # only competes with the CSR and the lookup (cfg2 4.40 vs 4.24-4.28 ms).
+        # RECD_SPLIT_PREP=0/1 forces it off / on.
+        sp = os.environ.get("RECD_SPLIT_PREP")
+        self.split_prep = (sp != "0") if sp else not self.fused_expand
+        self._side2 = torch.cuda.Stream(dev) if self.split_prep else None
 
     # ------------------------------------------- current stage / slot views
     def _st(self, stage=None) -> _Stage:
@@ -371,14 +379,20 @@ class TrainStep:
         if self.fused_expand:
             # main stream: dedup, inverse CSR, lookup with the expansion fused
             # through the CSR, unique-row gradients, then the scatter + SGD
-            # after the side stream's occurrence sort
+            # after the side stream's occurrence sort (split_prep: the sort
+            # starts right after the bookkeeping, beside the inverse CSR)
             ms = main.cuda_stream
             self.dedup(ms)
-            self.backward_stages(_lib.BWD_INVERSE, ms)
+            if self.split_prep:
+                self.backward_stages(_lib.BWD_SETUP, ms)
+            else:
+                self.backward_stages(_lib.BWD_INVERSE, ms)
             self._ev_fork.record(main)
             self._side.wait_event(self._ev_fork)
             self.backward_stages(_lib.BWD_OCCURRENCES, self._side.cuda_stream)
             self._ev_join.record(self._side)
+            if self.split_prep:
+                self.backward_stages(_lib.BWD_INVERSE | _lib.BWD_SETUP_DONE, ms)
             self.forward_expand(ms, share=True)
             self.backward_stages(_lib.BWD_GRAD, ms)
             main.wait_event(self._ev_join)
@@ -388,13 +402,24 @@ class TrainStep:
         # expansion, unique-row gradients (after the CSR only, so they run while
         # the sort finishes), then the scatter + SGD after the sort
         self.dedup(main.cuda_stream)
+        if self.split_prep:
+            self.backward_stages(_lib.BWD_SETUP, main.cuda_stream)
         self._ev_fork.record(main)
         self._side.wait_event(self._ev_fork)
         ss = self._side.cuda_stream
-        self.backward_stages(_lib.BWD_INVERSE, ss)
-        self._ev_inv.record(self._side)
-        self.backward_stages(_lib.BWD_OCCURRENCES, ss)
-        self._ev_join.record(self._side)
+        if self.split_prep:
+            # inverse CSR and occurrence sort side by side on two streams
+            # (latency-bound chains on small batches)
+            self._side2.wait_event(self._ev_fork)
+            self.backward_stages(_lib.BWD_INVERSE | _lib.BWD_SETUP_DONE, ss)
+            self._ev_inv.record(self._side)
+            self.backward_stages(_lib.BWD_OCCURRENCES, self._side2.cuda_stream)
+            self._ev_join.record(self._side2)
+        else:
+            self.backward_stages(_lib.BWD_INVERSE, ss)
+            self._ev_inv.record(self._side)
+            self.backward_stages(_lib.BWD_OCCURRENCES, ss)
+            self._ev_join.record(self._side)
         self.forward(main.cuda_stream, share=True)
         self.expand(main.cuda_stream)
         main.wait_event(self._ev_inv)
