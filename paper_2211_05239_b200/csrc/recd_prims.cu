@@ -39,6 +39,9 @@ constexpr uint32_t OS_AGG = 1u << 30, OS_PRE = 2u << 30, OS_CNT = (1u << 30) - 1
 #define RECD_OS_LB 8
 #endif
 constexpr int OS_LB = RECD_OS_LB;
+#ifndef RECD_OS_SETUP_CLEAR  // k_os_setup clears the sort state (no memset nodes)
+#define RECD_OS_SETUP_CLEAR 1
+#endif
 #ifndef RECD_OS_EARLY  // publish a tile's digit counts before its ranking
 #define RECD_OS_EARLY 1
 #endif
@@ -68,6 +71,7 @@ struct OsParams {
   uint32_t* status;    // [2][total_tcap][256]
   uint32_t* tmap;      // [total_tcap] ticket -> (segment << 24) | tile (RECD_OS_IL)
   int il;              // tickets interleaved over the segments (RECD_OS_IL and S > 1)
+  int clear_state;     // k_os_setup zeroes the ticket counters and pass 0's status rows
   const int32_t* gate; // nullable: run only if *gate != 0
 };
 
@@ -162,6 +166,13 @@ __global__ void __launch_bounds__(OS_NT) k_os_setup(const __grid_constant__ OsPa
   RECD_PDL_PROLOGUE();
   if (os_gated_off(p)) return;
   __shared__ int64_t s_scan[32];
+  if (p.clear_state) {  // (instead of two memset nodes before this kernel)
+    if (blockIdx.x == 0 && threadIdx.x < OS_MAXPASS) p.counters[threadIdx.x] = 0u;
+    const int64_t words = p.total_tcap * 256;
+    uint2* st2 = reinterpret_cast<uint2*>(p.status);  // 8-byte aligned (counters + 64 words)
+    for (int64_t i = (int64_t)blockIdx.x * OS_NT + threadIdx.x; i < words / 2; i += (int64_t)gridDim.x * OS_NT)
+      st2[i] = make_uint2(0u, 0u);
+  }
   if (p.il) {
     __shared__ int64_t s_T[OS_MAXSEG], s_p[OS_MAXSEG + 1];
     for (int q = threadIdx.x; q < p.S; q += OS_NT) s_T[q] = ceil_div(*p.seg[q].count, (int64_t)OS_TILE);
@@ -469,8 +480,12 @@ int seg_sort_pairs(const SegDesc* segs, int S, int bits, uint32_t* keys, uint32_
       // the producer of the keys already counted every pass's digits into
       // ghist (sort_hist_clear + its own smem histograms): only the ticket
       // counters and the first pass's tile status words need clearing
-      RECD_CUDA_CHECK(cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * OS_MAXPASS, stream));
-      RECD_CUDA_CHECK(cudaMemsetAsync(p.status, 0, sizeof(uint32_t) * p.total_tcap * 256, stream));
+      if (RECD_OS_SETUP_CLEAR) {
+        p.clear_state = 1;
+      } else {
+        RECD_CUDA_CHECK(cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * OS_MAXPASS, stream));
+        RECD_CUDA_CHECK(cudaMemsetAsync(p.status, 0, sizeof(uint32_t) * p.total_tcap * 256, stream));
+      }
       pdl(k_os_setup, p.S * npass, OS_NT, 0, stream)(p);
       note_launch(1);
     } else {

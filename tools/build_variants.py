@@ -6,6 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_05239_b200.build import build  # noqa: E402
 
 V = {
+    "memset": ["RECD_OS_SETUP_CLEAR=0"],
     "cpilp8": ["RECD_CP_ILP=8"],
     "gu256": ["RECD_GU_CH=256"],
     "os12": ["RECD_OS_ITEMS=12"],
